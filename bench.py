@@ -1,0 +1,321 @@
+"""Benchmark: sliced + grouped + rehash denoising throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Workload (BASELINE.json metric, configs[2] = "SVD-XT-shape"): the toy video
+U-Net of the reference at SD widths (base 320, norm_groups 32), latent
+25 frames x 4 x 72 x 128, random-init weights (seed 0) and a seeded synthetic
+initial latent.  One bench *step* = one complete 25-step denoising run with
+Step Rehash (key-step schedule G from a calibration run during setup,
+|G| = 13 of 25 like the paper's operating point: 13 full evaluations + 12
+tail evaluations + 25 latent updates), replayed as one CUDA graph.
+``value`` = denoising steps per second (25 x K / device time), whole job.
+
+Multi-GPU (torchrun, N > 1): every rank runs its own replica of the workload
+(the frame-sharded path is not used by this line); value = sum over ranks,
+time = max over ranks, "scaling": "weak".
+
+``--impl reference`` times the reference algorithm (oracle port of the numpy
+``sliceflow`` path, fp32, SlicedLoop, capped16) on the host cores with a
+bounded sample per step (first slice of every group, scaled by the slice
+count; one key step + one tail step, extrapolated to the 13/25 schedule).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(channels=4, frames=8, height=32, width=32, base_channels=8, norm_groups=4, steps=10),
+    "c2": dict(channels=4, frames=16, height=64, width=64, base_channels=320, norm_groups=32, steps=25),
+    "c3": dict(channels=4, frames=25, height=72, width=128, base_channels=320, norm_groups=32, steps=25),
+    "c4": dict(channels=4, frames=64, height=72, width=128, base_channels=320, norm_groups=32, steps=25),
+}
+WORKLOAD = {
+    "c1": "toy 8f x 4x32x32, base 8, K=10",
+    "c2": "AnimateDiff-shape 16f x 4x64x64, base 320, K=25",
+    "c3": "SVD-XT-shape 25f x 4x72x128 (576x1024), base 320, K=25",
+    "c4": "stress 64f x 4x72x128, base 320, K=25",
+}
+METRIC = "denoise steps/s (sliced+grouped+rehash, peak HBM/GPU reported)"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def n_target_keys(K: int) -> int:
+    return max(2, math.ceil(K * 13 / 25))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.strip().splitlines() if l.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_reference(args, world, rank):
+    """CPU arm: oracle port timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import threadpoolctl  # noqa: F401  (OpenBLAS thread control is via env)
+    from oracle.cpu_baseline import CpuBaseline, host_cores
+    from paper_2411_01171_b200.unet import UNetConfig
+    cfg = UNetConfig(**CONFIGS[args.config])
+    K = cfg.steps
+    nk = n_target_keys(K)
+    cb = CpuBaseline(cfg)
+    for _ in range(args.warmup):
+        cb.sample()
+    rates, samples = [], []
+    for _ in range(args.steps):
+        smp = cb.sample()
+        samples.append(smp["sample_s"])
+        rates.append(cb.steps_per_s(nk, K, smp))
+    value = float(np.mean(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": K / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "schedule": f"{nk} key + {K - nk} tail steps",
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": host_cores(), "kind": "port",
+                         "sample": "first slice of every group (scaled by slice count) for one key step and one "
+                                   f"tail step, extrapolated to {nk}/{K}; {np.mean(samples):.1f} s CPU per sample"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2411_01171_b200.executor import ExecConfig
+    from paper_2411_01171_b200.harness import Denoiser, initial_latent
+    from paper_2411_01171_b200.profiling import CallProfiler
+    from paper_2411_01171_b200.rehash import gamma_for_target, key_step_search
+    from paper_2411_01171_b200.unet import UNetConfig
+
+    cfg = UNetConfig(**CONFIGS[args.config])
+    K = cfg.steps
+    peaks, peak_src = load_peaks()
+    t_setup = time.perf_counter()
+    den = Denoiser(cfg, ExecConfig(gemm_backend=args.backend, spatial_k=args.spatial_k, temporal_k=args.temporal_k))
+    x0 = initial_latent(cfg)
+    # calibration (setup, untimed): all-key run recording the probe, then A1
+    t_cal = time.perf_counter()
+    _, S = den.calibrate(x0)
+    torch.cuda.synchronize()
+    t_cal = time.perf_counter() - t_cal
+    nk = n_target_keys(K)
+    gamma = args.gamma if args.gamma else gamma_for_target(S, nk)
+    sched = key_step_search(S, gamma, K)
+    den.trace = None
+    torch.cuda.empty_cache()
+    key = den.prepare(sched)
+    launches_per_run = den.launches[key]
+    dev = torch.device("cuda")
+    x0_rows = None
+    den.set_latent(x0)
+    x0_rows = den.plan.latent.clone()
+    setup_s = time.perf_counter() - t_setup
+
+    def one_run():
+        den.plan.latent.copy_(x0_rows)
+        den.launch(key)
+
+    for _ in range(max(args.warmup, 1)):
+        one_run()
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    barrier(world)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        start.record()
+        for _ in range(args.steps):
+            one_run()
+        end.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    dev_ms = max_over_ranks(world, start.elapsed_time(end))
+    peak_hbm = torch.cuda.max_memory_allocated()
+    runs_per_s = args.steps / (dev_ms / 1e3)
+    value = runs_per_s * K * world
+
+    # end to end through the public API: host latent in, host latent out
+    e2e_ms = []
+    for _ in range(args.steps):
+        barrier(world)
+        t0 = time.perf_counter()
+        den.run(x0, sched)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = max_over_ranks(world, float(np.mean(e2e_ms)))
+    e2e_value = K / (e2e_ms / 1e3) * world
+
+    # per-launch device timing of one eager key step + one tail step
+    prof_full, prof_tail = CallProfiler(), CallProfiler()
+    st = torch.cuda.current_stream().cuda_stream
+    with prof_full:
+        den.plan.run_full(st, den.emb_table[0].data_ptr())
+    with prof_tail:
+        den.plan.run_tail(st)
+    pf, pt = prof_full.summary(), prof_tail.summary()
+    gemm_keys = [k for k in pf["by_call"] if k.startswith("sf_gemm")]
+    g_ms = sum(pf["by_call"][k]["ms"] for k in gemm_keys)
+    g_fl = sum(pf["by_call"][k]["flops"] for k in gemm_keys)
+    g_calls = sum(pf["by_call"][k]["calls"] for k in gemm_keys)
+    achieved = g_fl / (g_ms * 1e9) if g_ms else 0.0
+    peak_tf = peaks["bf16_tflops_sustained"]
+    roofline = {"bound": "tensor", "kernel": "+".join(gemm_keys), "achieved": round(achieved, 2), "peak": peak_tf,
+                "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": None,
+                "share_of_step": round(g_ms / pf["total_ms"], 4) if pf["total_ms"] else None,
+                "launches_per_key_step": g_calls, "flops_per_key_step": g_fl,
+                "peak_source": f"{peak_src} bf16_tflops_sustained"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "unet": CONFIGS[args.config],
+                   "bench_step": f"one {K}-step rehash denoising run ({len(sched.key_steps)} key + "
+                                 f"{K - len(sched.key_steps)} tail evaluations), one CUDA graph",
+                   "schedule": {"key_steps": sched.key_steps, "gamma": gamma, "decision_margin": sched.margin},
+                   "l2": "activations exceed L2 (no flush needed)" if args.config != "c1" else "toy fits L2",
+                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+        "peak_hbm_bytes": int(peak_hbm), "arena_bytes": den.plan.arena_bytes,
+        "scratch_bytes": den.plan.scratch_bytes,
+        "frames_per_s": round(value / K * cfg.frames, 3),
+        "clocks": clk.summary(),
+        "e2e": {"value": round(e2e_value, 3), "unit": "steps/s",
+                "h2d_bytes_per_step": int(x0.nbytes), "d2h_bytes_per_step": int(x0.nbytes)},
+        "gpu_launches": launches_per_run * args.steps,
+        "roofline": roofline,
+        "profile": {"key_step_ms": round(pf["total_ms"], 3), "tail_step_ms": round(pt["total_ms"], 3),
+                    "top": {k: {"ms": round(v["ms"], 3), "calls": v["calls"], "share": round(v["share"], 3),
+                                "tflops": round(v["tflops"], 1)} for k, v in list(pf["by_call"].items())[:8]}},
+        "setup_s": round(setup_s, 2), "calibration_s": round(t_cal, 2),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle.cpu_baseline import CpuBaseline, host_cores
+        cb = CpuBaseline(cfg)
+        smp = cb.sample()
+        line["cpu_baseline"] = {
+            "value": round(cb.steps_per_s(len(sched.key_steps), K, smp), 6), "unit": "steps/s",
+            "cores": host_cores(), "kind": "port",
+            "sample": f"oracle fp32 SlicedLoop: first slice of every group scaled by slice count, one key + one "
+                      f"tail step extrapolated to {len(sched.key_steps)}/{K}; {smp['sample_s']:.1f} s CPU"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--backend", type=int, default=0)
+    ap.add_argument("--gamma", type=float, default=None)
+    ap.add_argument("--spatial-k", type=int, default=None)
+    ap.add_argument("--temporal-k", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

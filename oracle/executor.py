@@ -17,6 +17,8 @@ order -- the Step Rehash tail (``SPEC.md:425``, survey Appendix A).
 
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 from paper_2411_01171_b200.grouping import GroupedGraph, group_output_shape
@@ -41,7 +43,8 @@ def run_group_sliced(group, x, weights, max_slices=None):
     """Slice, run the chain per slice, reassemble (grouping.py:223-254)."""
     shape = Shape5(*x.shape)
     out_shape = group_output_shape(group, shape)
-    out = np.empty(tuple(out_shape), dtype=x.dtype)
+    # zeros, not empty: a sampled run (max_slices) leaves the other slices unwritten
+    out = np.zeros(tuple(out_shape), dtype=x.dtype)
     regions = plan_regions(shape, group.plan)
     if max_slices is not None:
         regions = regions[:max_slices]
@@ -65,8 +68,12 @@ def units_for(graph, grouped: GroupedGraph | None, mode: ExecMode):
 
 
 def evaluate(graph, weights, feeds, mode=ExecMode.REFERENCE, grouped=None, start_after=None,
-             capture=(), max_slices=None):
-    """One network evaluation; returns (output, {label: captured array})."""
+             capture=(), max_slices=None, timing=None):
+    """One network evaluation; returns (output, {label: captured array}).
+
+    ``max_slices`` runs only the first slices of every group (a bounded CPU
+    timing sample); ``timing`` (a list) receives (unit, sample_s, extrapolated_s).
+    """
     mode = ExecMode(mode)
     topo = graph.topo_order()
     pos = {n: i for i, n in enumerate(topo)}
@@ -77,7 +84,9 @@ def evaluate(graph, weights, feeds, mode=ExecMode.REFERENCE, grouped=None, start
         units = [u for u in units
                  if pos[u[1] if u[0] == "node" else grouped.groups[u[1]].ops[0].id] > cut]
     captured = {}
+    timings = [] if timing is not None else None
     for kind, ref in units:
+        t0 = time.perf_counter()
         if kind == "node":
             n = graph.nodes[ref]
             vals[ref] = K.apply_kernel(n.kind, [vals[r] for r in n.inputs], _params(weights, n), n.attrs)
@@ -86,8 +95,17 @@ def evaluate(graph, weights, feeds, mode=ExecMode.REFERENCE, grouped=None, start
             g = grouped.groups[ref]
             vals[g.tail] = run_group_sliced(g, vals[g.head_input], weights, max_slices)
             done = [g.tail]
+        if timings is not None:
+            dt = time.perf_counter() - t0
+            scale = 1.0
+            if kind == "group" and max_slices is not None:
+                n = grouped.groups[ref].plan.n_slices
+                scale = n / min(n, max_slices)
+            timings.append((ref if kind == "node" else grouped.groups[ref].label, dt, dt * scale))
         for d in done:
             lbl = graph.nodes[d].label
             if lbl in capture:
                 captured[lbl] = vals[d]
+    if timing is not None:
+        timing.extend(timings)
     return vals[graph.outputs[0]], captured

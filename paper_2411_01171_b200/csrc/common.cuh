@@ -1,0 +1,97 @@
+// Shared helpers for the sm_100a kernels of sliceflow_b200.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/sliceflow_b200.h"
+
+namespace sf {
+
+typedef __nv_bfloat16 bf16;
+typedef __nv_bfloat162 bf162;
+
+// thread-local last error text (sf_last_error)
+void set_error(const std::string& msg);
+
+#define SF_CHECK_ARG(cond, code, msg)                   \
+  do {                                                  \
+    if (!(cond)) {                                      \
+      ::sf::set_error(std::string(__func__) + ": " + (msg)); \
+      return (code);                                    \
+    }                                                   \
+  } while (0)
+
+inline sf_status launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return SF_ERR_CUDA;
+  }
+  return SF_OK;
+}
+
+// Row (o, i) of a two-level view.
+template <typename T>
+__device__ __forceinline__ T* row_ptr(const sf_view_t& v, int64_t o, int64_t i) {
+  return reinterpret_cast<T*>(v.ptr) + (o * v.ostride + i) * v.ld;
+}
+
+__device__ __forceinline__ float silu_f(float x) {
+  // x * sigmoid(x) without exponentiating a positive argument (kernels.py:247-253)
+  float e = __expf(-fabsf(x));
+  float s = x >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+  return x * s;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, m));
+  return v;
+}
+
+// 8 x bf16 <-> 8 x float through one 16-byte access
+struct alignas(16) bf16x8 {
+  bf162 h[4];
+};
+__device__ __forceinline__ void unpack8(const bf16x8& v, float* f) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 t = __bfloat1622float2(v.h[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+__device__ __forceinline__ bf16x8 pack8(const float* f) {
+  bf16x8 v;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v.h[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+  return v;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+inline bool view_vec8_ok(const sf_view_t& v) { return aligned16(v.ptr) && (v.ld % 8) == 0; }
+
+inline int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (!n) n = 148;
+  }
+  return n;
+}
+
+}  // namespace sf

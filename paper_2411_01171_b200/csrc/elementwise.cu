@@ -1,0 +1,823 @@
+// HBM-bound kernels of the sliceflow path: norms, SiLU, add, resampling,
+// copies, softmax rows, latent-edge convolutions, similarity dot products.
+//
+// All bf16 activation kernels move 16-byte vectors (8 channels) and require
+// C % 8 == 0 and 16-byte aligned rows; reductions are fixed-order (no float
+// atomics) so results are bit-reproducible run to run.
+#include "common.cuh"
+
+#include <cmath>
+#include <mutex>
+
+namespace sf {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+// ---------------------------------------------------------------------------
+// GroupNorm (kernels.py:228-237)
+// ---------------------------------------------------------------------------
+
+static int gn_splits(int frames, int n_inner) {
+  int want = (4 * num_sms() + frames - 1) / frames;      // >= ~4 CTAs per SM overall
+  int most = (n_inner + 127) / 128;                      // >= 128 rows per CTA
+  int s = want < most ? want : most;
+  return s < 1 ? 1 : s;
+}
+
+// partial[frame][split][c] = (sum x, sum x^2) over the split's rows, fp64
+__global__ void gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits, double2* partial) {
+  const int frame = blockIdx.x / splits, split = blockIdx.x % splits;
+  const int nvec = C / 8;
+  const int rows_per_iter = blockDim.x / nvec > 0 ? blockDim.x / nvec : 1;
+  const int chunk = (n_inner + splits - 1) / splits;
+  const int r0 = split * chunk, r1 = min(n_inner, r0 + chunk);
+  extern __shared__ double2 red[];  // [rows_per_iter][C] when nvec <= blockDim
+  const int lane_v = nvec <= (int)blockDim.x ? (int)threadIdx.x % nvec : (int)threadIdx.x;
+  const int lane_r = nvec <= (int)blockDim.x ? (int)threadIdx.x / nvec : 0;
+  const bool active = nvec <= (int)blockDim.x ? lane_r < rows_per_iter : true;
+  for (int vbase = lane_v; vbase < nvec; vbase += (nvec <= (int)blockDim.x ? nvec : blockDim.x)) {
+    double s[8], q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.0;
+    if (active) {
+      for (int r = r0 + lane_r; r < r1; r += rows_per_iter) {
+        bf16x8 v = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r) + vbase * 8);
+        float f[8];
+        unpack8(v, f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s[j] += f[j];
+          q[j] += (double)f[j] * f[j];
+        }
+      }
+    }
+    if (nvec <= (int)blockDim.x) {
+      if (active) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) red[lane_r * C + vbase * 8 + j] = make_double2(s[j], q[j]);
+      }
+      __syncthreads();
+      if (lane_r == 0) {
+        for (int j = 0; j < 8; ++j) {
+          double ss = 0, qq = 0;
+          for (int rr = 0; rr < rows_per_iter; ++rr) {
+            double2 t = red[rr * C + vbase * 8 + j];
+            ss += t.x;
+            qq += t.y;
+          }
+          partial[((int64_t)frame * splits + split) * C + vbase * 8 + j] = make_double2(ss, qq);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        partial[((int64_t)frame * splits + split) * C + vbase * 8 + j] = make_double2(s[j], q[j]);
+    }
+  }
+}
+
+// one warp per (frame, group): combine splits x channels in fixed order
+__global__ void gn_finalize_kernel(const double2* partial, int frames, int splits, int C, int groups,
+                                   int64_t count, float eps, float* mean, float* rstd) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= frames * groups) return;
+  const int frame = warp / groups, g = warp % groups, cg = C / groups;
+  double s = 0, q = 0;
+  for (int idx = lane; idx < splits * cg; idx += 32) {
+    int sp = idx / cg, c = g * cg + idx % cg;
+    double2 t = partial[((int64_t)frame * splits + sp) * C + c];
+    s += t.x;
+    q += t.y;
+  }
+  s = warp_sum_d(s);
+  q = warp_sum_d(q);
+  if (lane == 0) {
+    double mu = s / (double)count;
+    double var = q / (double)count - mu * mu;
+    if (var < 0) var = 0;
+    mean[warp] = (float)mu;
+    rstd[warp] = (float)(1.0 / sqrt(var + (double)eps));
+  }
+}
+
+__global__ void gn_apply_kernel(sf_view_t x, sf_view_t y, int frames, int n_inner, int C, int groups,
+                                const float* __restrict__ mean, const float* __restrict__ rstd,
+                                const float* __restrict__ gamma, const float* __restrict__ beta, int act) {
+  const int nvec = C / 8, cg = C / groups;
+  const int64_t total = (int64_t)frames * n_inner * nvec;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int v = idx % nvec;
+    int64_t row = idx / nvec;
+    int frame = row / n_inner, r = row % n_inner;
+    bf16x8 in = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r) + v * 8);
+    float f[8];
+    unpack8(in, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int c = v * 8 + j, g = c / cg;
+      float m = mean[frame * groups + g], s = rstd[frame * groups + g];
+      float t = (f[j] - m) * s * gamma[c] + beta[c];
+      f[j] = act ? silu_f(t) : t;
+    }
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, frame, r) + v * 8) = pack8(f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm over channels (kernels.py:240-244): one warp per row, two-pass
+// from registers (mean, then mean of squared deviations), like the reference.
+// ---------------------------------------------------------------------------
+template <int VPL>
+__global__ void layer_norm_kernel(sf_view_t x, sf_view_t y, int n_outer, int n_inner, int C,
+                                  const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                                  int act) {
+  const int64_t rows = (int64_t)n_outer * n_inner;
+  const int lane = threadIdx.x & 31;
+  const int nvec = C / 8;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int o = row / n_inner, i = row % n_inner;
+    const bf16* src = row_ptr<const bf16>(x, o, i);
+    float f[VPL][8];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      int v = lane + 32 * k;
+      if (v < nvec) {
+        unpack8(*reinterpret_cast<const bf16x8*>(src + v * 8), f[k]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += f[k][j];
+      }
+    }
+    const float mu = warp_sum(s) / C;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      int v = lane + 32 * k;
+      if (v < nvec) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float d = f[k][j] - mu;
+          q += d * d;
+        }
+      }
+    }
+    const float rs = rsqrtf(warp_sum(q) / C + eps);
+    bf16* dst = row_ptr<bf16>(y, o, i);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      int v = lane + 32 * k;
+      if (v < nvec) {
+        float g[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          int c = v * 8 + j;
+          float t = (f[k][j] - mu) * rs * gamma[c] + beta[c];
+          g[j] = act ? silu_f(t) : t;
+        }
+        *reinterpret_cast<bf16x8*>(dst + v * 8) = pack8(g);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise on row views
+// ---------------------------------------------------------------------------
+enum { EW_SILU = 0, EW_ADD = 1, EW_COPY = 2 };
+
+template <int OP>
+__global__ void rows_ew_kernel(sf_view_t a, sf_view_t b, sf_view_t y, int n_outer, int n_inner, int C,
+                               int b_bcast) {
+  const int nvec = C / 8;
+  const int64_t total = (int64_t)n_outer * n_inner * nvec;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int v = idx % nvec;
+    int64_t row = idx / nvec;
+    int o = row / n_inner, i = row % n_inner;
+    bf16x8 va = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(a, o, i) + v * 8);
+    if (OP == EW_COPY) {
+      *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, o, i) + v * 8) = va;
+      continue;
+    }
+    float f[8];
+    unpack8(va, f);
+    if (OP == EW_SILU) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] = silu_f(f[j]);
+    } else {
+      float g[8];
+      unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(b, o, b_bcast ? 0 : i) + v * 8), g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += g[j];
+    }
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, o, i) + v * 8) = pack8(f);
+  }
+}
+
+__global__ void copy_rows_scalar_kernel(sf_view_t x, sf_view_t y, int n_outer, int n_inner, int C) {
+  const int64_t total = (int64_t)n_outer * n_inner * C;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int c = idx % C;
+    int64_t row = idx / C;
+    int o = row / n_inner, i = row % n_inner;
+    row_ptr<bf16>(y, o, i)[c] = row_ptr<const bf16>(x, o, i)[c];
+  }
+}
+
+__global__ void downsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int W, int C) {
+  const int nvec = C / 8, Ho = H / 2, Wo = W / 2;
+  const int64_t total = (int64_t)frames * Ho * Wo * nvec;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int v = idx % nvec;
+    int64_t p = idx / nvec;
+    int xo = p % Wo, yo = (p / Wo) % Ho, f = p / ((int64_t)Wo * Ho);
+    float a[8], b[8], c[8], d[8], r[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yo) * W + 2 * xo) + v * 8), a);
+    unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yo) * W + 2 * xo + 1) + v * 8), b);
+    unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yo + 1) * W + 2 * xo) + v * 8), c);
+    unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yo + 1) * W + 2 * xo + 1) + v * 8), d);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (((a[j] + b[j]) + c[j]) + d[j]) * 0.25f;
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, yo * Wo + xo) + v * 8) = pack8(r);
+  }
+}
+
+__global__ void upsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int W, int C) {
+  const int nvec = C / 8, Ho = 2 * H, Wo = 2 * W;
+  const int64_t total = (int64_t)frames * Ho * Wo * nvec;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int v = idx % nvec;
+    int64_t p = idx / nvec;
+    int xo = p % Wo, yo = (p / Wo) % Ho, f = p / ((int64_t)Wo * Ho);
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, yo * Wo + xo) + v * 8) =
+        *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (yo / 2) * W + xo / 2) + v * 8);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// softmax rows: fp32 scores -> bf16 probabilities (kernels.py:272-276)
+// ---------------------------------------------------------------------------
+template <int PER>
+__global__ void softmax_rows_kernel(const float* __restrict__ s, int64_t lds, bf16* __restrict__ p, int64_t ldp,
+                                    int n) {
+  const int64_t row = blockIdx.x;
+  const float* src = s + row * lds;
+  float v[PER];
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    int c = threadIdx.x + k * blockDim.x;
+    v[k] = c < n ? src[c] : -INFINITY;
+    m = fmaxf(m, v[k]);
+  }
+  __shared__ float red[32];
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : -INFINITY;
+    t = warp_max(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  m = red[0];
+  __syncthreads();
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    int c = threadIdx.x + k * blockDim.x;
+    v[k] = c < n ? __expf(v[k] - m) : 0.f;
+    sum += v[k];
+  }
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = 1.f / red[0];
+  bf16* dst = p + row * ldp;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    int c = threadIdx.x + k * blockDim.x;
+    if (c < n) dst[c] = __float2bfloat16(v[k] * inv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// temporal attention core: one CTA per pixel, T <= 64 tokens of width C.
+// S = q k^T * scale (fp32 in smem), softmax, O = P v  (kernels.py:269-308)
+// ---------------------------------------------------------------------------
+constexpr int TA_MAXT = 64;
+constexpr int TA_CHUNK = 32;
+__global__ void __launch_bounds__(256) temporal_attn_kernel(sf_view_t qkv, int koff, int voff, sf_view_t out,
+                                                            int T, int n_inner, int C, float scale) {
+  const int pix = blockIdx.x % n_inner, b = blockIdx.x / n_inner;
+  __shared__ float S[TA_MAXT][TA_MAXT + 1];
+  __shared__ float qs[TA_MAXT][TA_CHUNK + 1];
+  __shared__ float ks[TA_MAXT][TA_CHUNK + 1];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int TT = T * T;
+  float acc[TA_MAXT * TA_MAXT / 256];
+#pragma unroll
+  for (int k = 0; k < TA_MAXT * TA_MAXT / 256; ++k) acc[k] = 0.f;
+  for (int c0 = 0; c0 < C; c0 += TA_CHUNK) {
+    for (int idx = tid; idx < T * TA_CHUNK; idx += nth) {
+      int t = idx / TA_CHUNK, c = idx % TA_CHUNK;
+      const bf16* r = row_ptr<const bf16>(qkv, (int64_t)b * T + t, pix);
+      bool ok = c0 + c < C;
+      qs[t][c] = ok ? __bfloat162float(r[c0 + c]) : 0.f;
+      ks[t][c] = ok ? __bfloat162float(r[koff + c0 + c]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < TA_MAXT * TA_MAXT / 256; ++k) {
+      int e = tid + k * 256;
+      if (e < TT) {
+        int i = e / T, j = e % T;
+        float a = 0.f;
+#pragma unroll 8
+        for (int c = 0; c < TA_CHUNK; ++c) a += qs[i][c] * ks[j][c];
+        acc[k] += a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < TA_MAXT * TA_MAXT / 256; ++k) {
+    int e = tid + k * 256;
+    if (e < TT) S[e / T][e % T] = acc[k] * scale;
+  }
+  __syncthreads();
+  // softmax: one warp per row
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int i = warp; i < T; i += nth / 32) {
+    float a = lane < T ? S[i][lane] : -INFINITY;
+    float bb = lane + 32 < T ? S[i][lane + 32] : -INFINITY;
+    float m = warp_max(fmaxf(a, bb));
+    a = lane < T ? __expf(a - m) : 0.f;
+    bb = lane + 32 < T ? __expf(bb - m) : 0.f;
+    float inv = 1.f / warp_sum(a + bb);
+    if (lane < T) S[i][lane] = a * inv;
+    if (lane + 32 < T) S[i][lane + 32] = bb * inv;
+  }
+  __syncthreads();
+  // O = P v, chunked over channels (reuse qs as the v chunk)
+  for (int c0 = 0; c0 < C; c0 += TA_CHUNK) {
+    for (int idx = tid; idx < T * TA_CHUNK; idx += nth) {
+      int t = idx / TA_CHUNK, c = idx % TA_CHUNK;
+      const bf16* r = row_ptr<const bf16>(qkv, (int64_t)b * T + t, pix);
+      qs[t][c] = c0 + c < C ? __bfloat162float(r[voff + c0 + c]) : 0.f;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < T * TA_CHUNK; idx += nth) {
+      int t = idx / TA_CHUNK, c = idx % TA_CHUNK;
+      if (c0 + c < C) {
+        float a = 0.f;
+        for (int j = 0; j < T; ++j) a += S[t][j] * qs[j][c];
+        row_ptr<bf16>(out, (int64_t)b * T + t, pix)[c0 + c] = __float2bfloat16(a);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// latent-edge convolutions with tiny channel counts (in_conv / out_conv)
+// ---------------------------------------------------------------------------
+// in_conv: cin <= 16, fp32 input; one thread per (pixel, 8 output channels)
+__global__ void conv_smallcin_kernel(const float* __restrict__ x, int frames, int H, int W, int cin,
+                                     const float* __restrict__ w, const float* __restrict__ bias, int cout,
+                                     sf_view_t y) {
+  const int nvec = cout / 8;
+  const int64_t total = (int64_t)frames * H * W * nvec;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int v = idx % nvec;
+    int64_t p = idx / nvec;
+    int px = p % W, py = (p / W) % H, f = p / ((int64_t)W * H);
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int dy = 0; dy < 3; ++dy) {
+      int yy = py + dy - 1;
+      if (yy < 0 || yy >= H) continue;
+      for (int dx = 0; dx < 3; ++dx) {
+        int xx = px + dx - 1;
+        if (xx < 0 || xx >= W) continue;
+        const float* src = x + (((int64_t)f * H + yy) * W + xx) * cin;
+        for (int ci = 0; ci < cin; ++ci) {
+          float a = src[ci];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += a * w[(((int64_t)(v * 8 + j) * cin + ci) * 3 + dy) * 3 + dx];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += bias[v * 8 + j];
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, (int64_t)py * W + px) + v * 8) = pack8(acc);
+  }
+}
+
+// out_conv: small cout; one warp per pixel, lanes stride over (tap, channel vector)
+template <int MAXCO>
+__global__ void conv_smallcout_kernel(sf_view_t x, int frames, int H, int W, int cin,
+                                      const float* __restrict__ wt /*[9][cin][cout]*/,
+                                      const float* __restrict__ bias, int cout, float* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t npix = (int64_t)frames * H * W;
+  const int nvec = cin / 8;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < npix;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int px = p % W, py = (p / W) % H, f = p / ((int64_t)W * H);
+    float acc[MAXCO];
+#pragma unroll
+    for (int j = 0; j < MAXCO; ++j) acc[j] = 0.f;
+    for (int e = lane; e < 9 * nvec; e += 32) {
+      int tap = e / nvec, v = e % nvec;
+      int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+      if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+      float a[8];
+      unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (int64_t)yy * W + xx) + v * 8), a);
+      const float* wr = wt + ((int64_t)tap * cin + v * 8) * cout;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int co = 0; co < MAXCO; ++co)
+          if (co < cout) acc[co] += a[j] * wr[j * cout + co];
+    }
+#pragma unroll
+    for (int co = 0; co < MAXCO; ++co) acc[co] = warp_sum(acc[co]);
+    if (lane == 0)
+      for (int co = 0; co < cout; ++co) y[p * cout + co] = acc[co] + bias[co];
+  }
+}
+
+__global__ void gemv_kernel(const float* __restrict__ Wm, const float* __restrict__ e, const float* __restrict__ b,
+                            float* __restrict__ y, int N, int K) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  float a = 0.f;
+  for (int k = lane; k < K; k += 32) a += Wm[(int64_t)warp * K + k] * e[k];
+  a = warp_sum(a);
+  if (lane == 0) y[warp] = a + (b ? b[warp] : 0.f);
+}
+
+__global__ void transpose_f32_kernel(const float* __restrict__ x, float* __restrict__ y, int frames, int A, int B,
+                                     int to_rows) {
+  // to_rows: x[f][A=C][B=HW] -> y[f][HW][C];  else x[f][A=HW][B=C] -> y[f][C][HW]
+  const int64_t total = (int64_t)frames * A * B;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t f = idx / ((int64_t)A * B);
+    int r = idx % ((int64_t)A * B);
+    int a = r / B, bb = r % B;
+    y[f * A * B + (int64_t)bb * A + a] = x[idx];
+  }
+}
+
+__global__ void axpy_kernel(float* __restrict__ x, const float* __restrict__ e, float alpha, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = x[i] - alpha * e[i];
+}
+
+// ---------------------------------------------------------------------------
+// similarity: fixed-order fp64 partials, then one block combines
+// ---------------------------------------------------------------------------
+constexpr int DOT_BLOCKS = 592, DOT_THREADS = 256;
+
+__global__ void dot3_partial_kernel(const bf16* __restrict__ a, const bf16* __restrict__ b, int64_t n,
+                                    double* __restrict__ part) {
+  double aa = 0, bb = 0, ab = 0;
+  const int64_t nv = n / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    float fa[8], fb[8];
+    unpack8(reinterpret_cast<const bf16x8*>(a)[i], fa);
+    unpack8(reinterpret_cast<const bf16x8*>(b)[i], fb);
+    float sa = 0, sb = 0, sab = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sa += fa[j] * fa[j];
+      sb += fb[j] * fb[j];
+      sab += fa[j] * fb[j];
+    }
+    aa += sa;
+    bb += sb;
+    ab += sab;
+  }
+  for (int64_t i = nv * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double x = __bfloat162float(a[i]), y = __bfloat162float(b[i]);
+    aa += x * x;
+    bb += y * y;
+    ab += x * y;
+  }
+  __shared__ double red[3][DOT_THREADS / 32];
+  aa = warp_sum_d(aa);
+  bb = warp_sum_d(bb);
+  ab = warp_sum_d(ab);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = aa;
+    red[1][threadIdx.x >> 5] = bb;
+    red[2][threadIdx.x >> 5] = ab;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0;
+    for (int w = 0; w < DOT_THREADS / 32; ++w) s += red[threadIdx.x][w];
+    part[blockIdx.x * 3 + threadIdx.x] = s;
+  }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int nparts, int width, double* __restrict__ out) {
+  // out[j] = sum_p part[p*width + j], fixed order
+  for (int j = threadIdx.x; j < width; j += blockDim.x) {
+    double s = 0;
+    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * width + j];
+    out[j] = s;
+  }
+}
+
+// Gram: each block covers a slice of the element range for every (i<=j) pair
+constexpr int GRAM_BLOCKS = 296;
+__global__ void gram_partial_kernel(const bf16* const* __restrict__ probes, int K, int64_t n,
+                                    double* __restrict__ part) {
+  const int npairs = K * (K + 1) / 2;
+  const int64_t nv = n / 8;
+  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
+  const int64_t v0 = blockIdx.x * per, v1 = min(nv, v0 + per);
+  __shared__ double red[DOT_THREADS / 32];
+  for (int pr = 0; pr < npairs; ++pr) {
+    int i = 0, rem = pr;
+    while (rem >= K - i) {
+      rem -= K - i;
+      ++i;
+    }
+    int j = i + rem;
+    double acc = 0;
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+      float fa[8], fb[8];
+      unpack8(reinterpret_cast<const bf16x8*>(probes[i])[v], fa);
+      unpack8(reinterpret_cast<const bf16x8*>(probes[j])[v], fb);
+      float s = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += fa[k] * fb[k];
+      acc += s;
+    }
+    if (blockIdx.x == 0)
+      for (int64_t e = nv * 8 + threadIdx.x; e < n; e += blockDim.x)
+        acc += (double)__bfloat162float(probes[i][e]) * __bfloat162float(probes[j][e]);
+    acc = warp_sum_d(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0;
+      for (int w = 0; w < DOT_THREADS / 32; ++w) s += red[w];
+      part[(int64_t)blockIdx.x * npairs + pr] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void gram_finalize_kernel(const double* __restrict__ sums, int K, double* __restrict__ out) {
+  int pr = 0;
+  for (int i = 0; i < K; ++i)
+    for (int j = i; j < K; ++j, ++pr)
+      if (threadIdx.x == 0) {
+        out[i * K + j] = sums[pr];
+        out[j * K + i] = sums[pr];
+      }
+}
+
+static int ew_grid(int64_t total, int threads) {
+  int64_t g = (total + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* sf_last_error(void) { return g_err.c_str(); }
+int32_t sf_version(void) { return 1; }
+
+int64_t sf_group_norm_workspace(int32_t frames, int32_t n_inner, int32_t C) {
+  return (int64_t)frames * gn_splits(frames, n_inner) * C * (int64_t)sizeof(double2);
+}
+
+sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups, float eps,
+                              void* work, float* mean, float* rstd, void* stream) {
+  SF_CHECK_ARG(frames >= 1 && n_inner >= 1 && C >= 8 && C % 8 == 0, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
+  SF_CHECK_ARG(view_vec8_ok(x) && work && mean && rstd, SF_ERR_PARAM, "unaligned view or null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  int splits = gn_splits(frames, n_inner);
+  int nvec = C / 8;
+  int threads = nvec <= 256 ? (256 / nvec) * nvec : 256;
+  size_t smem = nvec <= 256 ? (size_t)(256 / nvec) * C * sizeof(double2) : 0;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(gn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  gn_partial_kernel<<<frames * splits, threads, smem, st>>>(x, n_inner, C, splits, (double2*)work);
+  int warps = frames * groups;
+  gn_finalize_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>((const double2*)work, frames, splits, C, groups,
+                                                                (int64_t)n_inner * (C / groups), eps, mean, rstd);
+  return launch_status("sf_group_norm_stats");
+}
+
+sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
+                              const float* mean, const float* rstd, const float* gamma, const float* beta,
+                              int32_t act, void* stream) {
+  SF_CHECK_ARG(frames >= 1 && n_inner >= 1 && C % 8 == 0, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
+  SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
+  int64_t total = (int64_t)frames * n_inner * (C / 8);
+  gn_apply_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, n_inner, C, groups, mean,
+                                                                          rstd, gamma, beta, act);
+  return launch_status("sf_group_norm_apply");
+}
+
+sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C, const float* gamma,
+                        const float* beta, float eps, int32_t act, void* stream) {
+  SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0 && C <= 32 * 8 * 12, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
+  int64_t rows = (int64_t)n_outer * n_inner;
+  int grid = ew_grid(rows * 32, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  int vpl = (C / 8 + 31) / 32;
+  if (vpl <= 1)
+    layer_norm_kernel<1><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
+  else if (vpl <= 2)
+    layer_norm_kernel<2><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
+  else if (vpl <= 4)
+    layer_norm_kernel<4><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
+  else if (vpl <= 8)
+    layer_norm_kernel<8><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
+  else
+    layer_norm_kernel<12><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
+  return launch_status("sf_layer_norm");
+}
+
+sf_status sf_silu(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C, void* stream) {
+  SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
+  int64_t total = (int64_t)n_outer * n_inner * (C / 8);
+  rows_ew_kernel<EW_SILU><<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, x, y, n_outer, n_inner, C, 0);
+  return launch_status("sf_silu");
+}
+
+sf_status sf_add(sf_view_t a, sf_view_t b, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C,
+                 int32_t b_broadcast_inner, void* stream) {
+  SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(view_vec8_ok(a) && view_vec8_ok(b) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
+  int64_t total = (int64_t)n_outer * n_inner * (C / 8);
+  rows_ew_kernel<EW_ADD><<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(a, b, y, n_outer, n_inner, C,
+                                                                                 b_broadcast_inner);
+  return launch_status("sf_add");
+}
+
+sf_status sf_copy_rows(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C, void* stream) {
+  SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C >= 1, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(x.ptr && y.ptr, SF_ERR_PARAM, "null view");
+  if (C % 8 || !view_vec8_ok(x) || !view_vec8_ok(y)) {  // odd channel ranges: element copy
+    int64_t total = (int64_t)n_outer * n_inner * C;
+    copy_rows_scalar_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, n_outer, n_inner, C);
+    return launch_status("sf_copy_rows");
+  }
+  int64_t total = (int64_t)n_outer * n_inner * (C / 8);
+  rows_ew_kernel<EW_COPY><<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, x, y, n_outer, n_inner, C, 0);
+  return launch_status("sf_copy_rows");
+}
+
+sf_status sf_downsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, void* stream) {
+  SF_CHECK_ARG(H % 2 == 0 && W % 2 == 0, SF_ERR_SHAPE, "downsample2x needs even h, w");
+  SF_CHECK_ARG(frames >= 1 && C % 8 == 0 && view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "bad view");
+  int64_t total = (int64_t)frames * (H / 2) * (W / 2) * (C / 8);
+  downsample_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, H, W, C);
+  return launch_status("sf_downsample2x");
+}
+
+sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, void* stream) {
+  SF_CHECK_ARG(frames >= 1 && C % 8 == 0 && view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "bad view");
+  int64_t total = (int64_t)frames * (2 * H) * (2 * W) * (C / 8);
+  upsample_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, H, W, C);
+  return launch_status("sf_upsample2x");
+}
+
+sf_status sf_softmax_rows(const float* s, int64_t lds, void* p, int64_t ldp, int64_t rows, int32_t n, void* stream) {
+  SF_CHECK_ARG(rows >= 1 && n >= 1 && n <= 256 * 64, SF_ERR_SHAPE, "row length outside [1, 16384]");
+  cudaStream_t st = (cudaStream_t)stream;
+  int per = (n + 255) / 256;
+  bf16* P = (bf16*)p;
+#define SF_SM(K) softmax_rows_kernel<K><<<(unsigned)rows, 256, 0, st>>>(s, lds, P, ldp, n)
+  if (per <= 1) SF_SM(1);
+  else if (per <= 2) SF_SM(2);
+  else if (per <= 4) SF_SM(4);
+  else if (per <= 8) SF_SM(8);
+  else if (per <= 16) SF_SM(16);
+  else if (per <= 36) SF_SM(36);
+  else SF_SM(64);
+#undef SF_SM
+  return launch_status("sf_softmax_rows");
+}
+
+sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, sf_view_t out, int32_t B, int32_t T,
+                                     int32_t n_inner, int32_t C, float scale, void* stream) {
+  SF_CHECK_ARG(T >= 1 && T <= TA_MAXT, SF_ERR_SHAPE, "temporal attention supports 1 <= T <= 64");
+  SF_CHECK_ARG(B >= 1 && n_inner >= 1 && C >= 1, SF_ERR_SHAPE, "bad extents");
+  temporal_attn_kernel<<<B * n_inner, 256, 0, (cudaStream_t)stream>>>(qkv, koff, voff, out, T, n_inner, C, scale);
+  return launch_status("sf_temporal_attention_core");
+}
+
+sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t W, int32_t cin, const float* w,
+                              const float* bias, int32_t cout, sf_view_t y, void* stream) {
+  SF_CHECK_ARG(cin >= 1 && cin <= 64 && cout % 8 == 0, SF_ERR_SHAPE, "need cin <= 64 and cout % 8 == 0");
+  SF_CHECK_ARG(view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
+  int64_t total = (int64_t)frames * H * W * (cout / 8);
+  conv_smallcin_kernel<<<ew_grid(total, 128), 128, 0, (cudaStream_t)stream>>>(x, frames, H, W, cin, w, bias, cout, y);
+  return launch_status("sf_conv3x3_smallcin");
+}
+
+sf_status sf_conv3x3_smallcout(sf_view_t x, int32_t frames, int32_t H, int32_t W, int32_t cin, const float* wt,
+                               const float* bias, int32_t cout, float* y, void* stream) {
+  SF_CHECK_ARG(cout >= 1 && cout <= 16 && cin % 8 == 0, SF_ERR_SHAPE, "need cout <= 16 and cin % 8 == 0");
+  SF_CHECK_ARG(view_vec8_ok(x), SF_ERR_PARAM, "unaligned view");
+  int64_t npix = (int64_t)frames * H * W;
+  cudaStream_t st = (cudaStream_t)stream;
+  int grid = ew_grid(npix * 32, 256);
+  if (cout <= 4)
+    conv_smallcout_kernel<4><<<grid, 256, 0, st>>>(x, frames, H, W, cin, wt, bias, cout, y);
+  else if (cout <= 8)
+    conv_smallcout_kernel<8><<<grid, 256, 0, st>>>(x, frames, H, W, cin, wt, bias, cout, y);
+  else
+    conv_smallcout_kernel<16><<<grid, 256, 0, st>>>(x, frames, H, W, cin, wt, bias, cout, y);
+  return launch_status("sf_conv3x3_smallcout");
+}
+
+sf_status sf_gemv_f32(const float* W, const float* e, const float* b, float* y, int32_t N, int32_t K, void* stream) {
+  SF_CHECK_ARG(N >= 1 && K >= 1, SF_ERR_SHAPE, "bad extents");
+  gemv_kernel<<<(N * 32 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(W, e, b, y, N, K);
+  return launch_status("sf_gemv_f32");
+}
+
+sf_status sf_bcthw_to_rows_f32(const float* x, float* y, int32_t frames, int32_t C, int32_t HW, void* stream) {
+  int64_t total = (int64_t)frames * C * HW;
+  transpose_f32_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, C, HW, 1);
+  return launch_status("sf_bcthw_to_rows_f32");
+}
+
+sf_status sf_rows_to_bcthw_f32(const float* x, float* y, int32_t frames, int32_t C, int32_t HW, void* stream) {
+  int64_t total = (int64_t)frames * C * HW;
+  transpose_f32_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, HW, C, 0);
+  return launch_status("sf_rows_to_bcthw_f32");
+}
+
+sf_status sf_axpy_f32(float* x, const float* eps, float alpha, int64_t n, void* stream) {
+  axpy_kernel<<<ew_grid(n, 256), 256, 0, (cudaStream_t)stream>>>(x, eps, alpha, n);
+  return launch_status("sf_axpy_f32");
+}
+
+int64_t sf_dot3_workspace(int64_t n) { return (int64_t)DOT_BLOCKS * 3 * sizeof(double); }
+
+sf_status sf_dot3_bf16(const void* a, const void* b, int64_t n, void* work, double* out, void* stream) {
+  SF_CHECK_ARG(n >= 1 && aligned16(a) && aligned16(b), SF_ERR_PARAM, "bad probe buffers");
+  cudaStream_t st = (cudaStream_t)stream;
+  dot3_partial_kernel<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>((const bf16*)a, (const bf16*)b, n, (double*)work);
+  sum_parts_kernel<<<1, 32, 0, st>>>((const double*)work, DOT_BLOCKS, 3, out);
+  return launch_status("sf_dot3_bf16");
+}
+
+int64_t sf_gram_workspace(int32_t K, int64_t n) {
+  int64_t npairs = (int64_t)K * (K + 1) / 2;
+  return (GRAM_BLOCKS + 1) * npairs * (int64_t)sizeof(double);
+}
+
+sf_status sf_gram_bf16(const void* const* probes, int32_t K, int64_t n, void* work, double* out, void* stream) {
+  SF_CHECK_ARG(K >= 1 && n >= 1, SF_ERR_SHAPE, "bad extents");
+  cudaStream_t st = (cudaStream_t)stream;
+  int npairs = K * (K + 1) / 2;
+  double* part = (double*)work;
+  double* sums = part + (int64_t)GRAM_BLOCKS * npairs;
+  gram_partial_kernel<<<GRAM_BLOCKS, DOT_THREADS, 0, st>>>((const bf16* const*)probes, K, n, part);
+  sum_parts_kernel<<<1, 256, 0, st>>>(part, GRAM_BLOCKS, npairs, sums);
+  gram_finalize_kernel<<<1, 32, 0, st>>>(sums, K, out);
+  return launch_status("sf_gram_bf16");
+}
+
+}  // extern "C"

@@ -1,0 +1,739 @@
+"""Device executor: compiles a GroupedGraph into fused sm_100a launches.
+
+Mirrors the reference's missing ``executor`` module (contract ``SPEC.md:312-
+380``; ``ExecMode`` values ``grouping.py:343``).  ``execute(graph_or_grouped,
+mode, inputs, weights)`` keeps the reference signature; underneath, a
+:class:`Plan` is compiled once per (graph, weights, config) and replayed:
+
+1. **Operator Grouping** comes from :func:`grouping.group_operators` -- the
+   reference's own partition.  Each group runs slice by slice (Feature Slicer):
+   a spatial slice is a contiguous range of whole frames, a temporal slice is a
+   band of pixels across all frames; both are *views* into the channels-last
+   activation (``sf_view_t``), never copies.  Intermediates of a group live
+   in a slice-sized scratch region, so the per-group working set is bounded
+   by one slice (paper Eq. 1, §4.2).
+2. **Boundary fusion**: every ``Add`` whose first operand comes from a group
+   ending in a GEMM-type op (conv, temporal conv, linear, attention) is folded
+   into that GEMM's epilogue (the step-embedding add as a per-frame bias, the
+   residual adds as a residual read); a ``SiLU`` after a norm or GEMM is
+   folded into it; each ``Concat`` allocates one buffer whose channel ranges
+   its producers write directly (zero-copy).  None of this changes what is
+   computed, only where intermediate sums are rounded (fp32 epilogue instead
+   of a bf16 round trip).
+3. **Memory**: all group-boundary tensors live in one arena whose offsets come
+   from a liveness interval packing over the schedule; scratch is one region
+   sized for the largest slice.  ``Plan.arena_bytes + Plan.scratch_bytes`` is
+   the device analog of the reference's static peak model.
+
+Precision: activations are stored in bf16, every accumulation is fp32 (GEMM
+accumulators in TMEM/registers, norm statistics in fp64), the latent and the
+network output are fp32.  Tolerances against the fp64/fp32 oracle are stated
+in the tests.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as D
+from .device import Epilogue, Rows
+from .errors import InvalidParam, ShapeMismatch
+from .graph import Graph, infer_shapes
+from .grouping import GroupedGraph, group_operators
+from .kinds import Domain, OpKind
+from .modes import ExecMode
+from .slicer import default_temporal_config
+from .tensor import Shape5, Tensor5D
+from .unet import PROBE_LABEL, UNetConfig, sinusoidal_step_embedding
+
+GEMM_KINDS = (OpKind.CONV2D, OpKind.TEMPORAL_CONV, OpKind.LINEAR, OpKind.SPATIAL_ATTENTION,
+              OpKind.TEMPORAL_ATTENTION)
+
+
+@dataclass
+class ExecConfig:
+    """Device execution knobs.
+
+    spatial_k / temporal_k: slice counts per group (None = the fewest slices
+    whose scratch fits ``scratch_budget``).  gemm_backend: 0 auto (tcgen05
+    where the shape allows, else mma.sync), 1 mma.sync only, 2 tcgen05 only.
+    """
+
+    spatial_k: int | None = None
+    temporal_k: int | None = None
+    scratch_budget: int = 2 << 30
+    gemm_backend: int = 0
+    device: str = "cuda"
+
+
+def balanced(extent: int, k: int) -> list[tuple[int, int]]:
+    """k nearly equal contiguous chunks (device slice plan)."""
+    k = max(1, min(k, extent))
+    base, rem = divmod(extent, k)
+    out, s = [], 0
+    for i in range(k):
+        n = base + (1 if i < rem else 0)
+        out.append((s, s + n))
+        s += n
+    return out
+
+
+@dataclass
+class Value:
+    """Device storage of one graph value."""
+
+    name: str
+    shape: Shape5
+    kind: str = "rows"          # rows (bf16 channels-last) | emb (fp32 vector) | latent / eps (fp32 rows)
+    buf: str | None = None      # arena buffer key
+    col0: int = 0
+    width: int = 0              # storage row width (>= C when aliased into a concat)
+    tensor: torch.Tensor | None = None
+
+
+@dataclass
+class Unit:
+    """One schedule unit compiled to launches."""
+
+    label: str
+    run: object                  # callable(stream)
+    ref: tuple = ()              # schedule unit it lowers
+    reads: list = field(default_factory=list)
+    writes: list = field(default_factory=list)
+    gemm_flops: float = 0.0
+
+
+class Plan:
+    """Compiled launch program for one network evaluation (and its rehash tail)."""
+
+    def __init__(self, graph: Graph, grouped: GroupedGraph, dw: D.DeviceWeights, cfg: ExecConfig,
+                 emb_channels: int | None = None):
+        self.graph, self.grouped, self.dw, self.cfg = graph, grouped, dw, cfg
+        self.dev = dw.dev
+        self.shapes = infer_shapes(graph)
+        self.topo = graph.topo_order()
+        self.pos = {n: i for i, n in enumerate(self.topo)}
+        self.cons = graph.consumers()
+        self.values: dict[str, Value] = {}
+        self.fused_adds: dict[str, tuple[str, str]] = {}   # add id -> (producer tail, other operand)
+        self.epilogue_of: dict[str, tuple[str, str, bool]] = {}  # producer tail -> (add id, operand, is_emb)
+        self.units: list[Unit] = []
+        self.emb_nodes: list[str] = []
+        self._analyse()
+        self._layout()
+        self._compile()
+
+    # ------------------------------------------------------------------ analysis
+    def _producer_group(self, vid):
+        for gi, g in enumerate(self.grouped.groups):
+            if g.tail == vid:
+                return gi, g
+        return None, None
+
+    def _analyse(self):
+        g = self.graph
+        for nid in self.topo:
+            n = g.nodes[nid]
+            if n.kind is OpKind.LINEAR and n.inputs == ("step_emb",):
+                self.emb_nodes.append(nid)
+        for nid in self.topo:
+            n = g.nodes[nid]
+            if n.kind is not OpKind.ADD:
+                continue
+            a, b = n.inputs
+            gi, grp = self._producer_group(a)
+            if grp is None or grp.ops[-1].kind not in GEMM_KINDS or len(self.cons.get(a, [])) != 1:
+                continue
+            if grp.ops[-1].kind is OpKind.CONV2D and "w" not in self.dw.p[grp.ops[-1].id]:
+                continue
+            if a in self.epilogue_of:
+                continue
+            is_emb = b in self.emb_nodes
+            sa, sb = self.shapes[a], self.shapes[b]
+            if not is_emb and sa != sb:
+                continue
+            self.fused_adds[nid] = (a, b)
+            self.epilogue_of[a] = (nid, b, is_emb)
+
+    # ------------------------------------------------------------------ layout
+    def _storage_id(self, vid):
+        """Fused-add producers write straight into the add's output."""
+        if vid in self.epilogue_of:
+            return self.epilogue_of[vid][0]
+        return vid
+
+    def _layout(self):
+        g = self.graph
+        sched = list(self.grouped.schedule)
+        # unit index of definition / last use per stored value
+        unit_of = {}
+        for ui, (k, r) in enumerate(sched):
+            outs = [r] if k == "node" else [self.grouped.groups[r].tail]
+            for o in outs:
+                unit_of[o] = ui
+        uses: dict[str, list[int]] = {}
+        for ui, (k, r) in enumerate(sched):
+            ins = g.nodes[r].inputs if k == "node" else (self.grouped.groups[r].head_input,)
+            for v in ins:
+                uses.setdefault(v, []).append(ui)
+            if k == "group":
+                tail = self.grouped.groups[r].tail
+                if tail in self.epilogue_of:
+                    add_id, other, _ = self.epilogue_of[tail]
+                    uses.setdefault(other, []).append(ui)
+        # concat aliasing: operand -> (concat id, col offset)
+        alias: dict[str, tuple[str, int]] = {}
+        for nid in self.topo:
+            n = g.nodes[nid]
+            if n.kind is OpKind.CONCAT:
+                off = 0
+                ok = all(self._storage_id(v) not in alias and v in g.nodes for v in n.inputs)
+                if ok:
+                    for v in n.inputs:
+                        alias[self._storage_id(v)] = (nid, off)
+                        off += self.shapes[v].c
+        self.alias = alias
+        # buffers: one per storage root
+        intervals: dict[str, list[int]] = {}
+        sizes: dict[str, int] = {}
+
+        def root(sid):
+            while sid in alias:
+                sid = alias[sid][0]
+            return sid
+
+        special = {"x", "step_emb", *self.emb_nodes}
+        for vid, shape in self.shapes.items():
+            if vid in special:
+                continue
+            sid = root(self._storage_id(vid))
+            d = unit_of.get(vid, unit_of.get(self._storage_id(vid), 0))
+            last = max(uses.get(vid, [d]) + [d])
+            if vid in g.outputs:
+                last = len(sched)
+            lo, hi = intervals.get(sid, [d, last])
+            intervals[sid] = [min(lo, d), max(hi, last)]
+        out_id = g.outputs[0]
+        for sid in intervals:
+            s = self.shapes[sid]
+            sizes[sid] = s.b * s.t * s.h * s.w * s.c * 2
+        sizes[out_id] = self.shapes[out_id].count() * 4   # eps is fp32
+        # persistent: the rehash probe (its storage doubles as the feature cache)
+        probe = None
+        for n in g.nodes.values():
+            if n.label == PROBE_LABEL:
+                probe = root(self._storage_id(n.id))
+        if probe is not None:
+            intervals[probe] = [0, len(sched)]
+        self.probe_root = probe
+        # interval packing: largest first, lowest non-conflicting offset
+        placed: list[tuple[int, int, int, int]] = []  # (off, size, lo, hi)
+        offsets = {}
+        align = 256
+        for sid in sorted(sizes, key=lambda s: (-sizes[s], s)):
+            lo, hi = intervals[sid]
+            size = (sizes[sid] + align - 1) // align * align
+            cands = sorted({0} | {o + sz for o, sz, l2, h2 in placed})
+            for off in cands:
+                if all(not (l2 <= hi and lo <= h2 and off < o + sz and o < off + size) for o, sz, l2, h2 in placed):
+                    break
+            placed.append((off, size, lo, hi))
+            offsets[sid] = off
+        self.arena_bytes = max([o + s for o, s, _, _ in placed] + [align])
+        self.arena = torch.empty(self.arena_bytes, dtype=torch.uint8, device=self.dev)
+        self.buffers = {}
+        for sid, off in offsets.items():
+            s = self.shapes[sid]
+            rows = s.b * s.t * s.h * s.w
+            if sid == out_id:
+                t = self.arena[off:off + rows * s.c * 4].view(torch.float32).view(rows, s.c)
+            else:
+                t = self.arena[off:off + rows * s.c * 2].view(torch.bfloat16).view(rows, s.c)
+            self.buffers[sid] = t
+        # values
+        for vid, shape in self.shapes.items():
+            if vid in ("x", "step_emb") or vid in self.emb_nodes:
+                continue
+            sid = self._storage_id(vid)
+            col = 0
+            while sid in alias:
+                sid, c0 = alias[sid][0], alias[sid][1] + col
+                col = c0
+            self.values[vid] = Value(vid, shape, buf=sid, col0=col, tensor=self.buffers[sid])
+        # inputs: latent rows (fp32) and the emb table
+        xs = self.shapes["x"]
+        self.latent = torch.zeros(xs.b * xs.t * xs.h * xs.w, xs.c, dtype=torch.float32, device=self.dev)
+        self.eps = self.buffers[out_id]
+        # step-embedding projections of every res block: one gemv per step
+        ws = [self.dw.p[n]["w32"] for n in self.emb_nodes]
+        bs = [self.dw.p[n]["bias"] for n in self.emb_nodes]
+        self.emb_w = torch.cat(ws, 0).contiguous() if ws else None
+        self.emb_b = torch.cat(bs, 0).contiguous() if bs else None
+        self.emb_out = torch.zeros(sum(w.shape[0] for w in ws), dtype=torch.float32, device=self.dev)
+        self.emb_slot = {}
+        off = 0
+        for n, w in zip(self.emb_nodes, ws):
+            self.emb_slot[n] = self.emb_out[off:off + w.shape[0]]
+            off += w.shape[0]
+        self.emb_in = torch.zeros(self.shapes["step_emb"].c if "step_emb" in self.shapes else 1,
+                                  dtype=torch.float32, device=self.dev)
+        self.peak_model_bytes = self.arena_bytes
+
+    def rows(self, vid, row0=0, ostride=0) -> Rows:
+        v = self.values[vid]
+        return Rows(v.tensor, row0, ostride, v.col0)
+
+    # ------------------------------------------------------------------ compile
+    def _k_for(self, per_unit_bytes: int, extent: int, override: int | None) -> int:
+        if override:
+            return max(1, min(override, extent))
+        units = max(1, self.cfg.scratch_budget // max(1, per_unit_bytes))
+        return max(1, math.ceil(extent / units))
+
+    def _compile(self):
+        self.scratch_need = 0
+        self._scratch_users = []
+        for kind, ref in self.grouped.schedule:
+            if kind == "node":
+                u = self._compile_node(self.graph.nodes[ref])
+            else:
+                u = self._compile_group(self.grouped.groups[ref])
+            if u is not None:
+                u.ref = (kind, ref)
+                self.units.append(u)
+        self.scratch = torch.empty(max(self.scratch_need, 256), dtype=torch.uint8, device=self.dev)
+        for fn in self._scratch_users:
+            fn(self.scratch)
+        self.scratch_bytes = self.scratch.numel()
+        self.gn_work = None
+
+    def _scratch(self, specs):
+        """Reserve named slice-scratch tensors (bound after compile)."""
+        off, layout = 0, {}
+        for name, (rows, cols, dtype) in specs.items():
+            es = torch.empty((), dtype=dtype).element_size()
+            layout[name] = (off, rows, cols, dtype)
+            off += (rows * cols * es + 255) // 256 * 256
+        self.scratch_need = max(self.scratch_need, off)
+        holder = {}
+
+        def bind(buf):
+            for name, (o, r, c, dt) in layout.items():
+                es = torch.empty((), dtype=dt).element_size()
+                holder[name] = buf[o:o + r * c * es].view(dt).view(r, c)
+        self._scratch_users.append(bind)
+        return holder
+
+    def _epilogue(self, tail_id, rows_fn):
+        """Epilogue for a GEMM-ending group whose output feeds a fused Add."""
+        if tail_id not in self.epilogue_of:
+            return lambda sl: Epilogue()
+        add_id, other, is_emb = self.epilogue_of[tail_id]
+        if is_emb:
+            eb = self.emb_slot[other]
+            return lambda sl: Epilogue(rowbias=eb)
+        return lambda sl: Epilogue(res=rows_fn(other, sl))
+
+    def _compile_node(self, n):
+        g = self.graph
+        if n.id in self.fused_adds or n.id in self.emb_nodes:
+            return None
+        shp = self.shapes[n.id]
+        if n.kind is OpKind.CONCAT:
+            outs = []
+            for v in n.inputs:
+                if self.values[v].buf != self.values[n.id].buf:
+                    outs.append(v)
+            if not outs:
+                return None
+            off_map = {}
+            off = 0
+            for v in n.inputs:
+                off_map[v] = off
+                off += self.shapes[v].c
+
+            def run(st, n=n, outs=outs, off_map=off_map):
+                for v in outs:
+                    s = self.shapes[v]
+                    N.call("sf_copy_rows", self.rows(v).view(), self.rows(n.id).shifted(cols=off_map[v]).view(),
+                           1, s.b * s.t * s.h * s.w, s.c, st)
+            return Unit(n.id, run)
+        if n.kind is OpKind.ADD:
+            a, b = n.inputs
+            sa, sb = self.shapes[a], self.shapes[b]
+            if b in self.emb_nodes or a in self.emb_nodes:
+                raise InvalidParam(f"unfusable step-embedding add {n.id}")
+            bcast = (sb.h, sb.w) == (1, 1) and (sa.h, sa.w) != (1, 1)
+
+            def run(st, n=n, a=a, b=b, s=shp, bcast=bcast):
+                N.call("sf_add", self.rows(a).view(), self.rows(b, 0, 1 if bcast else 0).view(),
+                       self.rows(n.id).view(), s.b * s.t if bcast else 1,
+                       s.h * s.w if bcast else s.b * s.t * s.h * s.w, s.c, 1 if bcast else 0, st)
+            return Unit(n.id, run)
+        if n.kind is OpKind.SPLIT:
+            sizes = [int(v) for v in n.attrs["sizes"]]
+            off = sum(sizes[:int(n.attrs["index"])])
+
+            def run(st, n=n, off=off, s=shp):
+                N.call("sf_copy_rows", self.rows(n.inputs[0]).shifted(cols=off).view(), self.rows(n.id).view(), 1,
+                       s.b * s.t * s.h * s.w, s.c, st)
+            return Unit(n.id, run)
+        raise InvalidParam(f"ungrouped {n.kind.value} node {n.id} has no device lowering")
+
+    def _compile_group(self, grp):
+        ops = list(grp.ops)
+        kinds = [o.kind for o in ops]
+        head_in = grp.head_input
+        in_shape = self.shapes[head_in]
+        if ops[0].id in self.emb_nodes:
+            return None
+        if grp.domain is Domain.SPATIAL:
+            return self._compile_spatial(grp, ops, kinds, in_shape)
+        return self._compile_temporal(grp, ops, kinds, in_shape)
+
+    # spatial groups: slices are frame ranges
+    def _compile_spatial(self, grp, ops, kinds, s):
+        frames = s.b * s.t
+        HW = s.h * s.w
+        backend = self.cfg.gemm_backend
+        C = s.c
+        # per-frame scratch estimate of the chain
+        per_frame = 0
+        shape = s
+        for o in ops:
+            if o.kind is OpKind.SPATIAL_ATTENTION:
+                per_frame += HW * 3 * C * 2 + HW * HW * 6 + HW * C * 2
+            per_frame += shape.h * shape.w * max(shape.c, 8) * 2 * 2
+        k = self._k_for(per_frame, frames, self.cfg.spatial_k)
+        slices = balanced(frames, k)
+        fmax = max(b - a for a, b in slices)
+        tail = ops[-1].id
+        x_id = grp.head_input
+        latent_in = x_id == "x"
+
+        def vrows(vid, sl):
+            sh = self.shapes[vid]
+            return self.rows(vid, sl[0] * sh.h * sh.w, sh.h * sh.w)
+
+        epi_fn = self._epilogue(tail, vrows)
+        # lower the chain into steps over slice-local buffers
+        steps = []
+        specs = {}
+        shape = s
+        cur = "IN"
+        i = 0
+        nb = 0
+        flops = 0.0
+        gn_need = None
+        max_groups = max([int(o.attrs.get("groups", 1)) for o in ops if o.kind is OpKind.GROUP_NORM] + [1])
+        while i < len(ops):
+            o = ops[i]
+            nxt = ops[i + 1] if i + 1 < len(ops) else None
+            fuse_act = nxt is not None and nxt.kind is OpKind.SILU
+            last = (i + (2 if fuse_act else 1)) >= len(ops)
+            out_shape = self.shapes[ops[i + (1 if fuse_act else 0)].id]
+            dst = "OUT" if last else f"t{nb}"
+            if not last:
+                specs[dst] = (fmax * out_shape.h * out_shape.w, out_shape.c, torch.bfloat16)
+                nb += 1
+            act = N.ACT_SILU if fuse_act else N.ACT_NONE
+            steps.append((o, cur, dst, shape, out_shape, act, last))
+            cur = dst
+            if o.kind is OpKind.CONV2D:
+                flops += 2.0 * frames * out_shape.h * out_shape.w * shape.c * out_shape.c * 9
+            elif o.kind is OpKind.LINEAR:
+                flops += 2.0 * frames * HW * shape.c * out_shape.c
+            elif o.kind is OpKind.SPATIAL_ATTENTION:
+                flops += frames * (8.0 * HW * C * C + 4.0 * HW * HW * C)
+            if o.kind is OpKind.GROUP_NORM:
+                gn_need = max(gn_need or 0, N.query("sf_group_norm_workspace", fmax, shape.h * shape.w, shape.c))
+            if o.kind is OpKind.SPATIAL_ATTENTION:
+                hw = shape.h * shape.w
+                specs["qkv"] = (fmax * hw, 3 * shape.c, torch.bfloat16)
+                specs["o"] = (fmax * hw, shape.c, torch.bfloat16)
+                if hw > D.SMALL_SEQ:
+                    specs["s"] = (fmax * hw, hw, torch.float32)
+                    specs["p"] = (fmax * hw, hw, torch.bfloat16)
+            shape = out_shape
+            i += 2 if fuse_act else 1
+        if gn_need:
+            specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
+            specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
+        scratch = self._scratch(specs)
+        eps_out = tail == self.graph.outputs[0]
+
+        def run(st):
+            for sl in slices:
+                nf = sl[1] - sl[0]
+
+                def loc(name, shp):
+                    if name == "IN":
+                        return vrows(x_id, sl)
+                    if name == "OUT":
+                        return vrows(tail, sl)
+                    return Rows(scratch[name], 0, shp.h * shp.w)
+                for (o, src, dst, ish, osh, act, last) in steps:
+                    prm = self.dw.p.get(o.id)
+                    X = None if (latent_in and src == "IN") else loc(src, ish)
+                    Y = loc(dst, osh)
+                    epi = epi_fn(sl) if last else Epilogue()
+                    if act:
+                        epi.act = act
+                    k = o.kind
+                    ihw, ohw = ish.h * ish.w, osh.h * osh.w
+                    if k is OpKind.GROUP_NORM:
+                        groups = int(o.attrs.get("groups", 1))
+                        stats = scratch["gn_stats"]
+                        mean = stats[:nf * groups, 0]
+                        rstd = stats[fmax * max_groups: fmax * max_groups + nf * groups, 0]
+                        D.group_norm_stats(st, X, nf, ihw, ish.c, groups, float(o.attrs.get("eps", 1e-5)),
+                                           scratch["gn_work"], mean, rstd)
+                        D.group_norm_apply(st, X, Y, nf, ihw, ish.c, groups, mean, rstd, prm, act)
+                    elif k is OpKind.LAYER_NORM:
+                        D.layer_norm(st, X, Y, nf, ihw, ish.c, prm, float(o.attrs.get("eps", 1e-5)), act)
+                    elif k is OpKind.SILU:
+                        N.call("sf_silu", X.view(), Y.view(), nf, ihw, ish.c, st)
+                    elif k is OpKind.CONV2D:
+                        if latent_in and src == "IN":
+                            lat = self.latent[sl[0] * ihw:]
+                            N.call("sf_conv3x3_smallcin", lat.data_ptr(), nf, ish.h, ish.w, ish.c,
+                                   prm["w32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), st)
+                        elif last and eps_out:
+                            out = self.eps[sl[0] * ohw:]
+                            N.call("sf_conv3x3_smallcout", X.view(), nf, ish.h, ish.w, ish.c,
+                                   prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, out.data_ptr(), st)
+                        else:
+                            D.conv2d(st, X, Y, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend)
+                    elif k is OpKind.LINEAR:
+                        D.linear(st, X, Y, nf, ihw, ish.c, osh.c, prm, epi, backend)
+                    elif k is OpKind.SPATIAL_ATTENTION:
+                        D.spatial_attention(st, X, Y, nf, ihw, ish.c, prm, epi, scratch, backend)
+                    elif k is OpKind.DOWNSAMPLE2X:
+                        N.call("sf_downsample2x", X.view(), Y.view(), nf, ish.h, ish.w, ish.c, st)
+                    elif k is OpKind.UPSAMPLE2X:
+                        N.call("sf_upsample2x", X.view(), Y.view(), nf, ish.h, ish.w, ish.c, st)
+                    else:
+                        raise InvalidParam(f"no spatial lowering for {k.value}")
+        return Unit(grp.label, run, gemm_flops=flops)
+
+    # temporal groups: slices are pixel bands across all frames
+    def _compile_temporal(self, grp, ops, kinds, s):
+        B, T, HW, C = s.b, s.t, s.h * s.w, s.c
+        backend = self.cfg.gemm_backend
+        per_pix = 0
+        for o in ops:
+            per_pix += B * T * C * 2 * (4 if o.kind is OpKind.TEMPORAL_ATTENTION else 1)
+        k = self._k_for(per_pix, HW, self.cfg.temporal_k)
+        bands = balanced(HW, k)
+        pmax = max(b - a for a, b in bands)
+        tail = ops[-1].id
+        x_id = grp.head_input
+
+        def vrows(vid, band):
+            return self.rows(vid, band[0], HW)
+
+        epi_fn = self._epilogue(tail, vrows)
+        steps, specs = [], {}
+        i = nb = 0
+        flops = 0.0
+        while i < len(ops):
+            o = ops[i]
+            nxt = ops[i + 1] if i + 1 < len(ops) else None
+            fuse_act = nxt is not None and nxt.kind is OpKind.SILU
+            last = (i + (2 if fuse_act else 1)) >= len(ops)
+            oc = self.shapes[ops[i + (1 if fuse_act else 0)].id].c
+            dst = "OUT" if last else f"t{nb}"
+            if not last:
+                specs[dst] = (B * T * pmax, oc, torch.bfloat16)
+                nb += 1
+            steps.append((o, None, dst, N.ACT_SILU if fuse_act else N.ACT_NONE, last, oc))
+            if o.kind is OpKind.TEMPORAL_CONV:
+                flops += 2.0 * B * T * HW * C * oc * 3
+            elif o.kind is OpKind.LINEAR:
+                flops += 2.0 * B * T * HW * C * oc
+            elif o.kind is OpKind.TEMPORAL_ATTENTION:
+                flops += B * HW * (8.0 * T * C * C + 4.0 * T * T * C)
+                specs["qkv"] = (B * T * pmax, 3 * C, torch.bfloat16)
+                specs["o"] = (B * T * pmax, C, torch.bfloat16)
+            i += 2 if fuse_act else 1
+        # fix up sources: each step reads the previous step's destination
+        fixed, prev = [], "IN"
+        for (o, _src, dst, act, last, oc) in steps:
+            fixed.append((o, prev, dst, act, last, oc))
+            prev = dst
+        steps = fixed
+        scratch = self._scratch(specs)
+
+        def run(st):
+            for band in bands:
+                npx = band[1] - band[0]
+
+                def loc(name):
+                    if name == "IN":
+                        return vrows(x_id, band)
+                    if name == "OUT":
+                        return vrows(tail, band)
+                    return Rows(scratch[name], 0, npx)
+                cin = C
+                for (o, src, dst, act, last, oc) in steps:
+                    prm = self.dw.p.get(o.id)
+                    X, Y = loc(src), loc(dst)
+                    epi = epi_fn(band) if last else Epilogue()
+                    if act:
+                        epi.act = act
+                    k = o.kind
+                    if k is OpKind.LAYER_NORM:
+                        D.layer_norm(st, X, Y, B * T, npx, cin, prm, float(o.attrs.get("eps", 1e-5)), act)
+                    elif k is OpKind.SILU:
+                        N.call("sf_silu", X.view(), Y.view(), B * T, npx, cin, st)
+                    elif k is OpKind.TEMPORAL_CONV:
+                        D.temporal_conv(st, X, Y, B * T, T, npx, cin, oc, prm, epi, backend)
+                    elif k is OpKind.LINEAR:
+                        D.linear(st, X, Y, B * T, npx, cin, oc, prm, epi, backend)
+                    elif k is OpKind.TEMPORAL_ATTENTION:
+                        D.temporal_attention(st, X, Y, B, T, npx, cin, prm, epi, scratch, backend)
+                    else:
+                        raise InvalidParam(f"no temporal lowering for {k.value}")
+                    cin = oc
+        return Unit(grp.label, run, gemm_flops=flops)
+
+    # ------------------------------------------------------------------ run
+    def units_after(self, node_id):
+        """Units strictly after ``node_id`` in topo order (the rehash tail)."""
+        cut = self.pos[node_id]
+        out = []
+        for u in self.units:
+            k, r = u.ref
+            first = r if k == "node" else self.grouped.groups[r].ops[0].id
+            if self.pos[first] > cut:
+                out.append(u)
+        return out
+
+    def emb_launch(self, st, emb_vec_ptr):
+        if self.emb_w is not None:
+            N.call("sf_gemv_f32", self.emb_w.data_ptr(), emb_vec_ptr, self.emb_b.data_ptr(),
+                   self.emb_out.data_ptr(), self.emb_w.shape[0], self.emb_w.shape[1], st)
+
+    def run_full(self, st, emb_vec_ptr):
+        self.emb_launch(st, emb_vec_ptr)
+        for u in self.units:
+            u.run(st)
+
+    def run_tail(self, st):
+        for u in self.tail_units:
+            u.run(st)
+
+    @property
+    def tail_units(self):
+        if not hasattr(self, "_tail"):
+            self._tail = self.units_after(self.graph.node_by_label(PROBE_LABEL).id)
+        return self._tail
+
+    @property
+    def probe(self) -> torch.Tensor:
+        return self.values[self.graph.node_by_label(PROBE_LABEL).id].tensor
+
+    def probe_rows(self) -> Rows:
+        return self.rows(self.graph.node_by_label(PROBE_LABEL).id)
+
+    def flops_full(self) -> float:
+        return sum(u.gemm_flops for u in self.units)
+
+    def flops_tail(self) -> float:
+        return sum(u.gemm_flops for u in self.tail_units)
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class DeviceModel:
+    """Graph + device weights + compiled plan; the object behind execute/rehash/run_denoise."""
+
+    def __init__(self, graph: Graph, weights, cfg: ExecConfig | None = None, grouped: GroupedGraph | None = None,
+                 unet_cfg: UNetConfig | None = None):
+        N.load()
+        if not torch.cuda.is_available():
+            from .errors import NativeError
+            raise NativeError("no CUDA device: the sliceflow_b200 path has no CPU fallback")
+        self.cfg = cfg or ExecConfig()
+        self.graph = graph
+        self.unet_cfg = unet_cfg
+        if grouped is None:
+            xs = graph.inputs["x"]
+            grouped = group_operators(graph, xs.b * xs.t, default_temporal_config(xs.h, xs.w))
+        self.grouped = grouped
+        self.dw = D.DeviceWeights(graph, weights, self.cfg.device)
+        self.plan = Plan(graph, grouped, self.dw, self.cfg)
+        xs = graph.inputs["x"]
+        self.x_shape = xs
+        self.host_in = torch.empty(xs.count(), dtype=torch.float32).pin_memory()
+        self.host_out = torch.empty(xs.count(), dtype=torch.float32).pin_memory()
+        self.dev_bcthw = torch.empty(xs.count(), dtype=torch.float32, device=self.dw.dev)
+
+    # latent edges
+    def upload_latent(self, st, x_host: np.ndarray):
+        xs = self.x_shape
+        self.host_in.numpy()[:] = np.ascontiguousarray(x_host, dtype=np.float32).ravel()
+        self.dev_bcthw.copy_(self.host_in, non_blocking=True)
+        N.call("sf_bcthw_to_rows_f32", self.dev_bcthw.data_ptr(), self.plan.latent.data_ptr(), xs.b * xs.t, xs.c,
+               xs.h * xs.w, st)
+
+    def latent_to_bcthw(self, st, src_rows: torch.Tensor):
+        xs = self.x_shape
+        N.call("sf_rows_to_bcthw_f32", src_rows.data_ptr(), self.dev_bcthw.data_ptr(), xs.b * xs.t, xs.c, xs.h * xs.w,
+               st)
+        return self.dev_bcthw
+
+    def download(self, dev_tensor) -> np.ndarray:
+        self.host_out.copy_(dev_tensor.view(-1), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.host_out.numpy().reshape(tuple(self.x_shape)).copy()
+
+
+def execute(graph_or_grouped, mode, inputs, weights, cfg: ExecConfig | None = None):
+    """One network evaluation on the device.
+
+    Returns ``(output Tensor5D, ledger, timing)`` like the reference contract;
+    ``ledger`` reports device bytes (arena + scratch, and the torch peak),
+    ``timing`` wall-clock ms per phase.  REFERENCE runs the same fused
+    kernels with one slice per group (unsliced); SLICED_LOOP / PIPELINED use
+    the slice plan of ``cfg`` (on one stream the pipelined wavefront and the
+    for-loop issue the same launches, so they are the same program here).
+    """
+    mode = ExecMode(mode)
+    if mode is ExecMode.NAIVE_CLIP:
+        raise InvalidParam("naiveclip is a quality-divergence baseline and is not part of the device path")
+    cfg = cfg or ExecConfig()
+    if mode is ExecMode.REFERENCE:
+        cfg = ExecConfig(spatial_k=1, temporal_k=1, scratch_budget=cfg.scratch_budget,
+                         gemm_backend=cfg.gemm_backend, device=cfg.device)
+    if isinstance(graph_or_grouped, GroupedGraph):
+        graph, grouped = graph_or_grouped.graph, graph_or_grouped
+    else:
+        graph, grouped = graph_or_grouped, None
+    t0 = time.perf_counter()
+    model = DeviceModel(graph, weights, cfg, grouped)
+    t1 = time.perf_counter()
+    x = inputs["x"].data if isinstance(inputs["x"], Tensor5D) else np.asarray(inputs["x"])
+    se = inputs["step_emb"].data if isinstance(inputs["step_emb"], Tensor5D) else np.asarray(inputs["step_emb"])
+    vec = np.ascontiguousarray(se.reshape(-1, se.shape[2])[0], dtype=np.float32)
+    if not np.all(se.reshape(-1, se.shape[2]) == vec[None]):
+        raise ShapeMismatch("device path expects the step embedding broadcast over (b, t) (unet.py:106-113)")
+    torch.cuda.reset_peak_memory_stats()
+    st = stream_handle()
+    model.upload_latent(st, x)
+    emb = torch.from_numpy(vec).to(model.dw.dev)
+    model.plan.run_full(st, emb.data_ptr())
+    out = model.download(model.latent_to_bcthw(st, model.plan.eps))
+    t2 = time.perf_counter()
+    ledger = {"arena_bytes": model.plan.arena_bytes, "scratch_bytes": model.plan.scratch_bytes,
+              "torch_peak_bytes": torch.cuda.max_memory_allocated()}
+    timing = {"compile_ms": (t1 - t0) * 1e3, "run_ms": (t2 - t1) * 1e3}
+    return Tensor5D(out), ledger, timing

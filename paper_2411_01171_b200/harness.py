@@ -1,0 +1,228 @@
+"""Denoising loop on the device: ``run_denoise`` / ``rehash_execute``.
+
+Restates the harness contract (``SPEC.md:464-512``, code missing from the
+reference): x <- x - alpha_s * f(x, s) with alpha_s = float32(0.08*(1 - s/K))
+(``SPEC.md:482``), step embedding from s (``unet.py:106``), initial latent
+``default_rng(seed+1).standard_normal(input_shape)`` (the builder's
+documented choice for the unpinned "seeded initial x").
+
+:class:`Denoiser` owns one compiled :class:`executor.Plan`.  A whole K-step
+run (key steps + rehash tails + latent updates) is one static launch sequence,
+so it is captured once into a CUDA graph and replayed: no Python or ctypes on
+the timed path.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ScheduleMismatch
+from .executor import DeviceModel, ExecConfig
+from .graph import Graph
+from .modes import ExecMode
+from .rehash import SimilarityMap, StepSchedule, gamma_for_target, gram_similarity, key_step_search, op_count_report
+from .tensor import Tensor5D
+from .unet import PROBE_LABEL, UNetConfig, build_toy_unet, sinusoidal_step_embedding
+
+# kernels launched per C-ABI call (for the gpu_launches count of the bench)
+KERNELS_PER_CALL = {"sf_group_norm_stats": 2, "sf_dot3_bf16": 2, "sf_gram_bf16": 3}
+
+
+def alpha(s: int, K: int) -> float:
+    return float(np.float32(0.08 * (1.0 - s / K)))
+
+
+def initial_latent(cfg: UNetConfig) -> np.ndarray:
+    return np.random.default_rng(cfg.seed + 1).standard_normal(tuple(cfg.input_shape())).astype(np.float32)
+
+
+class _LaunchCounter:
+    def __init__(self):
+        self.n = 0
+        self._orig = None
+
+    def __enter__(self):
+        self._orig = N.call
+
+        def counted(name, *a):
+            self.n += KERNELS_PER_CALL.get(name, 1)
+            return self._orig(name, *a)
+        N.call = counted
+        return self
+
+    def __exit__(self, *exc):
+        N.call = self._orig
+
+
+class Denoiser:
+    """Device denoising loop over one UNetConfig (weights from build_toy_unet)."""
+
+    def __init__(self, cfg: UNetConfig, exec_cfg: ExecConfig | None = None, graph: Graph | None = None,
+                 weights=None, K: int | None = None):
+        self.cfg = cfg
+        self.K = K or cfg.steps
+        if graph is None:
+            graph, w64 = build_toy_unet(cfg)
+            weights = w64
+        self.graph = graph
+        self.model = DeviceModel(graph, weights, exec_cfg, unet_cfg=cfg)
+        self.plan = self.model.plan
+        dev = self.model.dw.dev
+        emb = np.stack([sinusoidal_step_embedding(s, cfg.emb_channels, cfg.emb_scale) for s in range(self.K)])
+        self.emb_table = torch.from_numpy(emb.astype(np.float32)).to(dev).contiguous()
+        self.trace = None
+        self._graphs: dict = {}
+        self.launches: dict = {}
+
+    # -------------------------------------------------------------- programs
+    def _program(self, schedule: StepSchedule | None, record_trace: bool):
+        st = torch.cuda.current_stream().cuda_stream
+        p = self.plan
+        keys = set(range(self.K)) if schedule is None else set(schedule.key_steps)
+        n_lat = p.latent.numel()
+        for s in range(self.K):
+            if s in keys:
+                p.run_full(st, self.emb_table[s].data_ptr())
+                if record_trace:
+                    pr = p.probe_rows()
+                    sh = p.shapes[self.graph.node_by_label(PROBE_LABEL).id]
+                    N.call("sf_copy_rows", pr.view(), N.View(self.trace[s].data_ptr(), sh.c, 0), 1,
+                           sh.b * sh.t * sh.h * sh.w, sh.c, st)
+            else:
+                p.run_tail(st)
+            N.call("sf_axpy_f32", p.latent.data_ptr(), p.eps.data_ptr(), alpha(s, self.K), n_lat, st)
+
+    def _key(self, schedule, record_trace):
+        return (None if schedule is None else tuple(schedule.key_steps), record_trace)
+
+    def prepare(self, schedule: StepSchedule | None = None, record_trace: bool = False, use_graph: bool = True):
+        """Warm up (eager run, counts launches) and capture the run as a CUDA graph."""
+        if schedule is not None and schedule.K != self.K:
+            raise ScheduleMismatch(f"schedule has K={schedule.K}, run has K={self.K}")
+        key = self._key(schedule, record_trace)
+        if record_trace and self.trace is None:
+            sh = self.plan.shapes[self.graph.node_by_label(PROBE_LABEL).id]
+            self.trace = torch.empty(self.K, sh.count(), dtype=torch.bfloat16, device=self.model.dw.dev)
+        if key in self._graphs:
+            return key
+        with _LaunchCounter() as c:
+            self._program(schedule, record_trace)
+        torch.cuda.synchronize()
+        self.launches[key] = c.n
+        g = None
+        if use_graph:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._program(schedule, record_trace)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+        self._graphs[key] = g
+        return key
+
+    def launch(self, key):
+        g = self._graphs[key]
+        if g is not None:
+            g.replay()
+        else:
+            sched = None if key[0] is None else StepSchedule(list(key[0]), self.K)
+            self._program(sched, key[1])
+
+    # -------------------------------------------------------------- runs
+    def set_latent(self, x0: np.ndarray):
+        self.model.upload_latent(torch.cuda.current_stream().cuda_stream, x0)
+
+    def result(self) -> np.ndarray:
+        st = torch.cuda.current_stream().cuda_stream
+        return self.model.download(self.model.latent_to_bcthw(st, self.plan.latent))
+
+    def run(self, x0: np.ndarray, schedule: StepSchedule | None = None, record_trace=False) -> np.ndarray:
+        key = self.prepare(schedule, record_trace)
+        self.set_latent(x0)
+        self.launch(key)
+        return self.result()
+
+    def calibrate(self, x0: np.ndarray) -> tuple[np.ndarray, SimilarityMap]:
+        """All-key run recording the probe each step; returns (final x, S)."""
+        x = self.run(x0, None, record_trace=True)
+        S = gram_similarity([self.trace[s] for s in range(self.K)], PROBE_LABEL)
+        return x, S
+
+    def tail_node_count(self) -> int:
+        topo = self.graph.topo_order()
+        return len(topo) - 1 - topo.index(self.graph.node_by_label(PROBE_LABEL).id)
+
+
+@dataclass
+class DenoiseRunConfig:
+    """SPEC.md:468-472."""
+
+    unet: UNetConfig
+    steps: int | None = None
+    mode: ExecMode = ExecMode.SLICED_LOOP
+    schedule: StepSchedule | None = None
+    gamma: float | None = None
+    target_keys: int | None = None
+    exec_cfg: ExecConfig = field(default_factory=ExecConfig)
+
+
+@dataclass
+class RunReport:
+    """SPEC.md:473-476 (device flavour)."""
+
+    peak_bytes: int
+    arena_bytes: int
+    scratch_bytes: int
+    wall_ms: float
+    output_checksum: float
+    op_counts: dict
+    schedule: dict | None
+    similarity_summary: dict | None
+
+
+def run_denoise(cfg: DenoiseRunConfig) -> tuple[Tensor5D, RunReport]:
+    """Full or rehash denoising run on the device."""
+    ucfg = cfg.unet
+    K = cfg.steps or ucfg.steps
+    ex = cfg.exec_cfg
+    if ExecMode(cfg.mode) is ExecMode.REFERENCE:
+        ex = ExecConfig(spatial_k=1, temporal_k=1, gemm_backend=ex.gemm_backend, device=ex.device)
+    den = Denoiser(ucfg, ex, K=K)
+    x0 = initial_latent(ucfg)
+    torch.cuda.reset_peak_memory_stats()
+    t0 = time.perf_counter()
+    schedule, sim = cfg.schedule, None
+    if schedule is None and (cfg.gamma is not None or cfg.target_keys is not None):
+        _, S = den.calibrate(x0)
+        gamma = cfg.gamma if cfg.gamma is not None else gamma_for_target(S, cfg.target_keys)
+        schedule = key_step_search(S, gamma, K)
+        sim = {"mean_adjacent": float(np.mean([S.values[i, i + 1] for i in range(K - 1)])) if K > 1 else 1.0}
+    x = den.run(x0, schedule)
+    wall = (time.perf_counter() - t0) * 1e3
+    if not np.isfinite(x).all():
+        from .errors import SliceflowError
+        raise SliceflowError("non-finite latent")
+    sched = schedule or StepSchedule(list(range(K)), K)
+    rep = RunReport(
+        peak_bytes=int(torch.cuda.max_memory_allocated()),
+        arena_bytes=den.plan.arena_bytes, scratch_bytes=den.plan.scratch_bytes, wall_ms=wall,
+        output_checksum=float(np.sum(x, dtype=np.float64)),
+        op_counts=op_count_report(den.graph, sched, den.tail_node_count()),
+        schedule=sched.to_json_dict(), similarity_summary=sim)
+    return Tensor5D(x), rep
+
+
+def rehash_execute(graph: Graph, weights, schedule: StepSchedule, inputs, cfg: UNetConfig,
+                   exec_cfg: ExecConfig | None = None):
+    """Run the K-step loop under ``schedule`` -> (output, op_count_report)."""
+    den = Denoiser(cfg, exec_cfg, graph=graph, weights=weights, K=schedule.K)
+    x0 = inputs["x"].data if isinstance(inputs["x"], Tensor5D) else np.asarray(inputs["x"])
+    x = den.run(x0, schedule)
+    return Tensor5D(x), op_count_report(graph, schedule, den.tail_node_count())

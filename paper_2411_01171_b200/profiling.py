@@ -1,0 +1,64 @@
+"""Per-launch device timing of a compiled program (CUDA events on the launch stream).
+
+Wraps every C-ABI call of one eager (non-graph) pass with a pair of CUDA
+events recorded on the stream the kernel is launched on, then aggregates by
+entry point.  For ``sf_gemm`` the algorithmic FLOPs of each launch
+(2*M*N*K*batch, K = taps*cin) are recorded, so the bench can report the GEMM
+kernel's achieved TFLOP/s against the measured bf16 peak.
+"""
+
+from __future__ import annotations
+
+from collections import defaultdict
+
+import torch
+
+from . import _native as N
+
+
+def gemm_flops(args) -> float:
+    taps = {N.GEMM_PLAIN: 1, N.GEMM_CONV3X3: 9, N.GEMM_TCONV3: 3}[args.mode]
+    return 2.0 * args.n_outer * args.n_inner * args.N * taps * args.cin * args.batch
+
+
+class CallProfiler:
+    def __init__(self):
+        self.records = []  # (name, start_event, end_event, flops, backend)
+        self._orig = None
+
+    def __enter__(self):
+        self._orig = N.call
+
+        def timed(name, *a):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            stream = torch.cuda.current_stream()
+            s.record(stream)
+            self._orig(name, *a)
+            e.record(stream)
+            flops, be = 0.0, 0
+            if name == "sf_gemm":
+                args = a[0]
+                flops = gemm_flops(args)
+                be = N.query("sf_gemm_backend", args)
+                name = f"sf_gemm[{'tcgen05' if be == 2 else 'mma.sync'}]"
+            self.records.append((name, s, e, flops))
+        N.call = timed
+        return self
+
+    def __exit__(self, *exc):
+        N.call = self._orig
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        agg = defaultdict(lambda: {"calls": 0, "ms": 0.0, "flops": 0.0})
+        for name, s, e, fl in self.records:
+            a = agg[name]
+            a["calls"] += 1
+            a["ms"] += s.elapsed_time(e)
+            a["flops"] += fl
+        total = sum(v["ms"] for v in agg.values())
+        for v in agg.values():
+            v["share"] = v["ms"] / total if total else 0.0
+            v["tflops"] = v["flops"] / (v["ms"] * 1e9) if v["ms"] and v["flops"] else 0.0
+        return {"total_ms": total, "by_call": dict(sorted(agg.items(), key=lambda kv: -kv[1]["ms"]))}

@@ -1,0 +1,148 @@
+"""CUDA path vs the oracle / reference goldens.  Runs on a B200 (-m gpu).
+
+Tolerances (stated per test) are for bf16 activation storage with fp32
+accumulation against the fp64 reference:
+  * single kernels: max_rel <= 1.5e-2 (one bf16 rounding of inputs+output);
+  * a full 10-step toy denoise: final-latent max_rel <= 2e-2;
+  * Step Rehash schedule: identical key steps G at a gamma whose decision
+    margin exceeds the measured similarity error.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2411_01171_b200 import ops  # noqa: E402
+from paper_2411_01171_b200.build import build  # noqa: E402
+from paper_2411_01171_b200.harness import Denoiser, initial_latent  # noqa: E402
+from paper_2411_01171_b200.kinds import OpKind  # noqa: E402
+from paper_2411_01171_b200.rehash import StepSchedule, key_step_search  # noqa: E402
+from paper_2411_01171_b200.tensor import Tensor5D  # noqa: E402
+from paper_2411_01171_b200.unet import UNetConfig  # noqa: E402
+
+build()
+
+C1 = UNetConfig(channels=4, frames=8, height=32, width=32, base_channels=8, norm_groups=4, steps=10)
+WIDE = UNetConfig(channels=4, frames=4, height=16, width=16, base_channels=64, norm_groups=32, steps=3)
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+def test_kernels_match_reference_vectors(golden):
+    kv = golden["kernels"]
+    keys = sorted({k.split("/")[0] for k in kv.files if k[:2].isdigit() and k.split("/")[0].endswith("float64")})
+    worst = {}
+    for key in keys:
+        kind = OpKind("_".join(key.split("_")[1:-1]))
+        attrs = json.loads(bytes(kv[f"{key}/attrs"]).decode())
+        params = {f[len(key) + 3:]: kv[f] for f in kv.files if f.startswith(f"{key}/p_")} or None
+        y = ops.apply_kernel(kind, [Tensor5D(kv[f"{key}/x"])], params, attrs)
+        worst[key] = rel(y.data, kv[f"{key}/y"])
+    print(worst)
+    assert max(worst.values()) <= 1.5e-2, worst
+    y = ops.apply_kernel(OpKind.ADD, [Tensor5D(kv["add_bias/a"]), Tensor5D(kv["add_bias/b"])])
+    assert rel(y.data, kv["add_bias/y"]) <= 1e-2
+    y = ops.apply_kernel(OpKind.CONCAT, [Tensor5D(kv["concat/a"]), Tensor5D(kv["concat/b"])])
+    assert rel(y.data, kv["concat/y"]) <= 1e-2
+    c = ops.cosine_similarity(Tensor5D(kv["cos/a"]), Tensor5D(kv["cos/b"]))
+    assert abs(c - kv["cos/y"][0]) < 5e-3
+
+
+def _oracle_kernel(kind, x, params, attrs):
+    from oracle import kernels as K
+    return K.apply_kernel(kind, [x], params, attrs)
+
+
+@pytest.mark.parametrize("backend", [1, 0])
+@pytest.mark.parametrize("case", ["conv_l0", "conv_cat", "tconv", "linear", "sattn", "tattn"])
+def test_sd_width_kernels_vs_oracle(case, backend):
+    """SD-width channel counts (multiples of 64) at reduced spatial size, both GEMM backends."""
+    rng = np.random.default_rng(11)
+    if case == "conv_l0":
+        x = rng.standard_normal((1, 2, 320, 12, 16))
+        p = {"weight": rng.uniform(-.2, .2, (320, 320, 3, 3)) / np.sqrt(2880) * 2.5, "bias": rng.standard_normal(320)}
+        kind, attrs = OpKind.CONV2D, {"out_channels": 320}
+    elif case == "conv_cat":
+        x = rng.standard_normal((1, 2, 960, 8, 8))
+        p = {"weight": rng.uniform(-.2, .2, (640, 960, 3, 3)) / np.sqrt(8640) * 2.5, "bias": rng.standard_normal(640)}
+        kind, attrs = OpKind.CONV2D, {"out_channels": 640}
+    elif case == "tconv":
+        x = rng.standard_normal((1, 25, 320, 4, 8))
+        p = {"weight": rng.uniform(-.2, .2, (320, 320, 3)) / np.sqrt(960) * 2.5, "bias": rng.standard_normal(320)}
+        kind, attrs = OpKind.TEMPORAL_CONV, {"out_channels": 320}
+    elif case == "linear":
+        x = rng.standard_normal((1, 3, 960, 8, 8))
+        p = {"weight": rng.uniform(-.2, .2, (320, 960)) / np.sqrt(960) * 2.5, "bias": rng.standard_normal(320)}
+        kind, attrs = OpKind.LINEAR, {"out_features": 320}
+    elif case == "sattn":
+        x = rng.standard_normal((1, 2, 320, 16, 24))
+        p = {k: rng.uniform(-.2, .2, (320, 320)) / np.sqrt(320) * 2.5 for k in ("wq", "wk", "wv", "wo")}
+        kind, attrs = OpKind.SPATIAL_ATTENTION, {}
+    else:
+        x = rng.standard_normal((1, 25, 640, 2, 4))
+        p = {k: rng.uniform(-.2, .2, (640, 640)) / np.sqrt(640) * 2.5 for k in ("wq", "wk", "wv", "wo")}
+        kind, attrs = OpKind.TEMPORAL_ATTENTION, {}
+    ref = _oracle_kernel(kind, x, p, attrs)
+    y = ops.apply_kernel(kind, [Tensor5D(x)], p, attrs, backend=backend)
+    r = rel(y.data, ref)
+    print(case, backend, r)
+    assert r <= 1.5e-2
+
+
+@pytest.fixture(scope="module")
+def c1_denoiser():
+    return Denoiser(C1)
+
+
+def test_c1_full_denoise_matches_reference(golden, c1_denoiser):
+    runs = golden["runs"]
+    x0 = initial_latent(C1)
+    x, S = c1_denoiser.calibrate(x0)
+    r = rel(x, runs["c1_float64_final"])
+    s_err = float(np.abs(S.values - runs["c1_float64_S"]).max())
+    print("c1 final rel", r, "S err", s_err)
+    assert r <= 2e-2
+    assert s_err <= 5e-3
+    # identical schedule wherever the decision margin exceeds the similarity error
+    for g, G in golden["meta"]["c1_G"].items():
+        sch = key_step_search(runs["c1_float64_S"], float(g))
+        if sch.margin is not None and sch.margin > 2 * s_err:
+            assert key_step_search(S, float(g)).key_steps == G, g
+
+
+def test_c1_rehash_matches_reference(golden, c1_denoiser):
+    runs = golden["runs"]
+    G = golden["meta"]["c1_G"]["0.93"]
+    x = c1_denoiser.run(initial_latent(C1), StepSchedule(G, 10))
+    r = rel(x, runs["c1_float64_rehash_g093_final"])
+    print("c1 rehash rel", r)
+    assert r <= 2e-2
+
+
+def test_all_key_schedule_is_bit_identical(c1_denoiser):
+    x0 = initial_latent(C1)
+    a = c1_denoiser.run(x0, None)
+    b = c1_denoiser.run(x0, StepSchedule(list(range(10)), 10))
+    assert np.array_equal(a, b)
+    c = c1_denoiser.run(x0, None)
+    assert np.array_equal(a, c)  # deterministic kernels
+
+
+def test_wide_config_matches_reference(golden):
+    runs = golden["runs"]
+    den = Denoiser(WIDE)
+    x = den.run(initial_latent(WIDE), None)
+    r = rel(x, runs["wide_float64_final"])
+    print("wide final rel", r)
+    assert r <= 2e-2
