@@ -1,11 +1,572 @@
-// tcgen05 / TMEM / TMA implicit GEMM (sm_100a).  Placeholder until the
-// kernel lands: reports every shape unsupported so sf_gemm uses mma.sync.
+// tcgen05 / TMEM / TMA implicit GEMM for sm_100a.
+//
+// One persistent, warp-specialised kernel covers every contraction of the
+// sliceflow path whose channel counts are multiples of 64:
+//   * conv2d 3x3 (kernels.py:181-201): A tiles are 128-pixel rectangles of one
+//     frame loaded by a 4-D TMA box {64 ch, w_t, h_t, 1} per (tap, channel
+//     block); the zero padding is TMA's out-of-bounds fill;
+//   * temporal conv, 3 taps (kernels.py:204-225): 4-D box {64 ch, pixels,
+//     frames, 1}; tap j shifts the frame coordinate by j-1, OOB frames -> 0;
+//   * linear / attention projections / batched attention GEMMs (plain rows).
+// B (weights, or K for S = Q K^T, or V^T) is always K-major.
+//
+// Roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM
+// allocation), warps 2..5 = epilogue (TMEM -> registers -> bias / per-frame
+// bias / SiLU / residual -> global).  Shared-memory ring of STAGES
+// {A 128x64, B BNx64} bf16 tiles in the canonical K-major SWIZZLE_128B layout;
+// two TMEM accumulators (2 x BN fp32 columns) so the epilogue of tile t
+// overlaps the mainloop of tile t+1.
 #include "common.cuh"
 
+#include <cuda.h>
+#include <mutex>
+
 namespace sf {
-bool gemm_tc_supported(const sf_gemm_args&) { return false; }
-sf_status gemm_tc_launch(const sf_gemm_args&, cudaStream_t) {
-  set_error("tcgen05 backend not built");
-  return SF_ERR_UNSUPPORTED;
+namespace tc {
+
+constexpr int BM = 128, BK = 64;
+constexpr int NUM_THREADS = 192;
+
+struct Params {
+  int mode;
+  // M tiling
+  int n_inner, n_outer, T;   // PLAIN: o over n_outer (and z over batch); TCONV: o = b*T + t
+  int bi, bo;                // rows of a tile = bo outer x bi inner (PLAIN/TCONV)
+  int tiles_i, tiles_o, n_z; // PLAIN: tiles_o over n_outer, n_z = batch; TCONV: tiles_o over T, n_z = B
+  int H, W, w_t, h_t, tiles_x, tiles_y;  // CONV
+  int64_t tiles_m;
+  int tiles_n, N, BN;
+  int taps, cblocks;         // K loop = taps x cblocks (64-channel blocks)
+  int cin;
+  int b_batched;             // B map has a batch coordinate (z)
+  // epilogue
+  float alpha;
+  const float* bias;
+  const float* rowbias;
+  int64_t rowbias_stride;
+  int act;
+  sf_view_t res;
+  int64_t res_bstride;
+  sf_view_t out;
+  int64_t out_bstride;
+  int out_fp32;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// K-major, SWIZZLE_128B UMMA shared-memory descriptor (canonical layout
+// ((8,n),2):((8,SBO),1) in 16-byte units: SBO = 1024 B, LBO unused = 1).
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // version = 1 (sm100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N=n
+__host__ __device__ constexpr uint32_t make_idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// ---------------------------------------------------------------- tiling
+struct MTile {
+  int z, o0, i0;   // PLAIN/TCONV: batch/b, outer start (t0 or o0), inner start
+  int f, y0, x0;   // CONV
+};
+
+__device__ __forceinline__ MTile decode_m(const Params& p, int64_t tm) {
+  MTile t{};
+  if (p.mode == SF_GEMM_CONV3X3) {
+    t.x0 = (int)(tm % p.tiles_x) * p.w_t;
+    int64_t r = tm / p.tiles_x;
+    t.y0 = (int)(r % p.tiles_y) * p.h_t;
+    t.f = (int)(r / p.tiles_y);
+  } else {
+    t.i0 = (int)(tm % p.tiles_i) * p.bi;
+    int64_t r = tm / p.tiles_i;
+    t.o0 = (int)(r % p.tiles_o) * p.bo;
+    t.z = (int)(r / p.tiles_o);
+  }
+  return t;
+}
+
+template <int BN, int STAGES>
+struct SmemLayout {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mapA,
+                   const __grid_constant__ CUtensorMap mapB) {
+  using L = SmemLayout<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                 : (2 * BN <= 256) ? 256 : 512;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&mapA);
+    prefetch_map(&mapB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int64_t n_tiles = p.tiles_m * p.tiles_n;
+  const int kiters = p.taps * p.cblocks;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t tm = tile / p.tiles_n;
+        const int n0 = (int)(tile % p.tiles_n) * BN;
+        const MTile mt = decode_m(p, tm);
+        for (int it = 0; it < kiters; ++it) {
+          const int tap = it / p.cblocks, cb = it % p.cblocks;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], L::STAGE_BYTES);
+          void* dA = sA + stage * L::A_BYTES;
+          void* dB = sB + stage * L::B_BYTES;
+          if (p.mode == SF_GEMM_CONV3X3) {
+            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1, mt.f);
+          } else if (p.mode == SF_GEMM_TCONV3) {
+            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
+          } else {
+            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0, mt.z);
+          }
+          tma_load_3d(&mapB, &full[stage], dB, tap * p.cin + cb * BK, n0, p.b_batched ? mt.z : 0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int it = 0; it < kiters; ++it) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * L::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * L::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_f16(d, make_sdesc(a0 + k * 32), make_sdesc(b0 + k * 32), idesc, (it | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ================= epilogue =================
+    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;          // accumulator row == TMEM lane
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t tm = tile / p.tiles_n;
+      const int n0 = (int)(tile % p.tiles_n) * BN;
+      const MTile mt = decode_m(p, tm);
+      // output row of this thread
+      bool valid;
+      int64_t o, i;
+      int z = 0;
+      if (p.mode == SF_GEMM_CONV3X3) {
+        const int y = mt.y0 + row / p.w_t, x = mt.x0 + row % p.w_t;
+        valid = y < p.H && x < p.W;
+        o = mt.f;
+        i = (int64_t)y * p.W + x;
+      } else {
+        const int oo = mt.o0 + row / p.bi, ii = mt.i0 + row % p.bi;
+        if (p.mode == SF_GEMM_TCONV3) {
+          valid = oo < p.T && ii < p.n_inner;
+          o = (int64_t)mt.z * p.T + oo;
+        } else {
+          valid = oo < p.n_outer && ii < p.n_inner;
+          o = oo;
+          z = mt.z;
+        }
+        i = ii;
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tbase + c, v);
+        const int nb = n0 + c;
+        if (valid && nb < p.N) {
+          const int ncols = min(32, p.N - nb);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+          if (p.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncols) v[j] += __ldg(p.bias + nb + j);
+          }
+          if (p.rowbias) {
+            const float* rb = p.rowbias + o * p.rowbias_stride + nb;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncols) v[j] += __ldg(rb + j);
+          }
+          if (p.act == SF_ACT_SILU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+          }
+          if (p.res.ptr) {
+            const bf16* rr = reinterpret_cast<const bf16*>(p.res.ptr) + (int64_t)z * p.res_bstride +
+                             (o * p.res.ostride + i) * p.res.ld + nb;
+            if (ncols == 32) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                float f[8];
+                unpack8(reinterpret_cast<const bf16x8*>(rr)[j], f);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[j * 8 + e] += f[e];
+              }
+            } else {
+              for (int j = 0; j < ncols; ++j) v[j] += __bfloat162float(rr[j]);
+            }
+          }
+          if (p.out_fp32) {
+            float* dst = reinterpret_cast<float*>(p.out.ptr) + (int64_t)z * p.out_bstride +
+                         (o * p.out.ostride + i) * p.out.ld + nb;
+            if (ncols == 32) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+              for (int j = 0; j < ncols; ++j) dst[j] = v[j];
+            }
+          } else {
+            bf16* dst = reinterpret_cast<bf16*>(p.out.ptr) + (int64_t)z * p.out_bstride +
+                        (o * p.out.ostride + i) * p.out.ld + nb;
+            if (ncols == 32) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) reinterpret_cast<bf16x8*>(dst)[j] = pack8(v + 8 * j);
+            } else {
+              for (int j = 0; j < ncols; ++j) dst[j] = __float2bfloat16(v[j]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                   const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+  }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b, e,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int pow2_floor(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+
+static int pick_bn(int N) {
+  if (N % 256 == 0 && N >= 1024) return 256;
+  if (N % 160 == 0) return 160;
+  if (N % 128 == 0) return 128;
+  if (N <= 64) return 64;
+  return 128;
+}
+
+}  // namespace tc
+
+bool gemm_tc_supported(const sf_gemm_args& a) {
+  if (!a.w_kmajor) return false;
+  if (a.cin % 64) return false;
+  if (a.N % 16) return false;
+  if (a.out_fp32 == 0 && (a.out.ld % 8 || !aligned16(a.out.ptr))) return false;
+  if (a.res.ptr && (a.res.ld % 8 || !aligned16(a.res.ptr))) return false;
+  if (a.mode == SF_GEMM_CONV3X3 && a.batch != 1) return false;
+  if (a.mode == SF_GEMM_TCONV3 && a.batch != 1) return false;
+  // strides must be multiples of 16 bytes for TMA
+  if ((a.a.ostride * a.a.ld * 2) % 16 || (a.a_bstride * 2) % 16 || (a.w_bstride * 2) % 16) return false;
+  return tc::encode_fn() != nullptr;
+}
+
+template <int BN, int STAGES>
+static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st) {
+  constexpr int smem = tc::SmemLayout<BN, STAGES>::TOTAL;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  int64_t tiles = p.tiles_m * p.tiles_n;
+  int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  tc::tc_gemm_kernel<BN, STAGES><<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb);
+  return launch_status("sf_gemm(tcgen05)");
+}
+
+sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
+  using namespace tc;
+  Params p{};
+  p.mode = a.mode;
+  p.N = a.N;
+  p.cin = a.cin;
+  p.cblocks = a.cin / BK;
+  p.taps = a.mode == SF_GEMM_PLAIN ? 1 : (a.mode == SF_GEMM_CONV3X3 ? 9 : 3);
+  p.alpha = a.alpha;
+  p.bias = a.bias;
+  p.rowbias = a.rowbias;
+  p.rowbias_stride = a.rowbias_stride;
+  p.act = a.act;
+  p.res = a.res;
+  p.res_bstride = a.res_bstride;
+  p.out = a.out;
+  p.out_bstride = a.out_bstride;
+  p.out_fp32 = a.out_fp32;
+  const int BN = pick_bn(a.N);
+  p.BN = BN;
+  p.tiles_n = (a.N + BN - 1) / BN;
+
+  CUtensorMap ma, mb;
+  const uint64_t es = 2;
+  const uint64_t ld = (uint64_t)a.a.ld;
+  if (a.mode == SF_GEMM_CONV3X3) {
+    p.H = a.H;
+    p.W = a.W;
+    p.w_t = pow2_floor(a.W < 128 ? a.W : 128);
+    p.h_t = BM / p.w_t;
+    p.tiles_x = (a.W + p.w_t - 1) / p.w_t;
+    p.tiles_y = (a.H + p.h_t - 1) / p.h_t;
+    p.tiles_m = (int64_t)p.tiles_x * p.tiles_y * a.n_outer;
+    uint64_t dims[4] = {(uint64_t)a.cin, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.n_outer};
+    uint64_t str[3] = {ld * es, (uint64_t)a.W * ld * es, (uint64_t)a.a.ostride * ld * es};
+    uint32_t box[4] = {BK, (uint32_t)p.w_t, (uint32_t)p.h_t, 1};
+    if (a.n_outer == 1) str[2] = (uint64_t)a.H * a.W * ld * es;
+    SF_CHECK_ARG(encode(&ma, a.a.ptr, 4, dims, str, box), SF_ERR_CUDA, "tensor map A (conv)");
+  } else {
+    int n_inner = a.n_inner, n_outer = a.n_outer;
+    int64_t ostride = a.a.ostride;
+    auto flat = [&](const sf_view_t& v) { return v.ostride == n_inner || n_outer == 1; };
+    bool contiguous = flat(a.a) && flat(a.out) && (!a.res.ptr || flat(a.res)) &&
+                      (!a.rowbias || a.rowbias_stride == 0);
+    if (a.mode == SF_GEMM_PLAIN && contiguous && a.batch == 1 && (int64_t)n_inner * n_outer < (1ll << 31)) {
+      n_inner = n_inner * n_outer;  // collapse to one row range
+      n_outer = 1;
+      ostride = n_inner;
+    }
+    p.n_inner = n_inner;
+    p.bi = n_inner >= BM ? BM : pow2_floor(n_inner);
+    p.bo = BM / p.bi;
+    p.tiles_i = (n_inner + p.bi - 1) / p.bi;
+    uint64_t dims[4], str[3];
+    dims[0] = (uint64_t)a.cin * p.taps / p.taps;  // channels of one tap
+    dims[1] = (uint64_t)n_inner;
+    str[0] = ld * es;
+    str[1] = (uint64_t)(ostride ? ostride : n_inner) * ld * es;
+    if (a.mode == SF_GEMM_TCONV3) {
+      p.T = a.T;
+      p.n_outer = a.n_outer;
+      p.n_z = a.n_outer / a.T;
+      p.tiles_o = (a.T + p.bo - 1) / p.bo;
+      dims[2] = (uint64_t)a.T;
+      dims[3] = (uint64_t)p.n_z;
+      str[2] = (uint64_t)a.T * str[1];
+    } else {
+      p.n_outer = n_outer;
+      p.n_z = a.batch;
+      p.tiles_o = (n_outer + p.bo - 1) / p.bo;
+      dims[2] = (uint64_t)n_outer;
+      dims[3] = (uint64_t)a.batch;
+      str[2] = a.batch > 1 ? (uint64_t)a.a_bstride * es : (uint64_t)n_outer * str[1];
+      if (str[2] == 0) str[2] = str[1];
+    }
+    p.tiles_m = (int64_t)p.tiles_i * p.tiles_o * p.n_z;
+    uint32_t box[4] = {BK, (uint32_t)p.bi, (uint32_t)p.bo, 1};
+    SF_CHECK_ARG(encode(&ma, a.a.ptr, 4, dims, str, box), SF_ERR_CUDA, "tensor map A");
+  }
+  {
+    const int taps = p.taps;
+    uint64_t dims[3] = {(uint64_t)taps * a.cin, (uint64_t)a.N, (uint64_t)(a.batch > 1 ? a.batch : 1)};
+    uint64_t str[2] = {(uint64_t)a.w_ld * es, (uint64_t)(a.batch > 1 ? a.w_bstride : a.w_ld * a.N) * es};
+    uint32_t box[3] = {BK, (uint32_t)BN, 1};
+    p.b_batched = a.batch > 1 && a.mode == SF_GEMM_PLAIN;
+    SF_CHECK_ARG(encode(&mb, a.w, 3, dims, str, box), SF_ERR_CUDA, "tensor map B");
+  }
+  switch (BN) {
+    case 256: return launch_cfg<256, 4>(p, ma, mb, st);
+    case 160: return launch_cfg<160, 5>(p, ma, mb, st);
+    case 128: return launch_cfg<128, 6>(p, ma, mb, st);
+    default: return launch_cfg<64, 8>(p, ma, mb, st);
+  }
+}
+
 }  // namespace sf

@@ -1,0 +1,103 @@
+"""sf_gemm backends vs a torch fp32 reference of the same contraction (B200 only).
+
+Every implicit-GEMM mode (plain rows, 3x3 conv im2col, 3-tap temporal conv,
+batched attention GEMMs, two-level row views, fused epilogue) is run on the
+tcgen05/TMA backend and on the mma.sync backend and compared with
+torch.float32 math on the same bf16-rounded operands.  Tolerance: max_rel
+<= 1e-2 (fp32 accumulation, one bf16 rounding of the output).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.nn.functional as F  # noqa: E402
+
+from paper_2411_01171_b200 import _native as N  # noqa: E402
+from paper_2411_01171_b200 import device as D  # noqa: E402
+from paper_2411_01171_b200.build import build  # noqa: E402
+from paper_2411_01171_b200.device import Rows  # noqa: E402
+
+build()
+dev = torch.device("cuda")
+
+
+def rel(a, b):
+    return float((a.float() - b.float()).abs().max() / b.float().abs().max())
+
+
+def rnd(*shape, scale=1.0):
+    return (torch.randn(*shape, device=dev) * scale).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("backend", [1, 2])
+@pytest.mark.parametrize("M,K,Nn", [(1000, 320, 320), (4096, 640, 1920), (256, 1280, 1280), (77, 64, 96)])
+def test_plain(backend, M, K, Nn):
+    torch.manual_seed(0)
+    a, w = rnd(M, K), rnd(Nn, K, scale=K ** -0.5)
+    bias = torch.randn(Nn, device=dev)
+    res = rnd(M, Nn)
+    out = torch.empty(M, Nn, dtype=torch.bfloat16, device=dev)
+    args = D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=M, cin=K, n=Nn,
+                  a=Rows(a), w=w, out=Rows(out), bias=bias, res=Rows(res), act=N.ACT_SILU, backend=backend)
+    assert N.query("sf_gemm_backend", args) == backend
+    ref = F.silu(a.float() @ w.float().T + bias) + res.float()
+    assert rel(out, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("backend", [1, 2])
+@pytest.mark.parametrize("F_,H,W,C,Co", [(3, 72, 128, 64, 320), (2, 36, 64, 320, 640), (2, 9, 16, 128, 160),
+                                         (1, 16, 16, 64, 64)])
+def test_conv3x3(backend, F_, H, W, C, Co):
+    torch.manual_seed(1)
+    x = rnd(F_, H, W, C)
+    w = rnd(Co, C, 3, 3, scale=(9 * C) ** -0.5)
+    wk = w.permute(0, 2, 3, 1).reshape(Co, 9 * C).contiguous()
+    bias = torch.randn(Co, device=dev)
+    emb = torch.randn(Co, device=dev)
+    out = torch.empty(F_ * H * W, Co, dtype=torch.bfloat16, device=dev)
+    D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_CONV3X3, n_outer=F_, n_inner=H * W, H=H, W=W, cin=C,
+           n=Co, a=Rows(x.view(-1, C), 0, H * W), w=wk, out=Rows(out, 0, H * W), bias=bias, rowbias=emb,
+           backend=backend)
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float(), bias, padding=1) + emb[None, :, None, None]
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Co)
+    assert rel(out, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("backend", [1, 2])
+@pytest.mark.parametrize("B,T,P,C,band", [(1, 25, 576, 320, None), (1, 25, 144, 128, None), (2, 8, 64, 64, None),
+                                          (1, 16, 1024, 64, (100, 612))])
+def test_tconv(backend, B, T, P, C, band):
+    torch.manual_seed(2)
+    x = rnd(B * T * P, C)
+    w = rnd(C, C, 3, scale=(3 * C) ** -0.5)
+    wk = w.permute(0, 2, 1).reshape(C, 3 * C).contiguous()
+    res = rnd(B * T * P, C)
+    out = torch.zeros(B * T * P, C, dtype=torch.bfloat16, device=dev)
+    p0, p1 = band if band else (0, P)
+    D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_TCONV3, n_outer=B * T, n_inner=p1 - p0, T=T, cin=C,
+           n=C, a=Rows(x, p0, P), w=wk, out=Rows(out, p0, P), res=Rows(res, p0, P), backend=backend)
+    xc = x.float().view(B, T, P, C).permute(0, 2, 3, 1).reshape(B * P, C, T)
+    ref = F.conv1d(xc, w.float(), padding=1).reshape(B, P, C, T).permute(0, 3, 1, 2).reshape(-1, C) + res.float()
+    got = out.view(B, T, P, C)[:, :, p0:p1].reshape(-1, C)
+    assert rel(got, ref.view(B, T, P, C)[:, :, p0:p1].reshape(-1, C)) <= 1e-2
+
+
+@pytest.mark.parametrize("backend", [1, 2])
+@pytest.mark.parametrize("Fr,HW,C", [(2, 2304, 320), (3, 576, 640)])
+def test_batched_scores(backend, Fr, HW, C):
+    """S = q k^T * alpha per frame straight out of a fused qkv buffer, fp32 out."""
+    torch.manual_seed(3)
+    qkv = rnd(Fr * HW, 3 * C)
+    s = torch.empty(Fr * HW, HW, dtype=torch.float32, device=dev)
+    D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=HW, cin=C, n=HW,
+           a=Rows(qkv), w=qkv, w_ptr=qkv.data_ptr() + C * 2, w_ld=3 * C, out=Rows(s), out_fp32=True, batch=Fr,
+           a_bstride=HW * 3 * C, w_bstride=HW * 3 * C, out_bstride=HW * HW, alpha=0.05, backend=backend)
+    q = qkv.float().view(Fr, HW, 3 * C)[..., :C]
+    k = qkv.float().view(Fr, HW, 3 * C)[..., C:2 * C]
+    ref = (q @ k.transpose(1, 2) * 0.05).reshape(-1, HW)
+    assert rel(s, ref) <= 1e-2
