@@ -147,12 +147,8 @@ sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, 
 /* ---- network edges ---- */
 /* in_conv with tiny cin: x fp32 channels-last [frames][H*W][cin] -> bf16 rows */
 sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t W, int32_t cin,
-                              const float* w /*[co][ci][3][3] fp32*/, const float* bias, int32_t cout,
+                              const float* w /*[3][3][ci][co] fp32*/, const float* bias, int32_t cout,
                               sf_view_t y, void* stream);
-/* out_conv with tiny cout: bf16 rows -> fp32 channels-last [frames][H*W][cout] */
-sf_status sf_conv3x3_smallcout(sf_view_t x, int32_t frames, int32_t H, int32_t W, int32_t cin,
-                               const float* w /*[co][ci][3][3] fp32*/, const float* bias, int32_t cout,
-                               float* y, void* stream);
 /* y[n] = W[n][:] . e + b[n] for a batch of step embeddings (res-block emb_proj) */
 sf_status sf_gemv_f32(const float* W, const float* e, const float* b, float* y, int32_t N, int32_t K,
                       void* stream);

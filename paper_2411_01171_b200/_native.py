@@ -62,7 +62,6 @@ _PROTOS = {
     "sf_softmax_rows": [vp, i64, vp, i64, i64, i32, vp],
     "sf_temporal_attention_core": [View, i32, i32, View, i32, i32, i32, i32, f32, vp],
     "sf_conv3x3_smallcin": [vp, i32, i32, i32, i32, vp, vp, i32, View, vp],
-    "sf_conv3x3_smallcout": [View, i32, i32, i32, i32, vp, vp, i32, vp, vp],
     "sf_gemv_f32": [vp, vp, vp, vp, i32, i32, vp],
     "sf_bcthw_to_rows_f32": [vp, vp, i32, i32, i32, vp],
     "sf_rows_to_bcthw_f32": [vp, vp, i32, i32, i32, vp],

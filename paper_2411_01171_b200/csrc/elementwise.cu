@@ -395,9 +395,10 @@ __global__ void __launch_bounds__(256) temporal_attn_kernel(sf_view_t qkv, int k
 // ---------------------------------------------------------------------------
 // latent-edge convolutions with tiny channel counts (in_conv / out_conv)
 // ---------------------------------------------------------------------------
-// in_conv: cin <= 16, fp32 input; one thread per (pixel, 8 output channels)
+// in_conv: tiny cin, fp32 input; one thread per (pixel, 8 output channels).
+// Weights in [tap][ci][co] so a warp's weight reads are contiguous in co.
 __global__ void conv_smallcin_kernel(const float* __restrict__ x, int frames, int H, int W, int cin,
-                                     const float* __restrict__ w, const float* __restrict__ bias, int cout,
+                                     const float* __restrict__ wt, const float* __restrict__ bias, int cout,
                                      sf_view_t y) {
   const int nvec = cout / 8;
   const int64_t total = (int64_t)frames * H * W * nvec;
@@ -409,57 +410,22 @@ __global__ void conv_smallcin_kernel(const float* __restrict__ x, int frames, in
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    for (int dy = 0; dy < 3; ++dy) {
-      int yy = py + dy - 1;
-      if (yy < 0 || yy >= H) continue;
-      for (int dx = 0; dx < 3; ++dx) {
-        int xx = px + dx - 1;
-        if (xx < 0 || xx >= W) continue;
-        const float* src = x + (((int64_t)f * H + yy) * W + xx) * cin;
-        for (int ci = 0; ci < cin; ++ci) {
-          float a = src[ci];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] += a * w[(((int64_t)(v * 8 + j) * cin + ci) * 3 + dy) * 3 + dx];
-        }
+    for (int tap = 0; tap < 9; ++tap) {
+      int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+      if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+      const float* src = x + (((int64_t)f * H + yy) * W + xx) * cin;
+      const float* wr = wt + (int64_t)tap * cin * cout + v * 8;
+      for (int ci = 0; ci < cin; ++ci) {
+        float a = __ldg(src + ci);
+        float4 w0 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)ci * cout));
+        float4 w1 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)ci * cout) + 1);
+        acc[0] += a * w0.x; acc[1] += a * w0.y; acc[2] += a * w0.z; acc[3] += a * w0.w;
+        acc[4] += a * w1.x; acc[5] += a * w1.y; acc[6] += a * w1.z; acc[7] += a * w1.w;
       }
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] += bias[v * 8 + j];
     *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, (int64_t)py * W + px) + v * 8) = pack8(acc);
-  }
-}
-
-// out_conv: small cout; one warp per pixel, lanes stride over (tap, channel vector)
-template <int MAXCO>
-__global__ void conv_smallcout_kernel(sf_view_t x, int frames, int H, int W, int cin,
-                                      const float* __restrict__ wt /*[9][cin][cout]*/,
-                                      const float* __restrict__ bias, int cout, float* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  const int64_t npix = (int64_t)frames * H * W;
-  const int nvec = cin / 8;
-  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < npix;
-       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    int px = p % W, py = (p / W) % H, f = p / ((int64_t)W * H);
-    float acc[MAXCO];
-#pragma unroll
-    for (int j = 0; j < MAXCO; ++j) acc[j] = 0.f;
-    for (int e = lane; e < 9 * nvec; e += 32) {
-      int tap = e / nvec, v = e % nvec;
-      int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
-      if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
-      float a[8];
-      unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (int64_t)yy * W + xx) + v * 8), a);
-      const float* wr = wt + ((int64_t)tap * cin + v * 8) * cout;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-#pragma unroll
-        for (int co = 0; co < MAXCO; ++co)
-          if (co < cout) acc[co] += a[j] * wr[j * cout + co];
-    }
-#pragma unroll
-    for (int co = 0; co < MAXCO; ++co) acc[co] = warp_sum(acc[co]);
-    if (lane == 0)
-      for (int co = 0; co < cout; ++co) y[p * cout + co] = acc[co] + bias[co];
   }
 }
 
@@ -752,22 +718,6 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
   int64_t total = (int64_t)frames * H * W * (cout / 8);
   conv_smallcin_kernel<<<ew_grid(total, 128), 128, 0, (cudaStream_t)stream>>>(x, frames, H, W, cin, w, bias, cout, y);
   return launch_status("sf_conv3x3_smallcin");
-}
-
-sf_status sf_conv3x3_smallcout(sf_view_t x, int32_t frames, int32_t H, int32_t W, int32_t cin, const float* wt,
-                               const float* bias, int32_t cout, float* y, void* stream) {
-  SF_CHECK_ARG(cout >= 1 && cout <= 16 && cin % 8 == 0, SF_ERR_SHAPE, "need cout <= 16 and cin % 8 == 0");
-  SF_CHECK_ARG(view_vec8_ok(x), SF_ERR_PARAM, "unaligned view");
-  int64_t npix = (int64_t)frames * H * W;
-  cudaStream_t st = (cudaStream_t)stream;
-  int grid = ew_grid(npix * 32, 256);
-  if (cout <= 4)
-    conv_smallcout_kernel<4><<<grid, 256, 0, st>>>(x, frames, H, W, cin, wt, bias, cout, y);
-  else if (cout <= 8)
-    conv_smallcout_kernel<8><<<grid, 256, 0, st>>>(x, frames, H, W, cin, wt, bias, cout, y);
-  else
-    conv_smallcout_kernel<16><<<grid, 256, 0, st>>>(x, frames, H, W, cin, wt, bias, cout, y);
-  return launch_status("sf_conv3x3_smallcout");
 }
 
 sf_status sf_gemv_f32(const float* W, const float* e, const float* b, float* y, int32_t N, int32_t K, void* stream) {

@@ -39,6 +39,7 @@ struct Params {
   int taps, cblocks;         // K loop = taps x cblocks (64-channel blocks)
   int cin;
   int b_batched;             // B map has a batch coordinate (z)
+  int a_batched;             // A map has a batch coordinate (0: one A shared by every batch)
   // epilogue
   float alpha;
   const float* bias;
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else if (p.mode == SF_GEMM_TCONV3) {
             tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
           } else {
-            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0, mt.z);
+            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0, p.a_batched ? mt.z : 0);
           }
           tma_load_3d(&mapB, &full[stage], dB, tap * p.cin + cb * BK, n0, p.b_batched ? mt.z : 0);
           if (++stage == STAGES) {
@@ -450,7 +451,6 @@ static int pick_bn(int N) {
 bool gemm_tc_supported(const sf_gemm_args& a) {
   if (!a.w_kmajor) return false;
   if (a.cin % 64) return false;
-  if (a.N % 16) return false;
   if (a.out_fp32 == 0 && (a.out.ld % 8 || !aligned16(a.out.ptr))) return false;
   if (a.res.ptr && (a.res.ld % 8 || !aligned16(a.res.ptr))) return false;
   if (a.mode == SF_GEMM_CONV3X3 && a.batch != 1) return false;
@@ -544,10 +544,10 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
       p.n_outer = n_outer;
       p.n_z = a.batch;
       p.tiles_o = (n_outer + p.bo - 1) / p.bo;
+      p.a_batched = a.batch > 1 && a.a_bstride != 0;
       dims[2] = (uint64_t)n_outer;
-      dims[3] = (uint64_t)a.batch;
-      str[2] = a.batch > 1 ? (uint64_t)a.a_bstride * es : (uint64_t)n_outer * str[1];
-      if (str[2] == 0) str[2] = str[1];
+      dims[3] = p.a_batched ? (uint64_t)a.batch : 1;
+      str[2] = p.a_batched ? (uint64_t)a.a_bstride * es : (uint64_t)n_outer * str[1];
     }
     p.tiles_m = (int64_t)p.tiles_i * p.tiles_o * p.n_z;
     uint32_t box[4] = {BK, (uint32_t)p.bi, (uint32_t)p.bo, 1};

@@ -141,11 +141,12 @@ class Epilogue:
         self.act, self.rowbias, self.res = act, rowbias, res
 
 
-def conv2d(stream, x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue, backend=0):
+def conv2d(stream, x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue, backend=0, out_fp32=False):
     if "w" not in prm:
         raise ShapeMismatch(f"conv2d with cin={cin} needs the small-channel path")
     return gemm(stream, mode=N.GEMM_CONV3X3, n_outer=frames, n_inner=H * W, H=H, W=W, cin=cin, n=cout, a=x,
-                w=prm["w"], out=y, bias=prm["bias"], rowbias=epi.rowbias, act=epi.act, res=epi.res, backend=backend)
+                w=prm["w"], out=y, out_fp32=out_fp32, bias=prm["bias"], rowbias=epi.rowbias, act=epi.act,
+                res=epi.res, backend=backend)
 
 
 def temporal_conv(stream, x: Rows, y: Rows, bt, T, n_inner, cin, cout, prm, epi: Epilogue, backend=0):
@@ -183,7 +184,7 @@ def spatial_attention(stream, x: Rows, y: Rows, frames, HW, C, prm, epi: Epilogu
     p [frames*HW, HW] bf16, o [frames*HW, C] bf16.
     """
     qkv, o = scratch["qkv"], scratch["o"]
-    gemm(stream, mode=N.GEMM_PLAIN, n_outer=frames, n_inner=HW, cin=C, n=3 * C, a=x,
+    gemm(stream, mode=N.GEMM_PLAIN, n_outer=frames, n_inner=HW, cin=C, n=3 * C if HW <= SMALL_SEQ else 2 * C, a=x,
          w=prm["wqkv"], out=Rows(qkv, 0, HW), backend=backend)
     if HW <= SMALL_SEQ:
         # short token sequences (deep toy levels): the fused per-sequence core,
@@ -191,6 +192,13 @@ def spatial_attention(stream, x: Rows, y: Rows, frames, HW, C, prm, epi: Epilogu
         N.call("sf_temporal_attention_core", Rows(qkv, 0, 1).view(), C, 2 * C, Rows(o, 0, 1).view(), frames, HW, 1,
                C, 1.0 / math.sqrt(C), stream)
     else:
+        # v^T[c][t] = sum_k wv[k][c] x[t][k]: the weights as A (M = C) and the
+        # frame's tokens as a K-major B, so P v below is K-major on both sides
+        vt = scratch["vt"]
+        xv = x.view()
+        gemm(stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=C, cin=C, n=HW, a=Rows(prm["wqkv"], 2 * C, 0),
+             w=vt, w_ptr=xv.ptr, w_ld=xv.ld, out=Rows(vt, 0, 0), batch=frames, a_bstride=0,
+             w_bstride=HW * xv.ld, out_bstride=C * HW, backend=backend)
         _spatial_core_materialized(stream, frames, HW, C, scratch, backend)
     gemm(stream, mode=N.GEMM_PLAIN, n_outer=frames, n_inner=HW, cin=C, n=C, a=Rows(o, 0, HW), w=prm["wo"],
          out=y, rowbias=epi.rowbias, act=epi.act, res=epi.res, backend=backend)
@@ -208,10 +216,10 @@ def _spatial_core_materialized(stream, frames, HW, C, scratch, backend):
          out=Rows(s, 0, 0), out_fp32=True, batch=frames, a_bstride=HW * 3 * C, w_bstride=HW * 3 * C,
          out_bstride=HW * HW, alpha=1.0 / math.sqrt(C), backend=backend)
     N.call("sf_softmax_rows", s.data_ptr(), HW, p.data_ptr(), HW, frames * HW, HW, stream)
+    vt = scratch["vt"]
     gemm(stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=HW, cin=HW, n=C, a=Rows(p, 0, 0),
-         w=qkv, w_ptr=qkv.data_ptr() + 2 * C * qkv.element_size(), w_ld=3 * C, w_kmajor=False,
-         out=Rows(o, 0, 0), batch=frames, a_bstride=HW * HW, w_bstride=HW * 3 * C, out_bstride=HW * C,
-         backend=backend)
+         w=vt, w_ld=HW, out=Rows(o, 0, 0), batch=frames, a_bstride=HW * HW, w_bstride=C * HW,
+         out_bstride=HW * C, backend=backend)
 
 
 def temporal_attention(stream, x: Rows, y: Rows, B, T, n_inner, C, prm, epi: Epilogue, scratch, backend=0):

@@ -460,6 +460,7 @@ class Plan:
                 if hw > D.SMALL_SEQ:
                     specs["s"] = (fmax * hw, hw, torch.float32)
                     specs["p"] = (fmax * hw, hw, torch.bfloat16)
+                    specs["vt"] = (fmax * shape.c, hw, torch.bfloat16)
             shape = out_shape
             i += 2 if fuse_act else 1
         if gn_need:
@@ -503,11 +504,11 @@ class Plan:
                         if latent_in and src == "IN":
                             lat = self.latent[sl[0] * ihw:]
                             N.call("sf_conv3x3_smallcin", lat.data_ptr(), nf, ish.h, ish.w, ish.c,
-                                   prm["w32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), st)
+                                   prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), st)
                         elif last and eps_out:
-                            out = self.eps[sl[0] * ohw:]
-                            N.call("sf_conv3x3_smallcout", X.view(), nf, ish.h, ish.w, ish.c,
-                                   prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, out.data_ptr(), st)
+                            # out_conv: fp32 network output straight from the GEMM epilogue
+                            out = Rows(self.eps, sl[0] * ohw, ohw)
+                            D.conv2d(st, X, out, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend, out_fp32=True)
                         else:
                             D.conv2d(st, X, Y, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend)
                     elif k is OpKind.LINEAR:

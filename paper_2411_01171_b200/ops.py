@@ -72,14 +72,14 @@ def apply_kernel(kind: OpKind, inputs: Sequence[Tensor5D], params: Mapping | Non
         if s.c % 8:
             x = to_rows(inputs[0], torch.float32)
             y = torch.empty(orows, out_s.c, dtype=torch.bfloat16, device=dev)
-            N.call("sf_conv3x3_smallcin", x.data_ptr(), frames, s.h, s.w, s.c, p["w32"].data_ptr(),
+            N.call("sf_conv3x3_smallcin", x.data_ptr(), frames, s.h, s.w, s.c, p["wt32"].data_ptr(),
                    p["bias"].data_ptr(), out_s.c, Rows(y).view(), st)
             return from_rows(y, out_s)
         x = to_rows(inputs[0])
         if out_s.c % 8:
             y = torch.empty(orows, out_s.c, dtype=torch.float32, device=dev)
-            N.call("sf_conv3x3_smallcout", Rows(x, 0, hw).view(), frames, s.h, s.w, s.c, p["wt32"].data_ptr(),
-                   p["bias"].data_ptr(), out_s.c, y.data_ptr(), st)
+            D.conv2d(st, Rows(x, 0, hw), Rows(y, 0, hw), frames, s.h, s.w, s.c, out_s.c, p, Epilogue(), backend,
+                     out_fp32=True)
             return from_rows(y, out_s)
         y = torch.empty(orows, out_s.c, dtype=torch.bfloat16, device=dev)
         D.conv2d(st, Rows(x, 0, hw), Rows(y, 0, hw), frames, s.h, s.w, s.c, out_s.c, p, Epilogue(), backend)
@@ -117,6 +117,7 @@ def apply_kernel(kind: OpKind, inputs: Sequence[Tensor5D], params: Mapping | Non
             sc = {"qkv": torch.empty(rows, 3 * s.c, dtype=torch.bfloat16, device=dev),
                   "s": torch.empty(rows, hw, dtype=torch.float32, device=dev),
                   "p": torch.empty(rows, hw, dtype=torch.bfloat16, device=dev),
+                  "vt": torch.empty(frames * s.c, hw, dtype=torch.bfloat16, device=dev),
                   "o": torch.empty(rows, s.c, dtype=torch.bfloat16, device=dev)}
             D.spatial_attention(st, Rows(x, 0, hw), Rows(y, 0, hw), frames, hw, s.c, p, Epilogue(), sc, backend)
         else:
