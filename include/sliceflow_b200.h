@@ -138,6 +138,13 @@ sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int
 /* Row softmax of fp32 scores S[rows][n] (already scaled) -> bf16 P[rows][n]. */
 sf_status sf_softmax_rows(const float* s, int64_t lds, void* p, int64_t ldp, int64_t rows, int32_t n,
                           void* stream);
+/* Fused spatial attention core (flash, tcgen05/TMEM): per frame,
+ * out = softmax(q k^T * scale) v over HW tokens, head_dim C in {128,192,256,320}.
+ * q, k: bf16 row views (o = frame, i = token) sharing one row stride; vt: bf16
+ * V^T [frames][C][HW]. */
+int32_t sf_flash_supported(int32_t HW, int32_t C);
+sf_status sf_spatial_attention_core(sf_view_t q, sf_view_t k, const void* vt, sf_view_t out, int32_t frames,
+                                    int32_t HW, int32_t C, float scale, void* stream);
 /* Temporal attention core per pixel: q|k|v rows (o = b*T+t, i = pixel), q at
  * column 0, k at qkv_koff, v at qkv_voff of view qkv; writes softmax(q k^T *
  * scale) v into out.  T <= 64. */

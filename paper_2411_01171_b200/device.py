@@ -186,7 +186,15 @@ def spatial_attention(stream, x: Rows, y: Rows, frames, HW, C, prm, epi: Epilogu
     qkv, o = scratch["qkv"], scratch["o"]
     gemm(stream, mode=N.GEMM_PLAIN, n_outer=frames, n_inner=HW, cin=C, n=3 * C if HW <= SMALL_SEQ else 2 * C, a=x,
          w=prm["wqkv"], out=Rows(qkv, 0, HW), backend=backend)
-    if HW <= SMALL_SEQ:
+    if HW > SMALL_SEQ and use_flash(HW, C):
+        vt = scratch["vt"]
+        xv = x.view()
+        gemm(stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=C, cin=C, n=HW, a=Rows(prm["wqkv"], 2 * C, 0),
+             w=vt, w_ptr=xv.ptr, w_ld=xv.ld, out=Rows(vt, 0, 0), batch=frames, a_bstride=0,
+             w_bstride=HW * xv.ld, out_bstride=C * HW, backend=backend)
+        N.call("sf_spatial_attention_core", Rows(qkv, 0, HW).view(), Rows(qkv, 0, HW, C).view(), vt.data_ptr(),
+               Rows(o, 0, HW).view(), frames, HW, C, 1.0 / math.sqrt(C), stream)
+    elif HW <= SMALL_SEQ:
         # short token sequences (deep toy levels): the fused per-sequence core,
         # each frame's HW tokens as one sequence (row b*HW + t, ostride 1)
         N.call("sf_temporal_attention_core", Rows(qkv, 0, 1).view(), C, 2 * C, Rows(o, 0, 1).view(), frames, HW, 1,
@@ -205,6 +213,23 @@ def spatial_attention(stream, x: Rows, y: Rows, frames, HW, C, prm, epi: Epilogu
 
 
 SMALL_SEQ = 64
+FLASH = True  # fused tcgen05 attention where supported (tests flip it to compare paths)
+
+
+def use_flash(HW, C) -> bool:
+    return FLASH and HW % 8 == 0 and bool(N.query("sf_flash_supported", HW, C))
+
+
+def spatial_attention_scratch(rows, HW, C) -> dict:
+    """Slice scratch the spatial attention lowering needs: {name: (rows, cols, dtype)}."""
+    out = {"qkv": (rows, 3 * C, torch.bfloat16), "o": (rows, C, torch.bfloat16)}
+    frames = rows // HW
+    if HW > SMALL_SEQ:
+        out["vt"] = (frames * C, HW, torch.bfloat16)
+        if not use_flash(HW, C):
+            out["s"] = (rows, HW, torch.float32)
+            out["p"] = (rows, HW, torch.bfloat16)
+    return out
 
 
 def _spatial_core_materialized(stream, frames, HW, C, scratch, backend):

@@ -408,7 +408,8 @@ class Plan:
         shape = s
         for o in ops:
             if o.kind is OpKind.SPATIAL_ATTENTION:
-                per_frame += HW * 3 * C * 2 + HW * HW * 6 + HW * C * 2
+                per_frame += sum(r * c * torch.empty((), dtype=dt).element_size()
+                                 for r, c, dt in D.spatial_attention_scratch(HW, HW, C).values())
             per_frame += shape.h * shape.w * max(shape.c, 8) * 2 * 2
         k = self._k_for(per_frame, frames, self.cfg.spatial_k)
         slices = balanced(frames, k)
@@ -455,12 +456,7 @@ class Plan:
                 gn_need = max(gn_need or 0, N.query("sf_group_norm_workspace", fmax, shape.h * shape.w, shape.c))
             if o.kind is OpKind.SPATIAL_ATTENTION:
                 hw = shape.h * shape.w
-                specs["qkv"] = (fmax * hw, 3 * shape.c, torch.bfloat16)
-                specs["o"] = (fmax * hw, shape.c, torch.bfloat16)
-                if hw > D.SMALL_SEQ:
-                    specs["s"] = (fmax * hw, hw, torch.float32)
-                    specs["p"] = (fmax * hw, hw, torch.bfloat16)
-                    specs["vt"] = (fmax * shape.c, hw, torch.bfloat16)
+                specs.update(D.spatial_attention_scratch(fmax * hw, hw, shape.c))
             shape = out_shape
             i += 2 if fuse_act else 1
         if gn_need:

@@ -114,11 +114,8 @@ def apply_kernel(kind: OpKind, inputs: Sequence[Tensor5D], params: Mapping | Non
             _require_shape(_req(params, n, kind), (s.c, s.c), kind)
         p = _convert(kind, attrs, params, dev)
         if kind is OpKind.SPATIAL_ATTENTION:
-            sc = {"qkv": torch.empty(rows, 3 * s.c, dtype=torch.bfloat16, device=dev),
-                  "s": torch.empty(rows, hw, dtype=torch.float32, device=dev),
-                  "p": torch.empty(rows, hw, dtype=torch.bfloat16, device=dev),
-                  "vt": torch.empty(frames * s.c, hw, dtype=torch.bfloat16, device=dev),
-                  "o": torch.empty(rows, s.c, dtype=torch.bfloat16, device=dev)}
+            sc = {k: torch.empty(r, c, dtype=dt, device=dev)
+                  for k, (r, c, dt) in D.spatial_attention_scratch(rows, hw, s.c).items()}
             D.spatial_attention(st, Rows(x, 0, hw), Rows(y, 0, hw), frames, hw, s.c, p, Epilogue(), sc, backend)
         else:
             sc = {"qkv": torch.empty(rows, 3 * s.c, dtype=torch.bfloat16, device=dev),

@@ -101,3 +101,22 @@ def test_batched_scores(backend, Fr, HW, C):
     k = qkv.float().view(Fr, HW, 3 * C)[..., C:2 * C]
     ref = (q @ k.transpose(1, 2) * 0.05).reshape(-1, HW)
     assert rel(s, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("Fr,HW,C", [(2, 9216, 320), (3, 2304, 320), (2, 200, 320), (2, 576, 128), (1, 1000, 192),
+                                     (2, 4096, 256)])
+def test_flash_core(Fr, HW, C):
+    """Fused tcgen05 attention core vs torch softmax(q k^T / sqrt(C)) v (fp32 math)."""
+    if not N.query("sf_flash_supported", HW, C):
+        pytest.skip("shape not supported by the fused core")
+    torch.manual_seed(4)
+    qkv = rnd(Fr * HW, 2 * C, scale=1.5)
+    v = rnd(Fr, HW, C)
+    vt = v.transpose(1, 2).contiguous()
+    o = torch.empty(Fr * HW, C, dtype=torch.bfloat16, device=dev)
+    N.call("sf_spatial_attention_core", Rows(qkv, 0, HW).view(), Rows(qkv, 0, HW, C).view(), vt.data_ptr(),
+           Rows(o, 0, HW).view(), Fr, HW, C, C ** -0.5, torch.cuda.current_stream().cuda_stream)
+    q = qkv.float().view(Fr, HW, 2 * C)[..., :C]
+    k = qkv.float().view(Fr, HW, 2 * C)[..., C:]
+    ref = torch.softmax(q @ k.transpose(1, 2) * C ** -0.5, dim=-1) @ v.float()
+    assert rel(o.view(Fr, HW, C), ref) <= 1.5e-2
