@@ -393,6 +393,182 @@ __global__ void __launch_bounds__(256) temporal_attn_kernel(sf_view_t qkv, int k
 }
 
 // ---------------------------------------------------------------------------
+// temporal attention core, tensor-core version for T <= 32: one warp per pixel.
+// S (32x32, fp32 fragments) accumulated over 64-channel chunks with
+// mma.sync m16n8k16; softmax on the fragments (quad shuffles); P re-packed as
+// the A operand; O = P V per 64-channel chunk, V read with ldmatrix.trans.
+// Rows t >= T are zero-filled and their scores masked.
+// ---------------------------------------------------------------------------
+constexpr int TQ_WARPS = 4, TQ_CH = 64, TQ_LD = TQ_CH + 8;
+
+__device__ __forceinline__ void tq_ldsm_x4(unsigned* r, const void* p) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(s));
+}
+__device__ __forceinline__ void tq_ldsm_x4_t(unsigned* r, const void* p) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(s));
+}
+__device__ __forceinline__ void tq_mma(float* c, const unsigned* a, unsigned b0, unsigned b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ unsigned pack_bf2(float a, float b) {
+  bf162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<unsigned*>(&h);
+}
+
+// copy a [32 tokens][64 ch] chunk (columns col0..col0+63) into smem, zero rows t >= T / ch >= C
+__device__ __forceinline__ void tq_load(bf16 (*dst)[TQ_LD], const sf_view_t& v, int b, int T, int pix, int col0,
+                                        int cvalid, int lane) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int idx = lane + 32 * k;     // 256 vectors = 32 rows x 8
+    int t = idx >> 3, c = (idx & 7) * 8;
+    bf16x8 val;
+    if (t < T && c < cvalid) {
+      val = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(v, (int64_t)b * T + t, pix) + col0 + c);
+    } else {
+      val.h[0] = val.h[1] = val.h[2] = val.h[3] = __floats2bfloat162_rn(0.f, 0.f);
+    }
+    *reinterpret_cast<bf16x8*>(&dst[t][c]) = val;
+  }
+}
+
+__global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
+                                                                          sf_view_t out, int B, int T, int n_inner,
+                                                                          int C, float scale_log2) {
+  extern __shared__ __align__(16) unsigned char tq_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bf16 (*qs)[TQ_LD] = reinterpret_cast<bf16 (*)[TQ_LD]>(tq_smem + warp * 3 * 32 * TQ_LD * 2);
+  bf16 (*ks)[TQ_LD] = qs + 32;
+  bf16 (*vs)[TQ_LD] = qs + 64;
+  const int64_t gp = (int64_t)blockIdx.x * TQ_WARPS + warp;   // global pixel (b, pix)
+  if (gp >= (int64_t)B * n_inner) return;
+  const int b = gp / n_inner, pix = gp % n_inner;
+  float sacc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sacc[i][j][e] = 0.f;
+  for (int c0 = 0; c0 < C; c0 += TQ_CH) {
+    const int cv = min(TQ_CH, C - c0);
+    tq_load(qs, qkv, b, T, pix, c0, cv, lane);
+    tq_load(ks, qkv, b, T, pix, koff + c0, cv, lane);
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < TQ_CH; kk += 16) {
+      unsigned a[2][4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) tq_ldsm_x4(a[mi], &qs[mi * 16 + (lane & 15)][kk + (lane >> 4) * 8]);
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        unsigned r[4];
+        tq_ldsm_x4(r, &ks[nj * 16 + (lane & 7) + ((lane >> 4) << 3)][kk + ((lane >> 3) & 1) * 8]);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          tq_mma(sacc[mi][2 * nj], a[mi], r[0], r[1]);
+          tq_mma(sacc[mi][2 * nj + 1], a[mi], r[2], r[3]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // softmax over columns (keys) per row; lane holds rows lane/4 (+8) of each m-tile
+  float rsum[2][2];
+  const int colq = (lane & 3) * 2;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float m = -INFINITY;
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int col = nj * 8 + colq + e;
+          float v = col < T ? sacc[mi][nj][h * 2 + e] * scale_log2 : -INFINITY;
+          sacc[mi][nj][h * 2 + e] = v;
+          m = fmaxf(m, v);
+        }
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      float sum = 0.f;
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float pv = exp2f(sacc[mi][nj][h * 2 + e] - m);
+          sacc[mi][nj][h * 2 + e] = pv;
+          sum += pv;
+        }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      rsum[mi][h] = 1.f / sum;
+    }
+  }
+  // P as A fragments: k-step kk covers keys 16kk..16kk+15 = n-tiles 2kk, 2kk+1
+  unsigned pa[2][2][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      pa[mi][kk][0] = pack_bf2(sacc[mi][2 * kk][0], sacc[mi][2 * kk][1]);
+      pa[mi][kk][1] = pack_bf2(sacc[mi][2 * kk][2], sacc[mi][2 * kk][3]);
+      pa[mi][kk][2] = pack_bf2(sacc[mi][2 * kk + 1][0], sacc[mi][2 * kk + 1][1]);
+      pa[mi][kk][3] = pack_bf2(sacc[mi][2 * kk + 1][2], sacc[mi][2 * kk + 1][3]);
+    }
+  for (int c0 = 0; c0 < C; c0 += TQ_CH) {
+    const int cv = min(TQ_CH, C - c0);
+    tq_load(vs, qkv, b, T, pix, voff + c0, cv, lane);
+    __syncwarp();
+    float oacc[2][8][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) oacc[i][j][e] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj) {
+        unsigned r[4];
+        // V [k=token][n=ch]: trans loads (k0-7,n),(k8-15,n),(k0-7,n+8),(k8-15,n+8)
+        tq_ldsm_x4_t(r, &vs[kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8][nj * 16 + (lane >> 4) * 8]);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          tq_mma(oacc[mi][2 * nj], pa[mi][kk], r[0], r[1]);
+          tq_mma(oacc[mi][2 * nj + 1], pa[mi][kk], r[2], r[3]);
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = mi * 16 + (lane >> 2) + h * 8;
+        if (t >= T) continue;
+        bf16* dst = row_ptr<bf16>(out, (int64_t)b * T + t, pix) + c0;
+#pragma unroll
+        for (int nj = 0; nj < 8; ++nj) {
+          const int c = nj * 8 + colq;
+          if (c < cv)
+            *reinterpret_cast<bf162*>(dst + c) =
+                __floats2bfloat162_rn(oacc[mi][nj][h * 2] * rsum[mi][h], oacc[mi][nj][h * 2 + 1] * rsum[mi][h]);
+        }
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // latent-edge convolutions with tiny channel counts (in_conv / out_conv)
 // ---------------------------------------------------------------------------
 // in_conv: tiny cin, fp32 input; one thread per (pixel, 8 output channels).
@@ -707,6 +883,19 @@ sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, 
                                      int32_t n_inner, int32_t C, float scale, void* stream) {
   SF_CHECK_ARG(T >= 1 && T <= TA_MAXT, SF_ERR_SHAPE, "temporal attention supports 1 <= T <= 64");
   SF_CHECK_ARG(B >= 1 && n_inner >= 1 && C >= 1, SF_ERR_SHAPE, "bad extents");
+  if (T <= 32 && C % 8 == 0 && koff % 8 == 0 && voff % 8 == 0 && view_vec8_ok(qkv) && out.ld % 2 == 0) {
+    const int smem = TQ_WARPS * 3 * 32 * TQ_LD * 2;
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(temporal_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      init = true;
+    }
+    int64_t warps = (int64_t)B * n_inner;
+    temporal_attn_mma_kernel<<<(unsigned)((warps + TQ_WARPS - 1) / TQ_WARPS), TQ_WARPS * 32, smem,
+                               (cudaStream_t)stream>>>(qkv, koff, voff, out, B, T, n_inner, C,
+                                                       scale * 1.4426950408889634f);
+    return launch_status("sf_temporal_attention_core");
+  }
   temporal_attn_kernel<<<B * n_inner, 256, 0, (cudaStream_t)stream>>>(qkv, koff, voff, out, T, n_inner, C, scale);
   return launch_status("sf_temporal_attention_core");
 }

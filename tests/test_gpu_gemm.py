@@ -120,3 +120,18 @@ def test_flash_core(Fr, HW, C):
     k = qkv.float().view(Fr, HW, 2 * C)[..., C:]
     ref = torch.softmax(q @ k.transpose(1, 2) * C ** -0.5, dim=-1) @ v.float()
     assert rel(o.view(Fr, HW, C), ref) <= 1.5e-2
+
+
+@pytest.mark.parametrize("B,T,P,C", [(1, 25, 300, 320), (2, 8, 64, 32), (1, 32, 50, 640), (1, 64, 20, 64),
+                                     (1, 16, 40, 1280), (1, 3, 10, 24)])
+def test_temporal_core(B, T, P, C):
+    """Per-pixel attention over T frames vs torch (rows o = b*T+t, i = pixel)."""
+    torch.manual_seed(5)
+    qkv = rnd(B * T * P, 3 * C, scale=1.5)
+    o = torch.empty(B * T * P, C, dtype=torch.bfloat16, device=dev)
+    N.call("sf_temporal_attention_core", Rows(qkv, 0, P).view(), C, 2 * C, Rows(o, 0, P).view(), B, T, P, C,
+           C ** -0.5, torch.cuda.current_stream().cuda_stream)
+    x = qkv.float().view(B, T, P, 3 * C).permute(0, 2, 1, 3)
+    q, k, v = x[..., :C], x[..., C:2 * C], x[..., 2 * C:]
+    ref = (torch.softmax(q @ k.transpose(-1, -2) * C ** -0.5, dim=-1) @ v).permute(0, 2, 1, 3).reshape(-1, C)
+    assert rel(o, ref) <= 1.5e-2
