@@ -26,6 +26,7 @@ namespace tc {
 
 constexpr int BM = 128, BK = 64;
 constexpr int NUM_THREADS = 192;
+constexpr int EPI_W0 = 2;  // first epilogue warp
 
 struct Params {
   int mode;
@@ -39,6 +40,7 @@ struct Params {
   int taps, cblocks;         // K loop = taps x cblocks (64-channel blocks)
   int cin;
   int b_batched;             // B map has a batch coordinate (z)
+  int collapsed;             // PLAIN rows collapsed into one contiguous range
   int a_batched;             // A map has a batch coordinate (0: one A shared by every batch)
   // epilogue
   float alpha;
@@ -92,6 +94,11 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
           "r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -168,28 +175,35 @@ __device__ __forceinline__ MTile decode_m(const Params& p, int64_t tm) {
   return t;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool TMA_EPI>
 struct SmemLayout {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  // epilogue staging tile [128 rows][BN] bf16 (residual in, output out), row-major
+  static constexpr int OUT_BYTES = TMA_EPI ? BM * BN * 2 : 0;
+  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + OUT_BYTES + 256 /*barriers*/;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool TMA_EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mapA,
-                   const __grid_constant__ CUtensorMap mapB) {
-  using L = SmemLayout<BN, STAGES>;
+                   const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapR,
+                   const __grid_constant__ CUtensorMap mapO) {
+  using L = SmemLayout<BN, STAGES, TMA_EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * L::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint8_t* sOut = smem + STAGES * L::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + L::OUT_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* res_full = tempty + 2;    // residual tile landed in sOut
+  uint64_t* out_free = res_full + 1;  // previous tile's TMA store finished reading sOut
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(out_free + 1);
+  const bool has_res = TMA_EPI && p.res.ptr != nullptr;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
@@ -205,6 +219,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    mbar_init(res_full, 1);
+    mbar_init(out_free, 1);
+    if (TMA_EPI) {
+      prefetch_map(&mapO);
+      if (has_res) prefetch_map(&mapR);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -226,11 +246,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      uint32_t tcount = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
         const int64_t tm = tile / p.tiles_n;
         const int n0 = (int)(tile % p.tiles_n) * BN;
         const MTile mt = decode_m(p, tm);
+        bool res_pending = has_res;
         for (int it = 0; it < kiters; ++it) {
+          if (res_pending && it == (kiters > 2 ? 2 : kiters - 1)) {
+            // residual tile for this tile's epilogue, once sOut is free again
+            res_pending = false;
+            mbar_wait(out_free, (tcount & 1) ^ 1);
+            mbar_expect_tx(res_full, L::OUT_BYTES);
+            if (p.mode == SF_GEMM_CONV3X3)
+              tma_load_4d(&mapR, res_full, sOut, n0, mt.x0, mt.y0, mt.f);
+            else
+              tma_load_4d(&mapR, res_full, sOut, n0, mt.i0, mt.o0, mt.z);
+          }
           const int tap = it / p.cblocks, cb = it % p.cblocks;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], L::STAGE_BYTES);
@@ -291,7 +323,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row = q * 32 + lane;          // accumulator row == TMEM lane
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    uint32_t tcount = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const int64_t tm = tile / p.tiles_n;
       const int n0 = (int)(tile % p.tiles_n) * BN;
       const MTile mt = decode_m(p, tm);
@@ -319,6 +352,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (TMA_EPI) {
+        if (has_res) mbar_wait(res_full, tcount & 1);
+        else mbar_wait(out_free, (tcount & 1) ^ 1);
+        uint8_t* srow = sOut + row * (BN * 2);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          const int nb = n0 + c;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+          if (p.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(p.bias + nb + j) : 0.f;
+          }
+          if (p.rowbias) {
+            const float* rb = p.rowbias + o * p.rowbias_stride + nb;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(rb + j) : 0.f;
+          }
+          if (p.act == SF_ACT_SILU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+          }
+          bf16x8* sp = reinterpret_cast<bf16x8*>(srow + c * 2);
+          if (has_res) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float f[8];
+              unpack8(sp[j], f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[j * 8 + e] += f[e];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sp[j] = pack8(v + 8 * j);
+        }
+        // TMEM slot free for the next-but-one tile
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        // staging tile complete -> one thread stores it with TMA (OOB rows/cols are clipped)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == EPI_W0 && lane == 0) {
+          if (p.mode == SF_GEMM_CONV3X3)
+            tma_store_4d(&mapO, sOut, n0, mt.x0, mt.y0, mt.f);
+          else
+            tma_store_4d(&mapO, sOut, n0, mt.i0, mt.o0, mt.z);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(out_free);
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
@@ -389,6 +481,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
+  if (TMA_EPI && warp == EPI_W0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -415,7 +508,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 static bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                   const uint32_t* box) {
+                   const uint32_t* box, bool swizzle = true) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], s[4];
@@ -427,7 +520,8 @@ static bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* d
   }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b, e,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -452,6 +546,8 @@ bool gemm_tc_supported(const sf_gemm_args& a) {
   if (!a.w_kmajor) return false;
   if (a.cin % 64) return false;
   if (a.out_fp32 == 0 && (a.out.ld % 8 || !aligned16(a.out.ptr))) return false;
+  if (a.out_fp32 == 0 && ((a.out.ostride * a.out.ld * 2) % 16 || (a.out_bstride * 2) % 16)) return false;
+  if (a.res.ptr && ((a.res.ostride * a.res.ld * 2) % 16 || (a.res_bstride * 2) % 16)) return false;
   if (a.res.ptr && (a.res.ld % 8 || !aligned16(a.res.ptr))) return false;
   if (a.mode == SF_GEMM_CONV3X3 && a.batch != 1) return false;
   if (a.mode == SF_GEMM_TCONV3 && a.batch != 1) return false;
@@ -460,18 +556,50 @@ bool gemm_tc_supported(const sf_gemm_args& a) {
   return tc::encode_fn() != nullptr;
 }
 
-template <int BN, int STAGES>
-static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st) {
-  constexpr int smem = tc::SmemLayout<BN, STAGES>::TOTAL;
+template <int BN, int STAGES, bool TMA_EPI>
+static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mr,
+                            const CUtensorMap& mo, cudaStream_t st) {
+  constexpr int smem = tc::SmemLayout<BN, STAGES, TMA_EPI>::TOTAL;
+  static_assert(smem <= 232448, "shared memory budget");
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, STAGES, TMA_EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     init = true;
   }
   int64_t tiles = p.tiles_m * p.tiles_n;
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  tc::tc_gemm_kernel<BN, STAGES><<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb);
+  tc::tc_gemm_kernel<BN, STAGES, TMA_EPI><<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb, mr, mo);
   return launch_status("sf_gemm(tcgen05)");
+}
+
+// Output / residual maps share the M tiling of A: box {BN cols, tile rows}.
+static bool encode_rows_map(CUtensorMap* m, const sf_gemm_args& a, const tc::Params& p, const sf_view_t& v,
+                            int64_t bstride, int BN) {
+  const uint64_t es = 2, ld = (uint64_t)v.ld;
+  if (a.mode == SF_GEMM_CONV3X3) {
+    uint64_t dims[4] = {(uint64_t)a.N, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.n_outer};
+    uint64_t str[3] = {ld * es, (uint64_t)a.W * ld * es,
+                       (uint64_t)(v.ostride ? v.ostride : (int64_t)a.H * a.W) * ld * es};
+    uint32_t box[4] = {(uint32_t)BN, (uint32_t)p.w_t, (uint32_t)p.h_t, 1};
+    return tc::encode(m, v.ptr, 4, dims, str, box, false);
+  }
+  uint64_t dims[4], str[3];
+  dims[0] = (uint64_t)a.N;
+  dims[1] = (uint64_t)p.n_inner;
+  str[0] = ld * es;
+  const int64_t ost = p.collapsed ? p.n_inner : (v.ostride ? v.ostride : p.n_inner);
+  str[1] = (uint64_t)ost * ld * es;
+  if (a.mode == SF_GEMM_TCONV3) {
+    dims[2] = (uint64_t)p.T;
+    dims[3] = (uint64_t)p.n_z;
+    str[2] = (uint64_t)p.T * str[1];
+  } else {
+    dims[2] = (uint64_t)p.n_outer;
+    dims[3] = (uint64_t)p.n_z;
+    str[2] = p.n_z > 1 ? (uint64_t)bstride * es : (uint64_t)p.n_outer * str[1];
+  }
+  uint32_t box[4] = {(uint32_t)BN, (uint32_t)p.bi, (uint32_t)p.bo, 1};
+  return tc::encode(m, v.ptr, 4, dims, str, box, false);
 }
 
 sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
@@ -522,6 +650,7 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
       n_inner = n_inner * n_outer;  // collapse to one row range
       n_outer = 1;
       ostride = n_inner;
+      p.collapsed = 1;
     }
     p.n_inner = n_inner;
     p.bi = n_inner >= BM ? BM : pow2_floor(n_inner);
@@ -561,11 +690,22 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
     p.b_batched = a.batch > 1 && a.mode == SF_GEMM_PLAIN;
     SF_CHECK_ARG(encode(&mb, a.w, 3, dims, str, box), SF_ERR_CUDA, "tensor map B");
   }
+  CUtensorMap mr = mb, mo = mb;
+  if (!a.out_fp32) {
+    SF_CHECK_ARG(encode_rows_map(&mo, a, p, a.out, a.out_bstride, BN), SF_ERR_CUDA, "tensor map out");
+    if (a.res.ptr) SF_CHECK_ARG(encode_rows_map(&mr, a, p, a.res, a.res_bstride, BN), SF_ERR_CUDA, "tensor map res");
+    switch (BN) {
+      case 256: return launch_cfg<256, 3, true>(p, ma, mb, mr, mo, st);
+      case 160: return launch_cfg<160, 5, true>(p, ma, mb, mr, mo, st);
+      case 128: return launch_cfg<128, 6, true>(p, ma, mb, mr, mo, st);
+      default: return launch_cfg<64, 8, true>(p, ma, mb, mr, mo, st);
+    }
+  }
   switch (BN) {
-    case 256: return launch_cfg<256, 4>(p, ma, mb, st);
-    case 160: return launch_cfg<160, 5>(p, ma, mb, st);
-    case 128: return launch_cfg<128, 6>(p, ma, mb, st);
-    default: return launch_cfg<64, 8>(p, ma, mb, st);
+    case 256: return launch_cfg<256, 4, false>(p, ma, mb, mr, mo, st);
+    case 160: return launch_cfg<160, 5, false>(p, ma, mb, mr, mo, st);
+    case 128: return launch_cfg<128, 6, false>(p, ma, mb, mr, mo, st);
+    default: return launch_cfg<64, 8, false>(p, ma, mb, mr, mo, st);
   }
 }
 

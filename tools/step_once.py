@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--backend", type=int, default=0)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--detail", action="store_true")
 a = ap.parse_args()
 cfg = UNetConfig(**CONFIGS[a.config])
 den = Denoiser(cfg, ExecConfig(gemm_backend=a.backend), K=2)
@@ -29,3 +30,29 @@ for _ in range(a.reps):
     den.plan.run_tail(st)
 torch.cuda.synchronize()
 print("ok", len(den.plan.units), "units")
+if a.detail:
+    from paper_2411_01171_b200 import _native as N
+    from paper_2411_01171_b200.profiling import gemm_flops
+    recs = []
+    orig = N.call
+
+    def rec(name, *args):
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record()
+        orig(name, *args)
+        e_.record()
+        info = ""
+        if name == "sf_gemm":
+            g = args[0]
+            info = (f"mode={g.mode} M={g.n_outer * g.n_inner} N={g.N} K={g.cin * (9 if g.mode == 1 else 3 if g.mode == 2 else 1)}"
+                    f" batch={g.batch} be={N.query('sf_gemm_backend', g)}")
+            recs.append((name, info, s_, e_, gemm_flops(g)))
+        else:
+            recs.append((name, info, s_, e_, 0.0))
+    N.call = rec
+    den.plan.run_full(st, den.emb_table[0].data_ptr())
+    torch.cuda.synchronize()
+    N.call = orig
+    for name, info, s_, e_, fl in recs:
+        ms = s_.elapsed_time(e_)
+        print(f"{ms*1e3:9.1f} us  {fl/ (ms*1e9) if fl else 0:7.1f} TF  {name} {info}")
