@@ -39,10 +39,11 @@ __device__ __forceinline__ T* row_ptr(const sf_view_t& v, int64_t o, int64_t i) 
 }
 
 __device__ __forceinline__ float silu_f(float x) {
-  // x * sigmoid(x) without exponentiating a positive argument (kernels.py:247-253)
-  float e = __expf(-fabsf(x));
-  float s = x >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
-  return x * s;
+  // x * sigmoid(x) without exponentiating a positive argument (kernels.py:247-253);
+  // one ex2 + one fast reciprocal (SiLU sits in GEMM epilogues, so it must be cheap)
+  const float e = __expf(-fabsf(x));
+  const float r = __fdividef(1.f, 1.f + e);
+  return x * (x >= 0.f ? r : e * r);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -175,22 +175,24 @@ __device__ __forceinline__ MTile decode_m(const Params& p, int64_t tm) {
   return t;
 }
 
-template <int BN, int STAGES, bool TMA_EPI>
+template <int BN, int STAGES, int EPI>
 struct SmemLayout {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // epilogue staging tile [128 rows][BN] bf16 (residual in, output out), row-major
-  static constexpr int OUT_BYTES = TMA_EPI ? BM * BN * 2 : 0;
+  static constexpr int OUT_TILE = BM * BN * 2;
+  static constexpr int OUT_BYTES = EPI * OUT_TILE;   // EPI staging buffers (0 = direct stores)
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + OUT_BYTES + 256 /*barriers*/;
 };
 
-template <int BN, int STAGES, bool TMA_EPI>
+template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapR,
                    const __grid_constant__ CUtensorMap mapO) {
-  using L = SmemLayout<BN, STAGES, TMA_EPI>;
+  using L = SmemLayout<BN, STAGES, EPI>;
+  constexpr bool TMA_EPI = EPI > 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -200,9 +202,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
-  uint64_t* res_full = tempty + 2;    // residual tile landed in sOut
-  uint64_t* out_free = res_full + 1;  // previous tile's TMA store finished reading sOut
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(out_free + 1);
+  uint64_t* res_full = tempty + 2;    // [2] residual tile landed in staging buffer b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 2);
   const bool has_res = TMA_EPI && p.res.ptr != nullptr;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -220,8 +221,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
     }
-    mbar_init(res_full, 1);
-    mbar_init(out_free, 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&res_full[b], 1);
     if (TMA_EPI) {
       prefetch_map(&mapO);
       if (has_res) prefetch_map(&mapR);
@@ -251,18 +251,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int64_t tm = tile / p.tiles_n;
         const int n0 = (int)(tile % p.tiles_n) * BN;
         const MTile mt = decode_m(p, tm);
-        bool res_pending = has_res;
         for (int it = 0; it < kiters; ++it) {
-          if (res_pending && it == (kiters > 2 ? 2 : kiters - 1)) {
-            // residual tile for this tile's epilogue, once sOut is free again
-            res_pending = false;
-            mbar_wait(out_free, (tcount & 1) ^ 1);
-            mbar_expect_tx(res_full, L::OUT_BYTES);
-            if (p.mode == SF_GEMM_CONV3X3)
-              tma_load_4d(&mapR, res_full, sOut, n0, mt.x0, mt.y0, mt.f);
-            else
-              tma_load_4d(&mapR, res_full, sOut, n0, mt.i0, mt.o0, mt.z);
-          }
           const int tap = it / p.cblocks, cb = it % p.cblocks;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], L::STAGE_BYTES);
@@ -349,13 +338,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         i = ii;
       }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if constexpr (TMA_EPI) {
-        if (has_res) mbar_wait(res_full, tcount & 1);
-        else mbar_wait(out_free, (tcount & 1) ^ 1);
-        uint8_t* srow = sOut + row * (BN * 2);
+        const bool leader = warp == EPI_W0 && lane == 0;
+        const int ob = EPI == 2 ? (int)(tcount & 1) : 0;
+        const uint32_t use = EPI == 2 ? (tcount >> 1) : tcount;
+        uint8_t* sbuf = sOut + ob * L::OUT_TILE;
+        if (EPI == 1) {
+          // single staging buffer: the previous store must have drained it; then fetch the residual
+          if (leader) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            if (has_res) {
+              mbar_expect_tx(&res_full[0], L::OUT_TILE);
+              if (p.mode == SF_GEMM_CONV3X3)
+                tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
+              else
+                tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        } else if (tcount == 0 && has_res && leader) {
+          // double staging: residual of the first tile; later ones are prefetched a tile ahead
+          mbar_expect_tx(&res_full[0], L::OUT_TILE);
+          if (p.mode == SF_GEMM_CONV3X3)
+            tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
+          else
+            tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        if (has_res) mbar_wait(&res_full[ob], use & 1);
+        uint8_t* srow = sbuf + row * (BN * 2);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
@@ -389,28 +402,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) sp[j] = pack8(v + 8 * j);
         }
-        // TMEM slot free for the next-but-one tile
+        // accumulator free for the tile after next
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         // staging tile complete -> one thread stores it with TMA (OOB rows/cols are clipped)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == EPI_W0 && lane == 0) {
+        if (leader) {
           if (p.mode == SF_GEMM_CONV3X3)
-            tma_store_4d(&mapO, sOut, n0, mt.x0, mt.y0, mt.f);
+            tma_store_4d(&mapO, sbuf, n0, mt.x0, mt.y0, mt.f);
           else
-            tma_store_4d(&mapO, sOut, n0, mt.i0, mt.o0, mt.z);
+            tma_store_4d(&mapO, sbuf, n0, mt.i0, mt.o0, mt.z);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          mbar_arrive(out_free);
+          if (EPI == 2) {
+            // the other buffer's store (tile t-1) must drain before it is refilled
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            const int64_t nt = tile + gridDim.x;
+            if (has_res && nt < n_tiles) {
+              const MTile nm = decode_m(p, nt / p.tiles_n);
+              const int nn0 = (int)(nt % p.tiles_n) * BN;
+              uint8_t* nbuf = sOut + (ob ^ 1) * L::OUT_TILE;
+              mbar_expect_tx(&res_full[ob ^ 1], L::OUT_TILE);
+              if (p.mode == SF_GEMM_CONV3X3)
+                tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.x0, nm.y0, nm.f);
+              else
+                tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.i0, nm.o0, nm.z);
+            }
+          }
         }
+        if (EPI == 2) asm volatile("bar.sync 1, 128;" ::: "memory");
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
         continue;
       }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
@@ -481,7 +510,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  if (TMA_EPI && warp == EPI_W0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (EPI > 0 && warp == EPI_W0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -556,19 +585,19 @@ bool gemm_tc_supported(const sf_gemm_args& a) {
   return tc::encode_fn() != nullptr;
 }
 
-template <int BN, int STAGES, bool TMA_EPI>
+template <int BN, int STAGES, int EPI>
 static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mr,
                             const CUtensorMap& mo, cudaStream_t st) {
-  constexpr int smem = tc::SmemLayout<BN, STAGES, TMA_EPI>::TOTAL;
+  constexpr int smem = tc::SmemLayout<BN, STAGES, EPI>::TOTAL;
   static_assert(smem <= 232448, "shared memory budget");
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, STAGES, TMA_EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     init = true;
   }
   int64_t tiles = p.tiles_m * p.tiles_n;
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  tc::tc_gemm_kernel<BN, STAGES, TMA_EPI><<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb, mr, mo);
+  tc::tc_gemm_kernel<BN, STAGES, EPI><<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb, mr, mo);
   return launch_status("sf_gemm(tcgen05)");
 }
 
@@ -694,18 +723,29 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   if (!a.out_fp32) {
     SF_CHECK_ARG(encode_rows_map(&mo, a, p, a.out, a.out_bstride, BN), SF_ERR_CUDA, "tensor map out");
     if (a.res.ptr) SF_CHECK_ARG(encode_rows_map(&mr, a, p, a.res, a.res_bstride, BN), SF_ERR_CUDA, "tensor map res");
+    // long K: deep operand ring + one staging buffer; short K: double staging so the
+    // epilogue (residual prefetch + TMA store) overlaps the next tile
+    const bool long_k = p.taps * p.cblocks >= 32;
+    if (long_k) {
+      switch (BN) {
+        case 256: return launch_cfg<256, 3, 1>(p, ma, mb, mr, mo, st);
+        case 160: return launch_cfg<160, 5, 1>(p, ma, mb, mr, mo, st);
+        case 128: return launch_cfg<128, 6, 1>(p, ma, mb, mr, mo, st);
+        default: return launch_cfg<64, 8, 1>(p, ma, mb, mr, mo, st);
+      }
+    }
     switch (BN) {
-      case 256: return launch_cfg<256, 3, true>(p, ma, mb, mr, mo, st);
-      case 160: return launch_cfg<160, 5, true>(p, ma, mb, mr, mo, st);
-      case 128: return launch_cfg<128, 6, true>(p, ma, mb, mr, mo, st);
-      default: return launch_cfg<64, 8, true>(p, ma, mb, mr, mo, st);
+      case 256: return launch_cfg<256, 2, 2>(p, ma, mb, mr, mo, st);
+      case 160: return launch_cfg<160, 4, 2>(p, ma, mb, mr, mo, st);
+      case 128: return launch_cfg<128, 5, 2>(p, ma, mb, mr, mo, st);
+      default: return launch_cfg<64, 7, 2>(p, ma, mb, mr, mo, st);
     }
   }
   switch (BN) {
-    case 256: return launch_cfg<256, 4, false>(p, ma, mb, mr, mo, st);
-    case 160: return launch_cfg<160, 5, false>(p, ma, mb, mr, mo, st);
-    case 128: return launch_cfg<128, 6, false>(p, ma, mb, mr, mo, st);
-    default: return launch_cfg<64, 8, false>(p, ma, mb, mr, mo, st);
+    case 256: return launch_cfg<256, 4, 0>(p, ma, mb, mr, mo, st);
+    case 160: return launch_cfg<160, 5, 0>(p, ma, mb, mr, mo, st);
+    case 128: return launch_cfg<128, 6, 0>(p, ma, mb, mr, mo, st);
+    default: return launch_cfg<64, 8, 0>(p, ma, mb, mr, mo, st);
   }
 }
 
