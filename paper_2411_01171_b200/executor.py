@@ -70,10 +70,14 @@ class ExecConfig:
     scratch_budget: int = 2 << 30
     gemm_backend: int = 0
     device: str = "cuda"
+    rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
+    world: int = 1
 
 
 def balanced(extent: int, k: int) -> list[tuple[int, int]]:
     """k nearly equal contiguous chunks (device slice plan)."""
+    if extent <= 0:
+        return []
     k = max(1, min(k, extent))
     base, rem = divmod(extent, k)
     out, s = [], 0
@@ -104,6 +108,7 @@ class Unit:
     label: str
     run: object                  # callable(stream)
     ref: tuple = ()              # schedule unit it lowers
+    exchange: object = None      # parallel.ExchangeOp for frame<->pixel exchange units
     reads: list = field(default_factory=list)
     writes: list = field(default_factory=list)
     gemm_flops: float = 0.0
@@ -125,9 +130,12 @@ class Plan:
         self.epilogue_of: dict[str, tuple[str, str, bool]] = {}  # producer tail -> (add id, operand, is_emb)
         self.units: list[Unit] = []
         self.emb_nodes: list[str] = []
+        self.exchanger = None
         self._analyse()
         self._layout()
         self._compile()
+        if cfg.world > 1:
+            self._insert_exchanges()
 
     # ------------------------------------------------------------------ analysis
     def _producer_group(self, vid):
@@ -296,6 +304,27 @@ class Plan:
         units = max(1, self.cfg.scratch_budget // max(1, per_unit_bytes))
         return max(1, math.ceil(extent / units))
 
+    def _insert_exchanges(self):
+        from .parallel import plan_exchanges
+        ins = plan_exchanges(self)
+        out, j = [], 0
+        for ui, u in enumerate(self.units):
+            while j < len(ins) and ins[j][0] == ui:
+                op = ins[j][1]
+                out.append(Unit(f"exchange[{op.value} {op.src}->{op.dst}]", self._exchange_runner(op), ref=u.ref,
+                                exchange=op))
+                j += 1
+            out.append(u)
+        self.units = out
+        self.n_exchanges = len(ins)
+
+    def _exchange_runner(self, op):
+        def run(st):
+            if self.exchanger is None:
+                raise InvalidParam("sharded plan has no exchanger attached")
+            self.exchanger.exchange(self, op, st)
+        return run
+
     def _compile(self):
         self.scratch_need = 0
         self._scratch_users = []
@@ -411,9 +440,11 @@ class Plan:
                 per_frame += sum(r * c * torch.empty((), dtype=dt).element_size()
                                  for r, c, dt in D.spatial_attention_scratch(HW, HW, C).values())
             per_frame += shape.h * shape.w * max(shape.c, 8) * 2 * 2
-        k = self._k_for(per_frame, frames, self.cfg.spatial_k)
-        slices = balanced(frames, k)
-        fmax = max(b - a for a, b in slices)
+        from .parallel import shard_range
+        f0, f1 = shard_range(frames, self.cfg.world, self.cfg.rank)
+        k = self._k_for(per_frame, f1 - f0, self.cfg.spatial_k)
+        slices = [(a + f0, b + f0) for a, b in balanced(f1 - f0, k)]
+        fmax = max([b - a for a, b in slices] + [1])
         tail = ops[-1].id
         x_id = grp.head_input
         latent_in = x_id == "x"
@@ -526,9 +557,11 @@ class Plan:
         per_pix = 0
         for o in ops:
             per_pix += B * T * C * 2 * (4 if o.kind is OpKind.TEMPORAL_ATTENTION else 1)
-        k = self._k_for(per_pix, HW, self.cfg.temporal_k)
-        bands = balanced(HW, k)
-        pmax = max(b - a for a, b in bands)
+        from .parallel import shard_range
+        p0, p1 = shard_range(HW, self.cfg.world, self.cfg.rank)
+        k = self._k_for(per_pix, p1 - p0, self.cfg.temporal_k)
+        bands = [(a + p0, b + p0) for a, b in balanced(p1 - p0, k)]
+        pmax = max([b - a for a, b in bands] + [1])
         tail = ops[-1].id
         x_id = grp.head_input
 
@@ -654,7 +687,7 @@ class DeviceModel:
     """Graph + device weights + compiled plan; the object behind execute/rehash/run_denoise."""
 
     def __init__(self, graph: Graph, weights, cfg: ExecConfig | None = None, grouped: GroupedGraph | None = None,
-                 unet_cfg: UNetConfig | None = None):
+                 unet_cfg: UNetConfig | None = None, device_weights: D.DeviceWeights | None = None):
         N.load()
         if not torch.cuda.is_available():
             from .errors import NativeError
@@ -666,7 +699,7 @@ class DeviceModel:
             xs = graph.inputs["x"]
             grouped = group_operators(graph, xs.b * xs.t, default_temporal_config(xs.h, xs.w))
         self.grouped = grouped
-        self.dw = D.DeviceWeights(graph, weights, self.cfg.device)
+        self.dw = device_weights or D.DeviceWeights(graph, weights, self.cfg.device)
         self.plan = Plan(graph, grouped, self.dw, self.cfg)
         xs = graph.inputs["x"]
         self.x_shape = xs

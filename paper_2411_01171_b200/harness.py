@@ -25,7 +25,8 @@ from .errors import ScheduleMismatch
 from .executor import DeviceModel, ExecConfig
 from .graph import Graph
 from .modes import ExecMode
-from .rehash import SimilarityMap, StepSchedule, gamma_for_target, gram_similarity, key_step_search, op_count_report
+from .rehash import (SimilarityMap, StepSchedule, gamma_for_target, gram_partial, gram_similarity, key_step_search,
+                     op_count_report, similarity_from_gram)
 from .tensor import Tensor5D
 from .unet import PROBE_LABEL, UNetConfig, build_toy_unet, sinusoidal_step_embedding
 
@@ -63,15 +64,17 @@ class Denoiser:
     """Device denoising loop over one UNetConfig (weights from build_toy_unet)."""
 
     def __init__(self, cfg: UNetConfig, exec_cfg: ExecConfig | None = None, graph: Graph | None = None,
-                 weights=None, K: int | None = None):
+                 weights=None, K: int | None = None, exchanger=None, device_weights=None):
         self.cfg = cfg
         self.K = K or cfg.steps
         if graph is None:
             graph, w64 = build_toy_unet(cfg)
             weights = w64
         self.graph = graph
-        self.model = DeviceModel(graph, weights, exec_cfg, unet_cfg=cfg)
+        self.exec_cfg = exec_cfg or ExecConfig()
+        self.model = DeviceModel(graph, weights, self.exec_cfg, unet_cfg=cfg, device_weights=device_weights)
         self.plan = self.model.plan
+        self.plan.exchanger = exchanger
         dev = self.model.dw.dev
         emb = np.stack([sinusoidal_step_embedding(s, cfg.emb_channels, cfg.emb_scale) for s in range(self.K)])
         self.emb_table = torch.from_numpy(emb.astype(np.float32)).to(dev).contiguous()
@@ -89,13 +92,21 @@ class Denoiser:
             if s in keys:
                 p.run_full(st, self.emb_table[s].data_ptr())
                 if record_trace:
+                    # this rank's rows of the probe (all of them unsharded; the pixel band
+                    # across all frames when sharded -- the probe is a temporal-group output)
                     pr = p.probe_rows()
                     sh = p.shapes[self.graph.node_by_label(PROBE_LABEL).id]
-                    N.call("sf_copy_rows", pr.view(), N.View(self.trace[s].data_ptr(), sh.c, 0), 1,
-                           sh.b * sh.t * sh.h * sh.w, sh.c, st)
+                    b0, b1 = self._probe_band()
+                    N.call("sf_copy_rows", pr.shifted(rows=b0, ostride=sh.h * sh.w).view(),
+                           N.View(self.trace[s].data_ptr(), sh.c, b1 - b0), sh.b * sh.t, b1 - b0, sh.c, st)
             else:
                 p.run_tail(st)
             N.call("sf_axpy_f32", p.latent.data_ptr(), p.eps.data_ptr(), alpha(s, self.K), n_lat, st)
+
+    def _probe_band(self):
+        from .parallel import shard_range
+        sh = self.plan.shapes[self.graph.node_by_label(PROBE_LABEL).id]
+        return shard_range(sh.h * sh.w, self.exec_cfg.world, self.exec_cfg.rank)
 
     def _key(self, schedule, record_trace):
         return (None if schedule is None else tuple(schedule.key_steps), record_trace)
@@ -107,7 +118,9 @@ class Denoiser:
         key = self._key(schedule, record_trace)
         if record_trace and self.trace is None:
             sh = self.plan.shapes[self.graph.node_by_label(PROBE_LABEL).id]
-            self.trace = torch.empty(self.K, sh.count(), dtype=torch.bfloat16, device=self.model.dw.dev)
+            b0, b1 = self._probe_band()
+            self.trace = torch.empty(self.K, sh.b * sh.t * (b1 - b0) * sh.c, dtype=torch.bfloat16,
+                                     device=self.model.dw.dev)
         if key in self._graphs:
             return key
         with _LaunchCounter() as c:
@@ -116,14 +129,19 @@ class Denoiser:
         self.launches[key] = c.n
         g = None
         if use_graph:
-            g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
-                    self._program(schedule, record_trace)
-            torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.synchronize()
+            try:
+                g = torch.cuda.CUDAGraph()
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(g, stream=s):
+                        self._program(schedule, record_trace)
+                torch.cuda.current_stream().wait_stream(s)
+                torch.cuda.synchronize()
+            except RuntimeError:
+                # a transport that cannot be captured (e.g. an old NCCL): replay eagerly
+                torch.cuda.synchronize()
+                g = None
         self._graphs[key] = g
         return key
 
@@ -141,7 +159,19 @@ class Denoiser:
 
     def result(self) -> np.ndarray:
         st = torch.cuda.current_stream().cuda_stream
-        return self.model.download(self.model.latent_to_bcthw(st, self.plan.latent))
+        lat = self.plan.latent
+        if self.exec_cfg.world > 1:
+            # every rank holds its own frames of the latent: zero the rest and sum
+            import torch.distributed as dist
+            from .parallel import shard_range
+            xs = self.model.x_shape
+            f0, f1 = shard_range(xs.b * xs.t, self.exec_cfg.world, self.exec_cfg.rank)
+            hw = xs.h * xs.w
+            lat = lat.clone()
+            lat[:f0 * hw].zero_()
+            lat[f1 * hw:].zero_()
+            dist.all_reduce(lat)
+        return self.model.download(self.model.latent_to_bcthw(st, lat))
 
     def run(self, x0: np.ndarray, schedule: StepSchedule | None = None, record_trace=False) -> np.ndarray:
         key = self.prepare(schedule, record_trace)
@@ -150,10 +180,19 @@ class Denoiser:
         return self.result()
 
     def calibrate(self, x0: np.ndarray) -> tuple[np.ndarray, SimilarityMap]:
-        """All-key run recording the probe each step; returns (final x, S)."""
+        """All-key run recording the probe each step; returns (final x, S).
+
+        Sharded: each rank's Gram partial (its pixel band) is summed across
+        ranks in fp64 before normalisation, so every rank derives the same G.
+        """
         x = self.run(x0, None, record_trace=True)
-        S = gram_similarity([self.trace[s] for s in range(self.K)], PROBE_LABEL)
-        return x, S
+        G = gram_partial([self.trace[s] for s in range(self.K)])
+        if self.exec_cfg.world > 1:
+            import torch.distributed as dist
+            t = torch.from_numpy(G).to(self.model.dw.dev)
+            dist.all_reduce(t)
+            G = t.cpu().numpy()
+        return x, similarity_from_gram(G, PROBE_LABEL)
 
     def tail_node_count(self) -> int:
         topo = self.graph.topo_order()

@@ -73,8 +73,8 @@ class StepSchedule:
         return {"K": self.K, "gamma": self.gamma, "key_steps": list(self.key_steps)}
 
 
-def gram_similarity(probes: list[torch.Tensor], probe_label: str = "") -> SimilarityMap:
-    """S[i][j] = <p_i, p_j> / (|p_i| |p_j|) from one device Gram reduction."""
+def gram_partial(probes: list[torch.Tensor]) -> np.ndarray:
+    """K x K fp64 Gram matrix <p_i, p_j> of device probes (one fixed-order reduction)."""
     K = len(probes)
     n = probes[0].numel()
     dev = probes[0].device
@@ -83,7 +83,17 @@ def gram_similarity(probes: list[torch.Tensor], probe_label: str = "") -> Simila
     out = torch.empty(K * K, dtype=torch.float64, device=dev)
     N.call("sf_gram_bf16", ptrs.data_ptr(), K, n, work.data_ptr(), out.data_ptr(),
            torch.cuda.current_stream().cuda_stream)
-    G = out.cpu().numpy().reshape(K, K)
+    return out.cpu().numpy().reshape(K, K)
+
+
+def gram_similarity(probes: list[torch.Tensor], probe_label: str = "") -> SimilarityMap:
+    """S[i][j] = <p_i, p_j> / (|p_i| |p_j|) from one device Gram reduction."""
+    return similarity_from_gram(gram_partial(probes), probe_label)
+
+
+def similarity_from_gram(G: np.ndarray, probe_label: str = "") -> SimilarityMap:
+    """Normalise a (possibly rank-summed) Gram matrix into the cosine map (kernels.py:386-390)."""
+    K = G.shape[0]
     d = np.diag(G).copy()
     if np.any(d == 0.0):
         raise ZeroNorm("cosine similarity undefined for an identically-zero tensor")
