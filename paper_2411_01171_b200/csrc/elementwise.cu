@@ -101,24 +101,43 @@ __global__ void gn_finalize_kernel(const double2* partial, int frames, int split
   }
 }
 
-__global__ void gn_apply_kernel(sf_view_t x, sf_view_t y, int frames, int n_inner, int C, int groups,
-                                const float* __restrict__ mean, const float* __restrict__ rstd,
-                                const float* __restrict__ gamma, const float* __restrict__ beta, int act) {
-  const int nvec = C / 8, cg = C / groups;
-  const int64_t total = (int64_t)frames * n_inner * nvec;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int v = idx % nvec;
-    int64_t row = idx / nvec;
-    int frame = row / n_inner, r = row % n_inner;
-    bf16x8 in = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r) + v * 8);
+// y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]); one block covers a
+// chunk of one frame's rows with the frame's per-channel tables in shared memory.
+constexpr int GNA_THREADS = 256, GNA_VEC_PER_THREAD = 8;
+__global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(sf_view_t x, sf_view_t y, int n_inner, int C,
+                                                               int groups, int chunks,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ rstd,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ beta, int act) {
+  extern __shared__ float tab[];  // [3][C]: mean, scale, beta per channel
+  const int frame = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
+  const int cg = C / groups, nvec = C / 8;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int g = c / cg;
+    tab[c] = mean[frame * groups + g];
+    tab[C + c] = rstd[frame * groups + g] * gamma[c];
+    tab[2 * C + c] = beta[c];
+  }
+  __syncthreads();
+  const int64_t total = (int64_t)n_inner * nvec;
+  const int64_t per = (total + chunks - 1) / chunks;
+  const int64_t e0 = chunk * per, e1 = min(total, e0 + per);
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int v = (int)(e % nvec);
+    const int64_t r = e / nvec;
     float f[8];
-    unpack8(in, f);
+    unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r) + v * 8), f);
+    const float4* m4 = reinterpret_cast<const float4*>(tab + v * 8);
+    const float4* s4 = reinterpret_cast<const float4*>(tab + C + v * 8);
+    const float4* b4 = reinterpret_cast<const float4*>(tab + 2 * C + v * 8);
+    const float4 m0 = m4[0], m1 = m4[1], s0 = s4[0], s1 = s4[1], b0 = b4[0], b1 = b4[1];
+    const float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      int c = v * 8 + j, g = c / cg;
-      float m = mean[frame * groups + g], s = rstd[frame * groups + g];
-      float t = (f[j] - m) * s * gamma[c] + beta[c];
+      const float t = (f[j] - mm[j]) * ss[j] + bb[j];
       f[j] = act ? silu_f(t) : t;
     }
     *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, frame, r) + v * 8) = pack8(f);
@@ -126,55 +145,70 @@ __global__ void gn_apply_kernel(sf_view_t x, sf_view_t y, int frames, int n_inne
 }
 
 // ---------------------------------------------------------------------------
-// LayerNorm over channels (kernels.py:240-244): one warp per row, two-pass
-// from registers (mean, then mean of squared deviations), like the reference.
+// LayerNorm over channels (kernels.py:240-244): L lanes per row (32/L rows per
+// warp), VPL 16-byte vectors per lane, two-pass (mean, then mean of squared
+// deviations) from registers like the reference.
 // ---------------------------------------------------------------------------
-template <int VPL>
-__global__ void layer_norm_kernel(sf_view_t x, sf_view_t y, int n_outer, int n_inner, int C,
-                                  const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
-                                  int act) {
+template <int L, int VPL>
+__global__ void __launch_bounds__(256) layer_norm_kernel(sf_view_t x, sf_view_t y, int n_outer, int n_inner, int C,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ beta, float eps, int act) {
+  constexpr int RPW = 32 / L;  // rows per warp
   const int64_t rows = (int64_t)n_outer * n_inner;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, sub = lane % L, grp = lane / L;
   const int nvec = C / 8;
-  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows;
-       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int o = row / n_inner, i = row % n_inner;
+  const int64_t warps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * RPW; base < rows;
+       base += warps_total * RPW) {
+    const int64_t row = base + grp;
+    const bool live = row < rows;
+    const int o = live ? (int)(row / n_inner) : 0, i = live ? (int)(row % n_inner) : 0;
     const bf16* src = row_ptr<const bf16>(x, o, i);
     float f[VPL][8];
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      int v = lane + 32 * k;
-      if (v < nvec) {
+      const int v = sub + L * k;
+      if (live && v < nvec) {
         unpack8(*reinterpret_cast<const bf16x8*>(src + v * 8), f[k]);
 #pragma unroll
         for (int j = 0; j < 8; ++j) s += f[k][j];
       }
     }
-    const float mu = warp_sum(s) / C;
+#pragma unroll
+    for (int m = L / 2; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+    const float mu = s / C;
     float q = 0.f;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      int v = lane + 32 * k;
-      if (v < nvec) {
+      const int v = sub + L * k;
+      if (live && v < nvec) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          float d = f[k][j] - mu;
+          const float d = f[k][j] - mu;
           q += d * d;
         }
       }
     }
-    const float rs = rsqrtf(warp_sum(q) / C + eps);
+#pragma unroll
+    for (int m = L / 2; m > 0; m >>= 1) q += __shfl_xor_sync(0xffffffffu, q, m);
+    const float rs = rsqrtf(q / C + eps);
+    if (!live) continue;
     bf16* dst = row_ptr<bf16>(y, o, i);
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      int v = lane + 32 * k;
+      const int v = sub + L * k;
       if (v < nvec) {
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + v * 8));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + v * 8) + 1);
+        const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + v * 8));
+        const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + v * 8) + 1);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
         float g[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          int c = v * 8 + j;
-          float t = (f[k][j] - mu) * rs * gamma[c] + beta[c];
+          const float t = (f[k][j] - mu) * rs * gg[j] + bb[j];
           g[j] = act ? silu_f(t) : t;
         }
         *reinterpret_cast<bf16x8*>(dst + v * 8) = pack8(g);
@@ -789,9 +823,15 @@ sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t 
   SF_CHECK_ARG(frames >= 1 && n_inner >= 1 && C % 8 == 0, SF_ERR_SHAPE, "bad extents");
   SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
   SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
-  int64_t total = (int64_t)frames * n_inner * (C / 8);
-  gn_apply_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, n_inner, C, groups, mean,
-                                                                          rstd, gamma, beta, act);
+  SF_CHECK_ARG(aligned16(gamma) && aligned16(beta), SF_ERR_PARAM, "gamma/beta must be 16-byte aligned");
+  const int64_t per_frame = (int64_t)n_inner * (C / 8);
+  int chunks = (int)((per_frame + GNA_THREADS * GNA_VEC_PER_THREAD - 1) / (GNA_THREADS * GNA_VEC_PER_THREAD));
+  if (chunks < 1) chunks = 1;
+  const size_t smem = (size_t)3 * C * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(gn_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gn_apply_kernel<<<frames * chunks, GNA_THREADS, smem, (cudaStream_t)stream>>>(x, y, n_inner, C, groups, chunks, mean,
+                                                                               rstd, gamma, beta, act);
   return launch_status("sf_group_norm_apply");
 }
 
@@ -799,20 +839,28 @@ sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inn
                         const float* beta, float eps, int32_t act, void* stream) {
   SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0 && C <= 32 * 8 * 12, SF_ERR_SHAPE, "bad extents");
   SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
-  int64_t rows = (int64_t)n_outer * n_inner;
-  int grid = ew_grid(rows * 32, 256);
+  SF_CHECK_ARG(aligned16(gamma) && aligned16(beta), SF_ERR_PARAM, "gamma/beta must be 16-byte aligned");
+  const int64_t rows = (int64_t)n_outer * n_inner;
   cudaStream_t st = (cudaStream_t)stream;
-  int vpl = (C / 8 + 31) / 32;
-  if (vpl <= 1)
-    layer_norm_kernel<1><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
-  else if (vpl <= 2)
-    layer_norm_kernel<2><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
-  else if (vpl <= 4)
-    layer_norm_kernel<4><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
-  else if (vpl <= 8)
-    layer_norm_kernel<8><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
-  else
-    layer_norm_kernel<12><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act);
+  const int nvec = C / 8;
+  // lanes per row: enough that every lane holds <= 5 vectors (<= 12 for the widest rows)
+  int L = 1;
+  while (L < 32 && (nvec + L - 1) / L > 5) L *= 2;
+  const int vpl = (nvec + L - 1) / L;
+  const int64_t warps = (rows + 32 / L - 1) / (32 / L);
+  int64_t g = (warps * 32 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  const int grid = (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+#define SF_LN(LL, VV) layer_norm_kernel<LL, VV><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act)
+  if (L == 1) SF_LN(1, 5);
+  else if (L == 2) SF_LN(2, 5);
+  else if (L == 4) SF_LN(4, 5);
+  else if (L == 8) SF_LN(8, 5);
+  else if (L == 16) SF_LN(16, 5);
+  else if (vpl <= 5) SF_LN(32, 5);
+  else if (vpl <= 8) SF_LN(32, 8);
+  else SF_LN(32, 12);
+#undef SF_LN
   return launch_status("sf_layer_norm");
 }
 
