@@ -299,52 +299,52 @@ __global__ void upsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int
 // softmax rows: fp32 scores -> bf16 probabilities (kernels.py:272-276)
 // ---------------------------------------------------------------------------
 template <int PER>
-__global__ void softmax_rows_kernel(const float* __restrict__ s, int64_t lds, bf16* __restrict__ p, int64_t ldp,
-                                    int n) {
+__global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restrict__ s, int64_t lds,
+                                                           bf16* __restrict__ p, int64_t ldp, int n) {
+  // PER float4 chunks per thread; n % 4 == 0 and 16-byte aligned rows
   const int64_t row = blockIdx.x;
-  const float* src = s + row * lds;
-  float v[PER];
+  const float4* src = reinterpret_cast<const float4*>(s + row * lds);
+  const int n4 = n / 4;
+  float4 v[PER];
   float m = -INFINITY;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
-    int c = threadIdx.x + k * blockDim.x;
-    v[k] = c < n ? src[c] : -INFINITY;
-    m = fmaxf(m, v[k]);
+    const int c = threadIdx.x + k * blockDim.x;
+    v[k] = c < n4 ? src[c] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    m = fmaxf(m, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
   }
-  __shared__ float red[32];
+  __shared__ float red[8];
   m = warp_max(m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : -INFINITY;
-    t = warp_max(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
   m = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
   __syncthreads();
   float sum = 0.f;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
-    int c = threadIdx.x + k * blockDim.x;
-    v[k] = c < n ? __expf(v[k] - m) : 0.f;
-    sum += v[k];
+    v[k].x = __expf(v[k].x - m);
+    v[k].y = __expf(v[k].y - m);
+    v[k].z = __expf(v[k].z - m);
+    v[k].w = __expf(v[k].w - m);
+    sum += (v[k].x + v[k].y) + (v[k].z + v[k].w);
   }
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  const float inv = 1.f / red[0];
-  bf16* dst = p + row * ldp;
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = 1.f / tot;
+  bf162* dst = reinterpret_cast<bf162*>(p + row * ldp);
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
-    int c = threadIdx.x + k * blockDim.x;
-    if (c < n) dst[c] = __float2bfloat16(v[k] * inv);
+    const int c = threadIdx.x + k * blockDim.x;
+    if (c < n4) {
+      dst[2 * c] = __floats2bfloat162_rn(v[k].x * inv, v[k].y * inv);
+      dst[2 * c + 1] = __floats2bfloat162_rn(v[k].z * inv, v[k].w * inv);
+    }
   }
 }
 
@@ -605,37 +605,51 @@ __global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_vie
 // ---------------------------------------------------------------------------
 // latent-edge convolutions with tiny channel counts (in_conv / out_conv)
 // ---------------------------------------------------------------------------
-// in_conv: tiny cin, fp32 input; one thread per (pixel, 8 output channels).
-// Weights in [tap][ci][co] so a warp's weight reads are contiguous in co.
-__global__ void conv_smallcin_kernel(const float* __restrict__ x, int frames, int H, int W, int cin,
-                                     const float* __restrict__ wt, const float* __restrict__ bias, int cout,
-                                     sf_view_t y) {
-  const int nvec = cout / 8;
-  const int64_t total = (int64_t)frames * H * W * nvec;
+// in_conv: tiny cin, fp32 input.  A warp covers 32 consecutive pixels for one
+// chunk of 32 output channels; the [9][cin][cout] weights sit in shared memory
+// and every weight read is a warp-wide broadcast.
+constexpr int SC_THREADS = 128;
+template <int SC_CO>
+__global__ void __launch_bounds__(SC_THREADS) conv_smallcin_kernel(const float* __restrict__ x, int frames, int H,
+                                                                   int W, int cin, const float* __restrict__ wt,
+                                                                   const float* __restrict__ bias, int cout,
+                                                                   sf_view_t y) {
+  extern __shared__ float wsm[];  // [9][cin][cout]
+  const int nw = 9 * cin * cout;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) wsm[i] = wt[i];
+  __syncthreads();
+  const int nchunk = cout / SC_CO;
+  const int64_t npix = (int64_t)frames * H * W;
+  const int64_t total = npix * nchunk;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int v = idx % nvec;
-    int64_t p = idx / nvec;
-    int px = p % W, py = (p / W) % H, f = p / ((int64_t)W * H);
-    float acc[8];
+    // idx -> (chunk, pixel) with pixels fastest so a warp shares one weight chunk
+    const int64_t p = idx % npix;
+    const int ch = (int)(idx / npix);
+    const int px = p % W, py = (p / W) % H, f = p / ((int64_t)W * H);
+    float acc[SC_CO];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int j = 0; j < SC_CO; ++j) acc[j] = bias[ch * SC_CO + j];
     for (int tap = 0; tap < 9; ++tap) {
-      int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
-      if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+      const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+      const bool ok = yy >= 0 && yy < H && xx >= 0 && xx < W;
       const float* src = x + (((int64_t)f * H + yy) * W + xx) * cin;
-      const float* wr = wt + (int64_t)tap * cin * cout + v * 8;
       for (int ci = 0; ci < cin; ++ci) {
-        float a = __ldg(src + ci);
-        float4 w0 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)ci * cout));
-        float4 w1 = __ldg(reinterpret_cast<const float4*>(wr + (int64_t)ci * cout) + 1);
-        acc[0] += a * w0.x; acc[1] += a * w0.y; acc[2] += a * w0.z; acc[3] += a * w0.w;
-        acc[4] += a * w1.x; acc[5] += a * w1.y; acc[6] += a * w1.z; acc[7] += a * w1.w;
+        const float a = ok ? __ldg(src + ci) : 0.f;
+        const float4* wr = reinterpret_cast<const float4*>(wsm + ((tap * cin + ci) * cout + ch * SC_CO));
+#pragma unroll
+        for (int j = 0; j < SC_CO / 4; ++j) {
+          const float4 w4 = wr[j];
+          acc[4 * j] += a * w4.x;
+          acc[4 * j + 1] += a * w4.y;
+          acc[4 * j + 2] += a * w4.z;
+          acc[4 * j + 3] += a * w4.w;
+        }
       }
     }
+    bf16* dst = row_ptr<bf16>(y, f, (int64_t)py * W + px) + ch * SC_CO;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] += bias[v * 8 + j];
-    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, (int64_t)py * W + px) + v * 8) = pack8(acc);
+    for (int j = 0; j < SC_CO / 8; ++j) reinterpret_cast<bf16x8*>(dst)[j] = pack8(acc + 8 * j);
   }
 }
 
@@ -911,18 +925,19 @@ sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int
 }
 
 sf_status sf_softmax_rows(const float* s, int64_t lds, void* p, int64_t ldp, int64_t rows, int32_t n, void* stream) {
-  SF_CHECK_ARG(rows >= 1 && n >= 1 && n <= 256 * 64, SF_ERR_SHAPE, "row length outside [1, 16384]");
+  SF_CHECK_ARG(rows >= 1 && n >= 4 && n % 4 == 0 && n <= 256 * 4 * 16, SF_ERR_SHAPE,
+               "row length must be a multiple of 4 in [4, 16384]");
+  SF_CHECK_ARG(aligned16(s) && lds % 4 == 0 && ldp % 4 == 0, SF_ERR_PARAM, "rows must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  int per = (n + 255) / 256;
+  const int per = (n / 4 + 255) / 256;
   bf16* P = (bf16*)p;
 #define SF_SM(K) softmax_rows_kernel<K><<<(unsigned)rows, 256, 0, st>>>(s, lds, P, ldp, n)
   if (per <= 1) SF_SM(1);
   else if (per <= 2) SF_SM(2);
+  else if (per <= 3) SF_SM(3);
   else if (per <= 4) SF_SM(4);
-  else if (per <= 8) SF_SM(8);
-  else if (per <= 16) SF_SM(16);
-  else if (per <= 36) SF_SM(36);
-  else SF_SM(64);
+  else if (per <= 9) SF_SM(9);
+  else SF_SM(16);
 #undef SF_SM
   return launch_status("sf_softmax_rows");
 }
@@ -950,10 +965,31 @@ sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, 
 
 sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t W, int32_t cin, const float* w,
                               const float* bias, int32_t cout, sf_view_t y, void* stream) {
-  SF_CHECK_ARG(cin >= 1 && cin <= 64 && cout % 8 == 0, SF_ERR_SHAPE, "need cin <= 64 and cout % 8 == 0");
-  SF_CHECK_ARG(view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
-  int64_t total = (int64_t)frames * H * W * (cout / 8);
-  conv_smallcin_kernel<<<ew_grid(total, 128), 128, 0, (cudaStream_t)stream>>>(x, frames, H, W, cin, w, bias, cout, y);
+  SF_CHECK_ARG(cin >= 1 && cin <= 16 && cout % 8 == 0 && cout <= 1280, SF_ERR_SHAPE,
+               "need cin <= 16, cout % 8 == 0, cout <= 1280");
+  SF_CHECK_ARG(view_vec8_ok(y) && aligned16(w), SF_ERR_PARAM, "unaligned view or weights");
+  const size_t smem = (size_t)9 * cin * cout * sizeof(float);
+  SF_CHECK_ARG(smem <= 200 * 1024, SF_ERR_SHAPE, "in_conv weights exceed shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cout % 32 == 0) {
+    static size_t cfg32 = 0;
+    if (smem > 48 * 1024 && smem > cfg32) {
+      cudaFuncSetAttribute(conv_smallcin_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cfg32 = smem;
+    }
+    const int64_t total = (int64_t)frames * H * W * (cout / 32);
+    conv_smallcin_kernel<32><<<ew_grid(total, SC_THREADS), SC_THREADS, smem, st>>>(x, frames, H, W, cin, w, bias,
+                                                                                   cout, y);
+  } else {
+    static size_t cfg8 = 0;
+    if (smem > 48 * 1024 && smem > cfg8) {
+      cudaFuncSetAttribute(conv_smallcin_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cfg8 = smem;
+    }
+    const int64_t total = (int64_t)frames * H * W * (cout / 8);
+    conv_smallcin_kernel<8><<<ew_grid(total, SC_THREADS), SC_THREADS, smem, st>>>(x, frames, H, W, cin, w, bias,
+                                                                                  cout, y);
+  }
   return launch_status("sf_conv3x3_smallcin");
 }
 

@@ -51,6 +51,29 @@ __device__ __forceinline__ void tma3(const CUtensorMap* m, uint64_t* bar, void* 
       "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma3_mc(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                        uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
@@ -110,7 +133,11 @@ struct Layout {
   static constexpr int O_COL = 0, S_COL = 320;        // TMEM columns
 };
 
-template <int D>
+// MC: CTA pairs (cluster of 2 along the query-tile axis, same frame) share every
+// K/V^T ring slot: each CTA TMA-loads half of the slot and multicasts it to both,
+// and a slot is refilled only after both CTAs' MMAs released it -- half the L2
+// traffic per query tile.
+template <int D, bool MC>
 __global__ void __launch_bounds__(THREADS, 1)
     flash_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mQ,
                  const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV) {
@@ -139,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(q_full, 1);
     for (int s = 0; s < SLOTS; ++s) {
       mbar_init(&r_full[s], 1);
-      mbar_init(&r_empty[s], 1);
+      mbar_init(&r_empty[s], MC ? 2 : 1);   // both CTAs of the pair must release a shared slot
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
@@ -155,8 +182,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   fence_before();
   __syncthreads();
+  if (MC) cluster_sync();   // peer barriers initialised before any multicast / remote arrive
   fence_after();
   const uint32_t tmem = *tslot;
+  const uint32_t crank = MC ? cluster_rank() : 0;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -190,7 +219,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&r_empty[slot], ph ^ 1);
         mbar_expect_tx(&r_full[slot], L::SLOT_BYTES);
         uint8_t* dst = sRing + slot * L::SLOT_BYTES;
-        if (k_item) {
+        if (MC) {
+          // my half of the slot, multicast to both CTAs (the peer loads the other half)
+          if (k_item) {
+            const int c0 = crank == 0 ? 0 : (L::NCH + 1) / 2, c1 = crank == 0 ? (L::NCH + 1) / 2 : L::NCH;
+            for (int c = c0; c < c1; ++c)
+              tma3_mc(&mK, &r_full[slot], dst + c * BKV * 128, c * 64, j * BKV, f, 0x3);
+          } else {
+            tma3_mc(&mV, &r_full[slot], dst + crank * (D / 2) * 128, j * BKV, crank * (D / 2), f, 0x3);
+          }
+        } else if (k_item) {
           for (int c = 0; c < L::NCH; ++c) tma3(&mK, &r_full[slot], dst + c * BKV * 128, c * 64, j * BKV, f);
         } else {
           tma3(&mV, &r_full[slot], dst, j * BKV, 0, f);
@@ -222,7 +260,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             mma(d, sdesc(qa + c * BQ * 128 + k * 32), sdesc(kb + c * BKV * 128 + k * 32), idS, (c | k) != 0);
-        commit(&r_empty[slot]);
+        if (MC) commit_mc(&r_empty[slot], 0x3);
+        else commit(&r_empty[slot]);
         commit(&s_full[sb]);
         if (++slot == SLOTS) {
           slot = 0;
@@ -240,7 +279,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma(tmem + L::O_COL, sdesc(pa + k * 32), sdesc(vb + k * 32), idO, (j | k) != 0);
           mma(tmem + L::O_COL + D / 2, sdesc(pa + k * 32), sdesc(vb + (D / 2) * 128 + k * 32), idO, (j | k) != 0);
         }
-        commit(&r_empty[slot]);
+        if (MC) commit_mc(&r_empty[slot], 0x3);
+        else commit(&r_empty[slot]);
         commit(o_done);
         if (++slot == SLOTS) {
           slot = 0;
@@ -350,6 +390,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   fence_before();
   __syncthreads();
+  if (MC) cluster_sync();   // no CTA leaves while its peer may still multicast into it
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -388,11 +429,30 @@ static sf_status launch(const Params& p, const CUtensorMap& q, const CUtensorMap
   constexpr int smem = Layout<D>::TOTAL;
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(flash_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(flash_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(flash_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     init = true;
   }
-  dim3 grid((p.HW + BQ - 1) / BQ, p.frames);
-  flash_kernel<D><<<grid, THREADS, smem, st>>>(p, q, k, v);
+  const int qt = (p.HW + BQ - 1) / BQ;
+  if (qt >= 2) {
+    // CTA pairs share K/V: grid.x rounded up to even (a padding tile only masks its rows)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)((qt + 1) / 2 * 2), (unsigned)p.frames, 1);
+    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, flash_kernel<D, true>, p, q, k, v);
+  } else {
+    dim3 grid(qt, p.frames);
+    flash_kernel<D, false><<<grid, THREADS, smem, st>>>(p, q, k, v);
+  }
   return launch_status("sf_spatial_attention_core");
 }
 
