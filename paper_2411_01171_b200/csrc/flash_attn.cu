@@ -18,6 +18,7 @@
 #include "common.cuh"
 
 #include <cuda.h>
+#include <cstdlib>
 #include <mutex>
 
 namespace sf {
@@ -245,7 +246,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t idS = idesc(BKV), idO = idesc(D / 2);
       mbar_wait(q_full, 0);
       fence_after();
-      const uint32_t qa = smem_u32(sQ);
+      const uint64_t qd = sdesc(smem_u32(sQ));
+      const uint64_t pd = sdesc(smem_u32(sP));
       int slot = 0;
       uint32_t ph = 0;
       auto issue_S = [&](int j) {
@@ -253,13 +255,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
         mbar_wait(&r_full[slot], ph);
         fence_after();
-        const uint32_t kb = smem_u32(sRing + slot * L::SLOT_BYTES);
+        // descriptors built once; every MMA only adds a constant to the address field
+        const uint64_t kd = sdesc(smem_u32(sRing + slot * L::SLOT_BYTES));
         const uint32_t d = tmem + L::S_COL + sb * BKV;
 #pragma unroll
         for (int c = 0; c < L::NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma(d, sdesc(qa + c * BQ * 128 + k * 32), sdesc(kb + c * BKV * 128 + k * 32), idS, (c | k) != 0);
+            mma(d, qd + (uint64_t)((c * BQ * 128 + k * 32) >> 4), kd + (uint64_t)((c * BKV * 128 + k * 32) >> 4), idS,
+                (c | k) != 0);
         if (MC) commit_mc(&r_empty[slot], 0x3);
         else commit(&r_empty[slot]);
         commit(&s_full[sb]);
@@ -272,12 +276,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(p_full, j & 1);
         mbar_wait(&r_full[slot], ph);
         fence_after();
-        const uint32_t vb = smem_u32(sRing + slot * L::SLOT_BYTES);
-        const uint32_t pa = smem_u32(sP);
+        const uint64_t vd = sdesc(smem_u32(sRing + slot * L::SLOT_BYTES));
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          mma(tmem + L::O_COL, sdesc(pa + k * 32), sdesc(vb + k * 32), idO, (j | k) != 0);
-          mma(tmem + L::O_COL + D / 2, sdesc(pa + k * 32), sdesc(vb + (D / 2) * 128 + k * 32), idO, (j | k) != 0);
+          mma(tmem + L::O_COL, pd + (uint64_t)(k * 2), vd + (uint64_t)(k * 2), idO, (j | k) != 0);
+          mma(tmem + L::O_COL + D / 2, pd + (uint64_t)(k * 2), vd + (uint64_t)(((D / 2) * 128 + k * 32) >> 4), idO,
+              (j | k) != 0);
         }
         if (MC) commit_mc(&r_empty[slot], 0x3);
         else commit(&r_empty[slot]);
@@ -459,6 +463,10 @@ static sf_status launch(const Params& p, const CUtensorMap& q, const CUtensorMap
 }  // namespace fa
 }  // namespace sf
 
+namespace sf {
+sf_status flash2_launch(sf_view_t q, sf_view_t k, const void* vt, sf_view_t out, int frames, int HW, int C,
+                        float scale, cudaStream_t st);
+}
 using namespace sf;
 
 extern "C" int32_t sf_flash_supported(int32_t HW, int32_t C) {
@@ -486,6 +494,8 @@ extern "C" sf_status sf_spatial_attention_core(sf_view_t q, sf_view_t k, const v
   SF_CHECK_ARG(fa::enc3(&mv, vt, HW, C, frames, (uint64_t)HW * es, (uint64_t)C * HW * es, 64, C / 2), SF_ERR_CUDA,
                "tensor map V");
   cudaStream_t st = (cudaStream_t)stream;
+  static const bool use_v1 = getenv("SF_FLASH_V1") != nullptr;
+  if (!use_v1) return flash2_launch(q, k, vt, out, frames, HW, C, scale, st);
   switch (C) {
     case 320: return fa::launch<320>(p, mq, mk, mv, st);
     case 256: return fa::launch<256>(p, mq, mk, mv, st);

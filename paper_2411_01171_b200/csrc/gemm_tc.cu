@@ -287,11 +287,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int it = 0; it < kiters; ++it) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * L::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * L::B_BYTES);
+          const uint64_t ad = make_sdesc(smem_u32(sA + stage * L::A_BYTES));
+          const uint64_t bd = make_sdesc(smem_u32(sB + stage * L::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            umma_f16(d, make_sdesc(a0 + k * 32), make_sdesc(b0 + k * 32), idesc, (it | k) != 0);
+            // +32 B along K inside the 128 B swizzle atom = +2 in the 16-byte address field
+            umma_f16(d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (it | k) != 0);
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
