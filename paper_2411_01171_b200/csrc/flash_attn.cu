@@ -466,6 +466,9 @@ static sf_status launch(const Params& p, const CUtensorMap& q, const CUtensorMap
 namespace sf {
 sf_status flash2_launch(sf_view_t q, sf_view_t k, const void* vt, sf_view_t out, int frames, int HW, int C,
                         float scale, cudaStream_t st);
+sf_status flash3_launch(sf_view_t q, sf_view_t k, const void* vt, sf_view_t out, int frames, int HW, int C,
+                        float scale, cudaStream_t st);
+bool flash3_supported(int C);
 }
 using namespace sf;
 
@@ -494,8 +497,10 @@ extern "C" sf_status sf_spatial_attention_core(sf_view_t q, sf_view_t k, const v
   SF_CHECK_ARG(fa::enc3(&mv, vt, HW, C, frames, (uint64_t)HW * es, (uint64_t)C * HW * es, 64, C / 2), SF_ERR_CUDA,
                "tensor map V");
   cudaStream_t st = (cudaStream_t)stream;
-  static const bool use_v1 = getenv("SF_FLASH_V1") != nullptr;
-  if (!use_v1) return flash2_launch(q, k, vt, out, frames, HW, C, scale, st);
+  static const char* ver = getenv("SF_FLASH");   // "1" / "2" force an older kernel (A/B runs)
+  const int v = ver ? atoi(ver) : 3;
+  if (v >= 3 && flash3_supported(C) && (HW + 127) / 128 >= 2) return flash3_launch(q, k, vt, out, frames, HW, C, scale, st);
+  if (v >= 2) return flash2_launch(q, k, vt, out, frames, HW, C, scale, st);
   switch (C) {
     case 320: return fa::launch<320>(p, mq, mk, mv, st);
     case 256: return fa::launch<256>(p, mq, mk, mv, st);
