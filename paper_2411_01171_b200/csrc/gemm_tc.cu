@@ -19,6 +19,7 @@
 #include "common.cuh"
 
 #include <cuda.h>
+#include <cstdlib>
 #include <mutex>
 
 namespace sf {
@@ -100,6 +101,53 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+// ---- CTA-pair (cta_group::2) helpers ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t leader_addr(const void* ptr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(ptr)));
+  return r;
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_2sm(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1, int c2,
+                                                int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -116,9 +164,9 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
   return d;
 }
 
-// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N=n
-__host__ __device__ constexpr uint32_t make_idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M=m, N=n
+__host__ __device__ constexpr uint32_t make_idesc(int n, int m = BM) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -175,10 +223,10 @@ __device__ __forceinline__ MTile decode_m(const Params& p, int64_t tm) {
   return t;
 }
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, bool PAIR = false>
 struct SmemLayout {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;   // a pair stages half of B per CTA
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // epilogue staging tile [128 rows][BN] bf16 (residual in, output out), row-major
   static constexpr int OUT_TILE = BM * BN * 2;
@@ -186,12 +234,16 @@ struct SmemLayout {
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + OUT_BYTES + 256 /*barriers*/;
 };
 
-template <int BN, int STAGES, int EPI>
+// PAIR: CTA pairs (cluster of 2) run tcgen05.mma.cta_group::2 with M = 256:
+// CTA rank r owns M-tile 2*pair + r (its A rows, TMEM accumulator and epilogue)
+// and stages rows [r*BN/2, (r+1)*BN/2) of the B tile; the leader (rank 0)
+// issues every MMA and its commits arrive on both CTAs' barriers.
+template <int BN, int STAGES, int EPI, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapR,
                    const __grid_constant__ CUtensorMap mapO) {
-  using L = SmemLayout<BN, STAGES, EPI>;
+  using L = SmemLayout<BN, STAGES, EPI, PAIR>;
   constexpr bool TMA_EPI = EPI > 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -219,7 +271,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[s], PAIR ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
     }
     for (int b = 0; b < 2; ++b) mbar_init(&res_full[b], 1);
     if (TMA_EPI) {
@@ -229,17 +281,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int64_t n_tiles = p.tiles_m * p.tiles_n;
   const int kiters = p.taps * p.cblocks;
+  // tile walk: a pair walks pair-tiles (two adjacent M-tiles x one N-tile)
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int64_t tiles_mw = PAIR ? (p.tiles_m + 1) / 2 : p.tiles_m;
+  const int64_t n_tiles = tiles_mw * p.tiles_n;
+  const int64_t t_first = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t t_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  auto my_tm = [&](int64_t tile) -> int64_t {
+    const int64_t tw = tile / p.tiles_n;
+    return PAIR ? 2 * tw + rank : tw;
+  };
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -247,16 +316,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tcount = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-        const int64_t tm = tile / p.tiles_n;
+      for (int64_t tile = t_first; tile < n_tiles; tile += t_step, ++tcount) {
+        const int64_t tm = my_tm(tile);
         const int n0 = (int)(tile % p.tiles_n) * BN;
         const MTile mt = decode_m(p, tm);
         for (int it = 0; it < kiters; ++it) {
           const int tap = it / p.cblocks, cb = it % p.cblocks;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], L::STAGE_BYTES);
           void* dA = sA + stage * L::A_BYTES;
           void* dB = sB + stage * L::B_BYTES;
+          if constexpr (PAIR) {
+            // my A tile + my half of B, completion bytes counted on the leader's barrier
+            if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+            const uint32_t fb = leader_addr(&full[stage]);
+            if (p.mode == SF_GEMM_CONV3X3)
+              tma_load_4d_2sm(&mapA, fb, dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1, mt.f);
+            else if (p.mode == SF_GEMM_TCONV3)
+              tma_load_4d_2sm(&mapA, fb, dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
+            else
+              tma_load_4d_2sm(&mapA, fb, dA, cb * BK, mt.i0, mt.o0, p.a_batched ? mt.z : 0);
+            tma_load_3d_2sm(&mapB, fb, dB, tap * p.cin + cb * BK, n0 + (int)rank * (BN / 2), p.b_batched ? mt.z : 0);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          mbar_expect_tx(&full[stage], L::STAGE_BYTES);
           if (p.mode == SF_GEMM_CONV3X3) {
             tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1, mt.f);
           } else if (p.mode == SF_GEMM_TCONV3) {
@@ -274,13 +360,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(BN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = make_idesc(BN, PAIR ? 2 * BM : BM);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int64_t tile = t_first; tile < n_tiles; tile += t_step) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
@@ -292,15 +378,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 B along K inside the 128 B swizzle atom = +2 in the 16-byte address field
-            umma_f16(d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (it | k) != 0);
+            if (PAIR) umma_f16_pair(d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (it | k) != 0);
+            else umma_f16(d, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (it | k) != 0);
           }
-          umma_commit(&empty[stage]);
+          if (PAIR) umma_commit_pair(&empty[stage]);
+          else umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if (PAIR) umma_commit_pair(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -314,10 +403,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t tcount = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-      const int64_t tm = tile / p.tiles_n;
+    const uint32_t tempty_l = PAIR ? leader_addr(&tempty[0]) : 0;
+    for (int64_t tile = t_first; tile < n_tiles; tile += t_step, ++tcount) {
+      const int64_t tm = my_tm(tile);
       const int n0 = (int)(tile % p.tiles_n) * BN;
       const MTile mt = decode_m(p, tm);
+      const bool phantom = tm >= p.tiles_m;   // odd tile count: the pair's second tile is empty
       // output row of this thread
       bool valid;
       int64_t o, i;
@@ -339,15 +430,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         i = ii;
       }
+      valid = valid && !phantom;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if constexpr (TMA_EPI) {
-        const bool leader = warp == EPI_W0 && lane == 0;
+        const bool store_leader = warp == EPI_W0 && lane == 0;
         const int ob = EPI == 2 ? (int)(tcount & 1) : 0;
         const uint32_t use = EPI == 2 ? (tcount >> 1) : tcount;
         uint8_t* sbuf = sOut + ob * L::OUT_TILE;
         if (EPI == 1) {
           // single staging buffer: the previous store must have drained it; then fetch the residual
-          if (leader) {
+          if (store_leader) {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             if (has_res) {
               mbar_expect_tx(&res_full[0], L::OUT_TILE);
@@ -358,7 +450,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
-        } else if (tcount == 0 && has_res && leader) {
+        } else if (tcount == 0 && has_res && store_leader) {
           // double staging: residual of the first tile; later ones are prefetched a tile ahead
           mbar_expect_tx(&res_full[0], L::OUT_TILE);
           if (p.mode == SF_GEMM_CONV3X3)
@@ -406,11 +498,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // accumulator free for the tile after next
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (PAIR) arrive_remote(tempty_l + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
         // staging tile complete -> one thread stores it with TMA (OOB rows/cols are clipped)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (leader) {
+        if (store_leader) {
           if (p.mode == SF_GEMM_CONV3X3)
             tma_store_4d(&mapO, sbuf, n0, mt.x0, mt.y0, mt.f);
           else
@@ -419,9 +514,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (EPI == 2) {
             // the other buffer's store (tile t-1) must drain before it is refilled
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            const int64_t nt = tile + gridDim.x;
+            const int64_t nt = tile + t_step;
             if (has_res && nt < n_tiles) {
-              const MTile nm = decode_m(p, nt / p.tiles_n);
+              const MTile nm = decode_m(p, my_tm(nt));
               const int nn0 = (int)(nt % p.tiles_n) * BN;
               uint8_t* nbuf = sOut + (ob ^ 1) * L::OUT_TILE;
               mbar_expect_tx(&res_full[ob ^ 1], L::OUT_TILE);
@@ -504,7 +599,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR) arrive_remote(tempty_l + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -512,10 +610,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   if (EPI > 0 && warp == EPI_W0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
 }
 
@@ -586,20 +689,39 @@ bool gemm_tc_supported(const sf_gemm_args& a) {
   return tc::encode_fn() != nullptr;
 }
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, bool PAIR = false>
 static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mr,
                             const CUtensorMap& mo, cudaStream_t st) {
-  constexpr int smem = tc::SmemLayout<BN, STAGES, EPI>::TOTAL;
+  constexpr int smem = tc::SmemLayout<BN, STAGES, EPI, PAIR>::TOTAL;
   static_assert(smem <= 232448, "shared memory budget");
   static bool init = false;
+  auto kern = tc::tc_gemm_kernel<BN, STAGES, EPI, PAIR>;
   if (!init) {
-    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     init = true;
   }
-  int64_t tiles = p.tiles_m * p.tiles_n;
-  int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  tc::tc_gemm_kernel<BN, STAGES, EPI><<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb, mr, mo);
-  return launch_status("sf_gemm(tcgen05)");
+  if (!PAIR) {
+    int64_t tiles = p.tiles_m * p.tiles_n;
+    int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    kern<<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb, mr, mo);
+    return launch_status("sf_gemm(tcgen05)");
+  }
+  const int64_t pair_tiles = (p.tiles_m + 1) / 2 * p.tiles_n;
+  const int64_t max_pairs = num_sms() / 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * (pair_tiles < max_pairs ? pair_tiles : max_pairs)), 1, 1);
+  cfg.blockDim = dim3(tc::NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p, ma, mb, mr, mo);
+  return launch_status("sf_gemm(tcgen05 pair)");
 }
 
 // Output / residual maps share the M tiling of A: box {BN cols, tile rows}.
@@ -656,6 +778,10 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
 
   CUtensorMap ma, mb;
   const uint64_t es = 2;
+  // CTA pairs (cta_group::2, M = 256) whenever there are two M-tiles to pair up;
+  // SF_GEMM_PAIR=0 forces single-CTA tiles (A/B runs)
+  static const char* pair_env = getenv("SF_GEMM_PAIR");
+  bool pair = !(pair_env && pair_env[0] == '0');
   const uint64_t ld = (uint64_t)a.a.ld;
   if (a.mode == SF_GEMM_CONV3X3) {
     p.H = a.H;
@@ -712,11 +838,15 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
     uint32_t box[4] = {BK, (uint32_t)p.bi, (uint32_t)p.bo, 1};
     SF_CHECK_ARG(encode(&ma, a.a.ptr, 4, dims, str, box), SF_ERR_CUDA, "tensor map A");
   }
+  pair = pair && p.tiles_m >= 2;
+  // the two CTAs of a pair share one B tile: with a per-batch B (attention scores) a
+  // pair must not straddle two batches, i.e. each batch needs an even tile count
+  if (a.batch > 1 && a.mode == SF_GEMM_PLAIN && ((int64_t)p.tiles_i * p.tiles_o) % 2) pair = false;
   {
     const int taps = p.taps;
     uint64_t dims[3] = {(uint64_t)taps * a.cin, (uint64_t)a.N, (uint64_t)(a.batch > 1 ? a.batch : 1)};
     uint64_t str[2] = {(uint64_t)a.w_ld * es, (uint64_t)(a.batch > 1 ? a.w_bstride : a.w_ld * a.N) * es};
-    uint32_t box[3] = {BK, (uint32_t)BN, 1};
+    uint32_t box[3] = {BK, (uint32_t)(pair ? BN / 2 : BN), 1};
     p.b_batched = a.batch > 1 && a.mode == SF_GEMM_PLAIN;
     SF_CHECK_ARG(encode(&mb, a.w, 3, dims, str, box), SF_ERR_CUDA, "tensor map B");
   }
@@ -727,6 +857,22 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
     // long K: deep operand ring + one staging buffer; short K: double staging so the
     // epilogue (residual prefetch + TMA store) overlaps the next tile
     const bool long_k = p.taps * p.cblocks >= 32;
+    if (pair) {
+      if (long_k) {
+        switch (BN) {
+          case 256: return launch_cfg<256, 5, 1, true>(p, ma, mb, mr, mo, st);
+          case 160: return launch_cfg<160, 7, 1, true>(p, ma, mb, mr, mo, st);
+          case 128: return launch_cfg<128, 8, 1, true>(p, ma, mb, mr, mo, st);
+          default: return launch_cfg<64, 10, 1, true>(p, ma, mb, mr, mo, st);
+        }
+      }
+      switch (BN) {
+        case 256: return launch_cfg<256, 3, 2, true>(p, ma, mb, mr, mo, st);
+        case 160: return launch_cfg<160, 5, 2, true>(p, ma, mb, mr, mo, st);
+        case 128: return launch_cfg<128, 6, 2, true>(p, ma, mb, mr, mo, st);
+        default: return launch_cfg<64, 9, 2, true>(p, ma, mb, mr, mo, st);
+      }
+    }
     if (long_k) {
       switch (BN) {
         case 256: return launch_cfg<256, 3, 1>(p, ma, mb, mr, mo, st);
@@ -740,6 +886,14 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
       case 160: return launch_cfg<160, 4, 2>(p, ma, mb, mr, mo, st);
       case 128: return launch_cfg<128, 5, 2>(p, ma, mb, mr, mo, st);
       default: return launch_cfg<64, 7, 2>(p, ma, mb, mr, mo, st);
+    }
+  }
+  if (pair) {
+    switch (BN) {
+      case 256: return launch_cfg<256, 6, 0, true>(p, ma, mb, mr, mo, st);
+      case 160: return launch_cfg<160, 8, 0, true>(p, ma, mb, mr, mo, st);
+      case 128: return launch_cfg<128, 8, 0, true>(p, ma, mb, mr, mo, st);
+      default: return launch_cfg<64, 10, 0, true>(p, ma, mb, mr, mo, st);
     }
   }
   switch (BN) {
