@@ -217,8 +217,11 @@ class Plan:
             return sid
 
         special = {"x", "step_emb", *self.emb_nodes}
+        # only values that cross a schedule unit live in the arena: group tails and
+        # ungrouped nodes (group-internal intermediates live in the slice scratch)
+        self.materialized = {vid for vid in unit_of if vid not in special}
         for vid, shape in self.shapes.items():
-            if vid in special:
+            if vid not in self.materialized:
                 continue
             sid = root(self._storage_id(vid))
             d = unit_of.get(vid, unit_of.get(self._storage_id(vid), 0))
@@ -266,7 +269,7 @@ class Plan:
             self.buffers[sid] = t
         # values
         for vid, shape in self.shapes.items():
-            if vid in ("x", "step_emb") or vid in self.emb_nodes:
+            if vid not in self.materialized:
                 continue
             sid = self._storage_id(vid)
             col = 0
@@ -677,6 +680,40 @@ class Plan:
 
     def flops_tail(self) -> float:
         return sum(u.gemm_flops for u in self.tail_units)
+
+
+def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = None) -> dict:
+    """Arena / scratch bytes the device plan would reserve, computed without a GPU.
+
+    Builds the plan's layout on the ``meta`` device (shapes only), so the device
+    analog of the reference's static peak model (grouping.py:334-450) can be
+    checked and reported anywhere.
+    """
+    cfg = cfg or ExecConfig()
+    dw = D.DeviceWeights.__new__(D.DeviceWeights)
+    dw.dev = torch.device("meta")
+    dw.p = {}
+    for n in graph.nodes.values():
+        if n.kind is OpKind.CONV2D and graph.nodes[n.id].inputs[0] != "x":
+            dw.p[n.id] = {"w": None}
+        elif n.kind is OpKind.LINEAR:
+            dw.p[n.id] = {"w32": torch.empty(1, 1, device="meta"), "bias": torch.empty(1, device="meta")}
+        elif n.param_ref:
+            dw.p[n.id] = {}
+    plan = Plan.__new__(Plan)
+    plan.graph, plan.grouped, plan.dw = graph, grouped, dw
+    plan.cfg = ExecConfig(spatial_k=cfg.spatial_k, temporal_k=cfg.temporal_k, scratch_budget=cfg.scratch_budget,
+                          device="meta")
+    plan.dev = dw.dev
+    plan.shapes = infer_shapes(graph)
+    plan.topo = graph.topo_order()
+    plan.pos = {n: i for i, n in enumerate(plan.topo)}
+    plan.cons = graph.consumers()
+    plan.values, plan.fused_adds, plan.epilogue_of, plan.units, plan.emb_nodes = {}, {}, {}, [], []
+    plan.exchanger = None
+    plan._analyse()
+    plan._layout()
+    return {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers)}
 
 
 def stream_handle() -> int:
