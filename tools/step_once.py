@@ -20,6 +20,7 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--backend", type=int, default=0)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--detail", action="store_true")
+ap.add_argument("--key-only", action="store_true", help="one key step, no tail step")
 a = ap.parse_args()
 cfg = UNetConfig(**CONFIGS[a.config])
 den = Denoiser(cfg, ExecConfig(gemm_backend=a.backend), K=2)
@@ -27,7 +28,8 @@ den.set_latent(initial_latent(cfg))
 st = torch.cuda.current_stream().cuda_stream
 for _ in range(a.reps):
     den.plan.run_full(st, den.emb_table[0].data_ptr())
-    den.plan.run_tail(st)
+    if not a.key_only:
+        den.plan.run_tail(st)
 torch.cuda.synchronize()
 print("ok", len(den.plan.units), "units")
 if a.detail:
