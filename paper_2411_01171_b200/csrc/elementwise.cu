@@ -41,7 +41,33 @@ __global__ void gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits, d
 #pragma unroll
     for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.0;
     if (active) {
-      for (int r = r0 + lane_r; r < r1; r += rows_per_iter) {
+      // 4 independent 16-byte loads in flight per thread, then fp32 partials -> fp64
+      int r = r0 + lane_r;
+      for (; r + 3 * rows_per_iter < r1; r += 4 * rows_per_iter) {
+        bf16x8 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r + u * rows_per_iter) + vbase * 8);
+        float fs[8], fq[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) fs[j] = fq[j] = 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float f[8];
+          unpack8(v[u], f);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            fs[j] += f[j];
+            fq[j] += f[j] * f[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s[j] += fs[j];
+          q[j] += fq[j];
+        }
+      }
+      for (; r < r1; r += rows_per_iter) {
         bf16x8 v = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r) + vbase * 8);
         float f[8];
         unpack8(v, f);
@@ -103,7 +129,7 @@ __global__ void gn_finalize_kernel(const double2* partial, int frames, int split
 
 // y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]); one block covers a
 // chunk of one frame's rows with the frame's per-channel tables in shared memory.
-constexpr int GNA_THREADS = 256, GNA_VEC_PER_THREAD = 8;
+constexpr int GNA_THREADS = 256, GNA_VEC_PER_THREAD = 16;
 __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(sf_view_t x, sf_view_t y, int n_inner, int C,
                                                                int groups, int chunks,
                                                                const float* __restrict__ mean,
@@ -123,11 +149,22 @@ __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(sf_view_t x, sf_v
   const int64_t total = (int64_t)n_inner * nvec;
   const int64_t per = (total + chunks - 1) / chunks;
   const int64_t e0 = chunk * per, e1 = min(total, e0 + per);
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+  constexpr int U = 4;
+  for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += U * blockDim.x) {
+    bf16x8 in[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = eb + u * blockDim.x;
+      if (e < e1) in[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, e / nvec) + (e % nvec) * 8);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const int64_t e = eb + u * blockDim.x;
+    if (e >= e1) break;
     const int v = (int)(e % nvec);
     const int64_t r = e / nvec;
     float f[8];
-    unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r) + v * 8), f);
+    unpack8(in[u], f);
     const float4* m4 = reinterpret_cast<const float4*>(tab + v * 8);
     const float4* s4 = reinterpret_cast<const float4*>(tab + C + v * 8);
     const float4* b4 = reinterpret_cast<const float4*>(tab + 2 * C + v * 8);
@@ -141,6 +178,7 @@ __global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(sf_view_t x, sf_v
       f[j] = act ? silu_f(t) : t;
     }
     *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, frame, r) + v * 8) = pack8(f);
+    }
   }
 }
 
