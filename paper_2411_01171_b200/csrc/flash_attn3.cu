@@ -21,8 +21,9 @@
 namespace sf {
 namespace fa3 {
 
-constexpr int BQ = 128, BKV = 128, THREADS = 192;
+constexpr int BQ = 128, BKV = 64, THREADS = 192;
 
+// TMEM: O [0,320) | S double buffer [320,384) [384,448) | P double buffer [448,480) [480,512)
 constexpr int O_COL = 0, S_COL = 320, P_COL = 448;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -170,7 +171,7 @@ __host__ __device__ constexpr uint32_t idesc256(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
-constexpr int NSLOT3 = 14, SLOT3 = 10240;
+constexpr int NSLOT3 = 7, SLOT3 = 20480;
 
 struct Params {
   int HW, frames, n_kv, n_qt;
@@ -182,8 +183,11 @@ template <int D>
 struct Layout3 {
   static constexpr int NCH = D / 64;
   static constexpr int Q_BYTES = NCH * BQ * 128;
-  static constexpr int K_HALF = (BKV / 2) * 128;      // [64 keys x 64 d]
-  static constexpr int V_HALF = (D / 4) * 128;        // [D/4 d x 64 keys]
+  // ring items (per CTA): K_j half = NCH sub-tiles [32 keys x 64 d]; V^T_j half = 2 sub-tiles [D/4 d x 64 keys]
+  static constexpr int K_SUB = (BKV / 2) * 128;
+  static constexpr int V_SUB = (D / 4) * 128;
+  static constexpr int K_HALF = NCH * K_SUB;
+  static constexpr int V_HALF = 2 * V_SUB;
   static constexpr int TOTAL = 1024 + Q_BYTES + NSLOT3 * SLOT3 + 256;
   static_assert(K_HALF <= SLOT3 && V_HALF <= SLOT3, "ring slot too small");
   static_assert(D % 64 == 0 && D <= 320 && (D / 2) % 32 == 0, "head dim (2-CTA TS MMA needs N % 32 == 0)");
@@ -202,11 +206,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* q_full = bars;               // leader: Q of both CTAs landed
   uint64_t* r_full = bars + 1;           // [NSLOT3] leader: both halves of a ring item landed
   uint64_t* r_empty = r_full + NSLOT3;   // [NSLOT3] per CTA: item consumed
-  uint64_t* s_full = r_empty + NSLOT3;   // per CTA
-  uint64_t* s_empty = s_full + 1;        // leader: 8 softmax warps read S
-  uint64_t* p_full = s_empty + 1;        // leader: 8 softmax warps wrote P
-  uint64_t* o_done = p_full + 1;         // per CTA
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* s_full = r_empty + NSLOT3;   // [2] per CTA
+  uint64_t* s_empty = s_full + 2;        // [2] leader: 8 softmax warps read S buffer b
+  uint64_t* p_full = s_empty + 2;        // [2] leader: 8 softmax warps wrote P buffer b
+  uint64_t* o_done = p_full + 2;         // [2] per CTA: P.V of a block using buffer b done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -220,10 +224,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&r_full[s], 1);
       mbar_init(&r_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_empty, 8);
-    mbar_init(p_full, 8);
-    mbar_init(o_done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 8);
+      mbar_init(&p_full[b], 8);
+      mbar_init(&o_done[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -256,21 +262,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         return leader_addr(&r_full[slot]);
       };
       auto load_k = [&](int j) {
-        for (int c = 0; c < L::NCH; ++c) {
-          const uint32_t b = item(2 * L::K_HALF);
-          tma3_2sm(&mK, b, sRing + slot * SLOT3, c * 64, j * BKV + (int)rank * (BKV / 2), f);
-          next();
-        }
+        const uint32_t b = item(2 * L::K_HALF);
+        for (int c = 0; c < L::NCH; ++c)
+          tma3_2sm(&mK, b, sRing + slot * SLOT3 + c * L::K_SUB, c * 64, j * BKV + (int)rank * (BKV / 2), f);
+        next();
       };
       load_k(0);
       for (int j = 0; j < nkv; ++j) {
         if (j + 1 < nkv) load_k(j + 1);
-        for (int kc = 0; kc < 2; ++kc)
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t b = item(2 * L::V_HALF);
-            tma3_2sm(&mV, b, sRing + slot * SLOT3, j * BKV + kc * 64, h * (D / 2) + (int)rank * (D / 4), f);
-            next();
-          }
+        const uint32_t b = item(2 * L::V_HALF);
+        for (int h = 0; h < 2; ++h)
+          tma3_2sm(&mV, b, sRing + slot * SLOT3 + h * L::V_SUB, j * BKV, h * (D / 2) + (int)rank * (D / 4), f);
+        next();
       }
     }
   } else if (warp == 1) {
@@ -289,46 +292,36 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       };
       auto issue_S = [&](int j) {
-        mbar_wait(s_empty, (j & 1) ^ 1);
+        const int b = j & 1;
+        mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);   // softmax of block j-2 has read buffer b
+        mbar_wait(&r_full[slot], ph);
         fence_after();
-#pragma unroll 1
-        for (int c = 0; c < L::NCH; ++c) {
-          mbar_wait(&r_full[slot], ph);
-          fence_after();
-          const uint64_t kd = sdesc(smem_u32(sRing + slot * SLOT3));
+        const uint64_t kd = sdesc(smem_u32(sRing + slot * SLOT3));
+#pragma unroll
+        for (int c = 0; c < L::NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma2_ss(tmem + S_COL, qd + (uint64_t)((c * BQ * 128 + k * 32) >> 4), kd + (uint64_t)(2 * k), idS,
-                    (c | k) != 0);
-          commit2(&r_empty[slot]);
-          next();
-        }
-        commit2(s_full);
+            mma2_ss(tmem + S_COL + b * BKV, qd + (uint64_t)((c * BQ * 128 + k * 32) >> 4),
+                    kd + (uint64_t)((c * L::K_SUB + k * 32) >> 4), idS, (c | k) != 0);
+        commit2(&r_empty[slot]);
+        next();
+        commit2(&s_full[b]);
       };
       auto issue_PV = [&](int j) {
-        mbar_wait(p_full, j & 1);
+        const int b = j & 1;
+        mbar_wait(&p_full[b], (j >> 1) & 1);
+        mbar_wait(&r_full[slot], ph);
         fence_after();
-#pragma unroll 1
-        for (int kc = 0; kc < 2; ++kc) {
-          const int s0 = slot;
-          mbar_wait(&r_full[slot], ph);
-          next();
-          const int s1 = slot;
-          mbar_wait(&r_full[slot], ph);
-          next();
-          fence_after();
-          const uint64_t v0 = sdesc(smem_u32(sRing + s0 * SLOT3));
-          const uint64_t v1 = sdesc(smem_u32(sRing + s1 * SLOT3));
+        const uint64_t vd = sdesc(smem_u32(sRing + slot * SLOT3));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t pa = tmem + P_COL + (uint32_t)((kc * 64 + k * 16) / 2);
-            mma2_ts(tmem + O_COL, pa, v0 + (uint64_t)(2 * k), idO, (j | kc | k) != 0);
-            mma2_ts(tmem + O_COL + D / 2, pa, v1 + (uint64_t)(2 * k), idO, (j | kc | k) != 0);
-          }
-          commit2(&r_empty[s0]);
-          commit2(&r_empty[s1]);
+        for (int k = 0; k < BKV / 16; ++k) {
+          const uint32_t pa = tmem + P_COL + b * (BKV / 2) + (uint32_t)(k * 8);
+          mma2_ts(tmem + O_COL, pa, vd + (uint64_t)(2 * k), idO, (j | k) != 0);
+          mma2_ts(tmem + O_COL + D / 2, pa, vd + (uint64_t)((L::V_SUB + k * 32) >> 4), idO, (j | k) != 0);
         }
-        commit2(o_done);
+        commit2(&r_empty[slot]);
+        next();
+        commit2(&o_done[b]);
       };
       issue_S(0);
       for (int j = 0; j < nkv; ++j) {
@@ -345,15 +338,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t s_empty_l = leader_addr(s_empty), p_full_l = leader_addr(p_full);
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < nkv; ++j) {
-      mbar_wait(s_full, j & 1);
+      const int b = j & 1;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
       fence_after();
       uint32_t r[BKV];
 #pragma unroll
-      for (int k = 0; k < BKV / 32; ++k) tld32(tmem + lane_off + S_COL + 32 * k, r + 32 * k);
+      for (int k = 0; k < BKV / 32; ++k) tld32(tmem + lane_off + S_COL + b * BKV + 32 * k, r + 32 * k);
       tld_wait();
       fence_before();
       __syncwarp();
-      if (lane == 0) arrive_cluster(s_empty_l);
+      if (lane == 0) arrive_cluster(s_empty_l + b * 8);
       const int kbase = j * BKV;
       if (kbase + BKV > p.HW) {
 #pragma unroll
@@ -377,18 +371,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t pk[BKV / 2];
 #pragma unroll
       for (int e = 0; e < BKV / 2; ++e) {
-        const float a = ex2(fmaf(__uint_as_float(r[2 * e]), c, -m_run));
-        const float b = ex2(fmaf(__uint_as_float(r[2 * e + 1]), c, -m_run));
-        ls0 += a;
-        ls1 += b;
-        bf162 h = __floats2bfloat162_rn(a, b);
+        const float a0 = ex2(fmaf(__uint_as_float(r[2 * e]), c, -m_run));
+        const float b0 = ex2(fmaf(__uint_as_float(r[2 * e + 1]), c, -m_run));
+        ls0 += a0;
+        ls1 += b0;
+        bf162 h = __floats2bfloat162_rn(a0, b0);
         pk[e] = *reinterpret_cast<uint32_t*>(&h);
       }
-      if (j > 0) {
-        mbar_wait(o_done, (j - 1) & 1);
+      // P buffer b was last read by P.V of block j-2
+      if (j >= 2) {
+        mbar_wait(&o_done[b], ((j - 2) >> 1) & 1);
         fence_after();
       }
       if (__any_sync(0xffffffffu, need)) {
+        // rescaling O needs every earlier P.V finished (block j-1 included)
+        mbar_wait(&o_done[b ^ 1], ((j - 1) >> 1) & 1);
+        fence_after();
 #pragma unroll 1
         for (int cc = 0; cc < D; cc += 32) {
           uint32_t o[32];
@@ -399,15 +397,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           tst32(tmem + lane_off + O_COL + cc, o);
         }
       }
-      tst32(tmem + lane_off + P_COL, pk);
-      tst32(tmem + lane_off + P_COL + 32, pk + 32);
+      tst32(tmem + lane_off + P_COL + b * (BKV / 2), pk);
       tst_wait();
       l_run = l_run * corr + ls0 + ls1;
       fence_before();
       __syncwarp();
-      if (lane == 0) arrive_cluster(p_full_l);
+      if (lane == 0) arrive_cluster(p_full_l + b * 8);
     }
-    mbar_wait(o_done, (nkv - 1) & 1);
+    mbar_wait(&o_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     fence_after();
     const float inv = 1.f / l_run;
     const int qrow = q0 + row;
