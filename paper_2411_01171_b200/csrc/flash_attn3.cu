@@ -1,18 +1,20 @@
-// Fused single-head spatial attention, version 3 (kernels.py:269-300): the v2
-// design (128-key blocks, P in TMEM, fine-grained TMA ring) on CTA pairs.
+// Fused single-head spatial attention on CTA pairs (kernels.py:269-300):
 //   O = softmax(Q K^T * scale) V per frame, head_dim D = C <= 320.
 //
-// Built around the shared-memory port, which the v1 profile showed to be the
-// limit (SS-mode MMAs re-read Q for every key block, P was written and read
-// twice through smem, and TMA writes K/V into the same port):
-//   * 128-key blocks: Q is re-read once per 128 keys instead of per 64;
-//   * P lives in TMEM and is the A operand of P.V (tcgen05.mma A-from-TMEM):
-//     no P smem traffic at all;
-//   * K_j / V^T_j stream through a 7-slot ring of 20 KB items (one 64-wide d
-//     chunk of K_j, or one [D/2 x 64 keys] quarter of V^T_j) so loads run
-//     several items ahead of the tensor core.
-// TMEM: O [0,D) fp32 | S [320,448) fp32 (one 128-key block) | P [448,512) bf16x2.
-// Warps: 0 TMA, 1 MMA issuer (+TMEM alloc), 2..5 softmax + epilogue (one row each).
+// Two query tiles of one frame form a CTA pair (cluster of 2).  The leader
+// issues tcgen05.mma.cta_group::2 with M = 256: rows 0-127 come from the
+// leader's Q/P, 128-255 from the peer's.  B operands are split along N, so each
+// CTA stages only half of every K block (32 of 64 keys) and half of every V^T
+// block (D/4 of every D/2-row half), fetched with 2-SM TMA whose completion is
+// counted on the leader's barrier.
+// TMEM (per CTA): O [0,D) fp32 | S[2] [320,448) fp32 | P[2] [448,512) bf16x2.
+// S and P are double-buffered so the MMA of block j+2 never waits for the
+// softmax of block j; P is the A operand of P.V straight from TMEM.
+// Online softmax with a lazy max (O/l rescaled only when a row max grows by
+// more than 2^8), ex2.approx, relaxed cross-CTA arrives (every TMEM access
+// they publish has completed).
+// Warps: 0 TMA (both CTAs), 1 MMA issuer (leader only) + TMEM alloc,
+//        2..5 softmax + epilogue (one query row per thread).
 #include "common.cuh"
 
 #include <cuda.h>
