@@ -259,11 +259,28 @@ def run_ours(args, world, rank, local):
     g_calls = sum(pf["by_call"][k]["calls"] for k in gemm_keys)
     achieved = g_fl / (g_ms * 1e9) if g_ms else 0.0
     peak_tf = peaks["bf16_tflops_sustained"]
-    roofline = {"bound": "tensor", "kernel": "+".join(gemm_keys), "achieved": round(achieved, 2), "peak": peak_tf,
-                "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": None,
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"r01_{args.config}_keystep_launch_list.txt")
+    if os.path.exists(tpath):
+        for l in open(tpath):
+            if l.startswith("{") and "gemm_dram_bytes_per_key_step" in l:
+                traffic = json.loads(l)["gemm_dram_bytes_per_key_step"]
+    roofline = {"bound": "tensor", "kernel": "tc_gemm_kernel (" + "+".join(gemm_keys) + "), all sf_gemm launches "
+                "of one key step", "achieved": round(achieved, 2), "peak": peak_tf,
+                "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": traffic,
+                "traffic_note": "DRAM read+write bytes of the same launches per key step, from the committed ncu "
+                                "launch list (profiles/)" if traffic else None,
                 "share_of_step": round(g_ms / pf["total_ms"], 4) if pf["total_ms"] else None,
                 "launches_per_key_step": g_calls, "flops_per_key_step": g_fl,
                 "peak_source": f"{peak_src} bf16_tflops_sustained"}
+    fa = pf["by_call"].get("sf_spatial_attention_core")
+    roofline_attn = None
+    if fa and fa["ms"]:
+        fa_tf = fa["flops"] / (fa["ms"] * 1e9)
+        roofline_attn = {"bound": "tensor", "kernel": "flash3_kernel (fused spatial attention, CTA pairs)",
+                         "achieved": round(fa_tf, 2), "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": round(fa_tf / peak_tf, 4), "share_of_step": round(fa["ms"] / pf["total_ms"], 4),
+                         "flops_per_key_step": fa["flops"]}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world, "steps": args.steps,
@@ -283,6 +300,7 @@ def run_ours(args, world, rank, local):
                 "h2d_bytes_per_step": int(x0.nbytes), "d2h_bytes_per_step": int(x0.nbytes)},
         "gpu_launches": launches_per_run * args.steps,
         "roofline": roofline,
+        "roofline_attention": roofline_attn,
         "profile": {"key_step_ms": round(pf["total_ms"], 3), "tail_step_ms": round(pt["total_ms"], 3),
                     "top": {k: {"ms": round(v["ms"], 3), "calls": v["calls"], "share": round(v["share"], 3),
                                 "tflops": round(v["tflops"], 1)} for k, v in list(pf["by_call"].items())[:8]}},

@@ -42,6 +42,12 @@ class CallProfiler:
                 flops = gemm_flops(args)
                 be = N.query("sf_gemm_backend", args)
                 name = f"sf_gemm[{'tcgen05' if be == 2 else 'mma.sync'}]"
+            elif name == "sf_spatial_attention_core":
+                frames, hw, c = a[4], a[5], a[6]
+                flops = 4.0 * frames * hw * hw * c          # S = q k^T and P v
+            elif name == "sf_temporal_attention_core":
+                b, t, n_inner, c = a[4], a[5], a[6], a[7]
+                flops = 4.0 * b * n_inner * t * t * c
             self.records.append((name, s, e, flops))
         N.call = timed
         return self
