@@ -19,14 +19,15 @@ void set_error(const std::string& m) { g_err = m; }
 // ---------------------------------------------------------------------------
 
 static int gn_splits(int frames, int n_inner) {
-  int want = (4 * num_sms() + frames - 1) / frames;      // >= ~4 CTAs per SM overall
-  int most = (n_inner + 127) / 128;                      // >= 128 rows per CTA
+  int want = (12 * num_sms() + frames - 1) / frames;     // several waves of light CTAs
+  int most = (n_inner + 63) / 64;                        // >= 64 rows per CTA
   int s = want < most ? want : most;
   return s < 1 ? 1 : s;
 }
 
 // partial[frame][split][c] = (sum x, sum x^2) over the split's rows, fp64
-__global__ void gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits, double2* partial) {
+__global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits,
+                                                            double2* partial) {
   const int frame = blockIdx.x / splits, split = blockIdx.x % splits;
   const int nvec = C / 8;
   const int rows_per_iter = blockDim.x / nvec > 0 ? blockDim.x / nvec : 1;
@@ -37,9 +38,9 @@ __global__ void gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits, d
   const int lane_r = nvec <= (int)blockDim.x ? (int)threadIdx.x / nvec : 0;
   const bool active = nvec <= (int)blockDim.x ? lane_r < rows_per_iter : true;
   for (int vbase = lane_v; vbase < nvec; vbase += (nvec <= (int)blockDim.x ? nvec : blockDim.x)) {
-    double s[8], q[8];
+    float s[8], q[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.0;
+    for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.f;
     if (active) {
       // 4 independent 16-byte loads in flight per thread, then fp32 partials -> fp64
       int r = r0 + lane_r;
@@ -74,14 +75,14 @@ __global__ void gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits, d
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           s[j] += f[j];
-          q[j] += (double)f[j] * f[j];
+          q[j] += f[j] * f[j];
         }
       }
     }
     if (nvec <= (int)blockDim.x) {
       if (active) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) red[lane_r * C + vbase * 8 + j] = make_double2(s[j], q[j]);
+        for (int j = 0; j < 8; ++j) red[lane_r * C + vbase * 8 + j] = make_double2((double)s[j], (double)q[j]);
       }
       __syncthreads();
       if (lane_r == 0) {
@@ -98,7 +99,7 @@ __global__ void gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits, d
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        partial[((int64_t)frame * splits + split) * C + vbase * 8 + j] = make_double2(s[j], q[j]);
+        partial[((int64_t)frame * splits + split) * C + vbase * 8 + j] = make_double2((double)s[j], (double)q[j]);
     }
   }
 }
