@@ -104,7 +104,7 @@ def test_batched_scores(backend, Fr, HW, C):
 
 
 @pytest.mark.parametrize("Fr,HW,C", [(2, 9216, 320), (3, 2304, 320), (2, 200, 320), (2, 576, 128), (1, 1000, 192),
-                                     (2, 4096, 256)])
+                                     (2, 4096, 256), (1, 1000, 128), (2, 296, 256), (1, 136, 320)])
 def test_flash_core(Fr, HW, C):
     """Fused tcgen05 attention core vs torch softmax(q k^T / sqrt(C)) v (fp32 math)."""
     if not N.query("sf_flash_supported", HW, C):
