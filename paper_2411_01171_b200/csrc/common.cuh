@@ -62,22 +62,29 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// 8 x bf16 <-> 8 x float through one 16-byte access
+// 8 x bf16 <-> 8 x float through one 16-byte access.  Backed by a uint4 so a
+// copy is one LDG/STG.128 (bf162 members have user-defined copy operators,
+// which made struct copies member-wise 4-byte accesses).
 struct alignas(16) bf16x8 {
-  bf162 h[4];
+  uint4 u;
 };
+__device__ __forceinline__ bf162 bf2_of(uint32_t w) { return *reinterpret_cast<const bf162*>(&w); }
+__device__ __forceinline__ uint32_t u32_of(bf162 h) { return *reinterpret_cast<const uint32_t*>(&h); }
 __device__ __forceinline__ void unpack8(const bf16x8& v, float* f) {
+  const uint32_t w[4] = {v.u.x, v.u.y, v.u.z, v.u.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    float2 t = __bfloat1622float2(v.h[j]);
+    float2 t = __bfloat1622float2(bf2_of(w[j]));
     f[2 * j] = t.x;
     f[2 * j + 1] = t.y;
   }
 }
 __device__ __forceinline__ bf16x8 pack8(const float* f) {
   bf16x8 v;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) v.h[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+  v.u.x = u32_of(__floats2bfloat162_rn(f[0], f[1]));
+  v.u.y = u32_of(__floats2bfloat162_rn(f[2], f[3]));
+  v.u.z = u32_of(__floats2bfloat162_rn(f[4], f[5]));
+  v.u.w = u32_of(__floats2bfloat162_rn(f[6], f[7]));
   return v;
 }
 

@@ -6,6 +6,8 @@
 // atomics) so results are bit-reproducible run to run.
 #include "common.cuh"
 
+#include <algorithm>
+
 #include <cmath>
 #include <mutex>
 
@@ -506,7 +508,7 @@ __device__ __forceinline__ void tq_load(bf16 (*dst)[TQ_LD], const sf_view_t& v, 
     if (t < T && c < cvalid) {
       val = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(v, (int64_t)b * T + t, pix) + col0 + c);
     } else {
-      val.h[0] = val.h[1] = val.h[2] = val.h[3] = __floats2bfloat162_rn(0.f, 0.f);
+      val.u = make_uint4(0u, 0u, 0u, 0u);
     }
     *reinterpret_cast<bf16x8*>(&dst[t][c]) = val;
   }
@@ -690,6 +692,135 @@ __global__ void __launch_bounds__(SC_THREADS) conv_smallcin_kernel(const float* 
 #pragma unroll
     for (int j = 0; j < SC_CO / 8; ++j) reinterpret_cast<bf16x8*>(dst)[j] = pack8(acc + 8 * j);
   }
+}
+
+// 3x3 conv with few input channels (the UNet in_conv: latent cin = 4 -> 320)
+// as a tensor-core implicit GEMM: K = 9*cin taps padded to 16, mma.sync bf16.
+// Each CTA gathers the im2col tile of 128 pixels straight from the fp32
+// latent into shared memory (taps outside the image are zero), keeps the whole
+// weight matrix [cout][K] resident, and writes bf16 output through a staging
+// tile so every row leaves as full 128-byte segments.
+constexpr int SCM_THREADS = 256, SCM_TILE = 128, SCM_NCH = 64;
+template <int KP>
+struct ScmLayout {
+  static constexpr int LDA = KP + 8;                 // +16 B per row: conflict-free ldmatrix
+  static constexpr int LDO = SCM_NCH + 8;
+  static constexpr int A_ELEMS = SCM_TILE * LDA;
+  static constexpr int O_ELEMS = SCM_TILE * LDO;
+};
+template <int KP>
+__global__ void __launch_bounds__(SCM_THREADS) conv_smallcin_mma_kernel(const float* __restrict__ x, int frames, int H,
+                                                                       int W, int cin, const float* __restrict__ wt,
+                                                                       const float* __restrict__ bias, int cout,
+                                                                       sf_view_t y) {
+  using L = ScmLayout<KP>;
+  extern __shared__ __align__(16) uint8_t scm_raw[];
+  bf16* sA = reinterpret_cast<bf16*>(scm_raw);
+  bf16* sO = sA + L::A_ELEMS;
+  bf16* sB = sO + L::O_ELEMS;  // [cout][LDA]
+  float* sBias = reinterpret_cast<float*>(sB + (size_t)cout * L::LDA);
+  const int K = 9 * cin;
+  // weights [9][cin][cout] fp32 -> [cout][k = tap*cin + ci] bf16, zero past K
+  for (int i = threadIdx.x; i < cout * KP; i += SCM_THREADS) {
+    const int co = i / KP, k = i % KP;
+    sB[co * L::LDA + k] = __float2bfloat16(k < K ? wt[(size_t)k * cout + co] : 0.f);
+  }
+  for (int i = threadIdx.x; i < cout; i += SCM_THREADS) sBias[i] = bias[i];
+  // K padding columns of the im2col tile stay zero for every tile
+  for (int i = threadIdx.x; i < SCM_TILE * (KP - K); i += SCM_THREADS)
+    sA[(i / (KP - K)) * L::LDA + K + i % (KP - K)] = __float2bfloat16(0.f);
+  const int HW = H * W;
+  const int64_t npix = (int64_t)frames * HW;
+  const int64_t ntiles = (npix + SCM_TILE - 1) / SCM_TILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t p0 = t * SCM_TILE;
+    __syncthreads();  // previous tile's sA / sO reads are done (and weights are in place)
+    // one (pixel, tap) per thread iteration: cin consecutive floats
+    for (int i = threadIdx.x; i < SCM_TILE * 9; i += SCM_THREADS) {
+      const int r = i / 9, tap = i - r * 9;
+      const int64_t pp = p0 + r;
+      bf16* dst = sA + r * L::LDA + tap * cin;
+      const float* src = nullptr;
+      if (pp < npix) {
+        const int f = (int)(pp / HW), pix = (int)(pp - (int64_t)f * HW);
+        const int py = pix / W, px = pix - py * W;
+        const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+        if (yy >= 0 && yy < H && xx >= 0 && xx < W) src = x + ((int64_t)f * HW + (int64_t)yy * W + xx) * cin;
+      }
+      if (cin == 4) {
+        float4 v = src ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<unsigned*>(dst) = pack_bf2(v.x, v.y);
+        *reinterpret_cast<unsigned*>(dst + 2) = pack_bf2(v.z, v.w);
+      } else {
+        for (int ci = 0; ci < cin; ++ci) dst[ci] = __float2bfloat16(src ? __ldg(src + ci) : 0.f);
+      }
+    }
+    __syncthreads();
+    // A fragments of this warp's 16 rows, all K
+    unsigned af[KP / 16][4];
+#pragma unroll
+    for (int kk = 0; kk < KP / 16; ++kk)
+      tq_ldsm_x4(af[kk], sA + (warp * 16 + (lane & 15)) * L::LDA + kk * 16 + (lane >> 4) * 8);
+    for (int n0 = 0; n0 < cout; n0 += SCM_NCH) {
+      float acc[SCM_NCH / 8][4];
+#pragma unroll
+      for (int j = 0; j < SCM_NCH / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KP / 16; ++kk) {
+#pragma unroll
+        for (int j = 0; j < SCM_NCH / 8; j += 2) {
+          // two n-tiles: lanes 0-15 -> n-tile j (k lo/hi), lanes 16-31 -> n-tile j+1
+          unsigned b[4];
+          const int nrow = n0 + j * 8 + (lane & 7) + ((lane >> 4) << 3);
+          tq_ldsm_x4(b, sB + nrow * L::LDA + kk * 16 + ((lane >> 3) & 1) * 8);
+          tq_mma(acc[j], af[kk], b[0], b[1]);
+          tq_mma(acc[j + 1], af[kk], b[2], b[3]);
+        }
+      }
+      // bias, bf16, staging tile [128][64]
+      const int r0 = warp * 16 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < SCM_NCH / 8; ++j) {
+        const int c = j * 8 + (lane & 3) * 2;
+        const float b0 = sBias[n0 + c], b1 = sBias[n0 + c + 1];
+        *reinterpret_cast<unsigned*>(sO + r0 * L::LDO + c) = pack_bf2(acc[j][0] + b0, acc[j][1] + b1);
+        *reinterpret_cast<unsigned*>(sO + (r0 + 8) * L::LDO + c) = pack_bf2(acc[j][2] + b0, acc[j][3] + b1);
+      }
+      __syncthreads();
+      // 128 rows x 128 B: 8 threads per row, 16 B each
+      for (int i = threadIdx.x; i < SCM_TILE * (SCM_NCH / 8); i += SCM_THREADS) {
+        const int r = i >> 3, v = i & 7;
+        const int64_t pp = p0 + r;
+        if (pp < npix) {
+          const int f = (int)(pp / HW);
+          bf16* dst = row_ptr<bf16>(y, f, pp - (int64_t)f * HW) + n0 + v * 8;
+          *reinterpret_cast<bf16x8*>(dst) = *reinterpret_cast<const bf16x8*>(sO + r * L::LDO + v * 8);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int KP>
+static sf_status conv_smallcin_mma_launch(const float* x, int frames, int H, int W, int cin, const float* w,
+                                          const float* bias, int cout, sf_view_t y, cudaStream_t st) {
+  using L = ScmLayout<KP>;
+  const size_t smem = (size_t)(L::A_ELEMS + L::O_ELEMS + cout * L::LDA) * sizeof(bf16) + cout * sizeof(float);
+  static size_t cfg = 0;
+  if (smem > 48 * 1024 && smem > cfg) {
+    cudaFuncSetAttribute(conv_smallcin_mma_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cfg = smem;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_smallcin_mma_kernel<KP>, SCM_THREADS, smem);
+  const int64_t ntiles = ((int64_t)frames * H * W + SCM_TILE - 1) / SCM_TILE;
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));
+  conv_smallcin_mma_kernel<KP><<<(unsigned)grid, SCM_THREADS, smem, st>>>(x, frames, H, W, cin, w, bias, cout, y);
+  return launch_status("sf_conv3x3_smallcin(mma)");
 }
 
 __global__ void gemv_kernel(const float* __restrict__ Wm, const float* __restrict__ e, const float* __restrict__ b,
@@ -1006,10 +1137,18 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
                               const float* bias, int32_t cout, sf_view_t y, void* stream) {
   SF_CHECK_ARG(cin >= 1 && cin <= 16 && cout % 8 == 0 && cout <= 1280, SF_ERR_SHAPE,
                "need cin <= 16, cout % 8 == 0, cout <= 1280");
-  SF_CHECK_ARG(view_vec8_ok(y) && aligned16(w), SF_ERR_PARAM, "unaligned view or weights");
+  SF_CHECK_ARG(view_vec8_ok(y) && aligned16(w) && (cin != 4 || aligned16(x)), SF_ERR_PARAM,
+               "unaligned view, weights or latent");
   const size_t smem = (size_t)9 * cin * cout * sizeof(float);
   SF_CHECK_ARG(smem <= 200 * 1024, SF_ERR_SHAPE, "in_conv weights exceed shared memory");
   cudaStream_t st = (cudaStream_t)stream;
+  // tensor-core path: K = 9*cin padded to 16, whole cout resident in smem
+  if (cout % SCM_NCH == 0 && cout <= 640 && 9 * cin <= 96) {
+    const int kp = (9 * cin + 15) / 16 * 16;
+    if (kp <= 16) return conv_smallcin_mma_launch<16>(x, frames, H, W, cin, w, bias, cout, y, st);
+    if (kp <= 48) return conv_smallcin_mma_launch<48>(x, frames, H, W, cin, w, bias, cout, y, st);
+    return conv_smallcin_mma_launch<96>(x, frames, H, W, cin, w, bias, cout, y, st);
+  }
   if (cout % 32 == 0) {
     static size_t cfg32 = 0;
     if (smem > 48 * 1024 && smem > cfg32) {

@@ -73,7 +73,7 @@ def apply_kernel(kind: OpKind, inputs: Sequence[Tensor5D], params: Mapping | Non
             x = to_rows(inputs[0], torch.float32)
             y = torch.empty(orows, out_s.c, dtype=torch.bfloat16, device=dev)
             N.call("sf_conv3x3_smallcin", x.data_ptr(), frames, s.h, s.w, s.c, p["wt32"].data_ptr(),
-                   p["bias"].data_ptr(), out_s.c, Rows(y).view(), st)
+                   p["bias"].data_ptr(), out_s.c, Rows(y, 0, hw).view(), st)
             return from_rows(y, out_s)
         x = to_rows(inputs[0])
         if out_s.c % 8:

@@ -65,7 +65,7 @@ def _oracle_kernel(kind, x, params, attrs):
 
 
 @pytest.mark.parametrize("backend", [1, 0])
-@pytest.mark.parametrize("case", ["conv_l0", "conv_cat", "tconv", "linear", "sattn", "tattn"])
+@pytest.mark.parametrize("case", ["conv_l0", "conv_cat", "conv_in", "conv_in8", "tconv", "linear", "sattn", "tattn"])
 def test_sd_width_kernels_vs_oracle(case, backend):
     """SD-width channel counts (multiples of 64) at reduced spatial size, both GEMM backends."""
     rng = np.random.default_rng(11)
@@ -77,6 +77,12 @@ def test_sd_width_kernels_vs_oracle(case, backend):
         x = rng.standard_normal((1, 2, 960, 8, 8))
         p = {"weight": rng.uniform(-.2, .2, (640, 960, 3, 3)) / np.sqrt(8640) * 2.5, "bias": rng.standard_normal(640)}
         kind, attrs = OpKind.CONV2D, {"out_channels": 640}
+    elif case in ("conv_in", "conv_in8"):
+        # latent-width input conv (cin 4 / 8): the tensor-core small-channel path
+        ci, co = (4, 320) if case == "conv_in" else (8, 64)
+        x = rng.standard_normal((1, 3, ci, 20, 27))
+        p = {"weight": rng.uniform(-.2, .2, (co, ci, 3, 3)) / np.sqrt(9 * ci) * 2.5, "bias": rng.standard_normal(co)}
+        kind, attrs = OpKind.CONV2D, {"out_channels": co}
     elif case == "tconv":
         x = rng.standard_normal((1, 25, 320, 4, 8))
         p = {"weight": rng.uniform(-.2, .2, (320, 320, 3)) / np.sqrt(960) * 2.5, "bias": rng.standard_normal(320)}
