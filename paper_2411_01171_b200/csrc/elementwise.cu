@@ -7,6 +7,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <cmath>
 #include <mutex>
@@ -21,13 +22,16 @@ void set_error(const std::string& m) { g_err = m; }
 // ---------------------------------------------------------------------------
 
 static int gn_splits(int frames, int n_inner) {
-  int want = (12 * num_sms() + frames - 1) / frames;     // several waves of light CTAs
+  // ~2 CTAs per SM: each partial is a full (C) row of fp64 sums the finalize
+  // pass has to walk, so long CTAs beat many light ones (measured on B200)
+  int want = (2 * num_sms() + frames - 1) / frames;
   int most = (n_inner + 63) / 64;                        // >= 64 rows per CTA
   int s = want < most ? want : most;
   return s < 1 ? 1 : s;
 }
 
 // partial[frame][split][c] = (sum x, sum x^2) over the split's rows, fp64
+constexpr int GN_U = 8;
 __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits,
                                                             double2* partial) {
   const int frame = blockIdx.x / splits, split = blockIdx.x % splits;
@@ -44,18 +48,18 @@ __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_i
 #pragma unroll
     for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.f;
     if (active) {
-      // 4 independent 16-byte loads in flight per thread, then fp32 partials -> fp64
+      // GN_U independent 16-byte loads in flight per thread, then fp32 partials -> fp64
       int r = r0 + lane_r;
-      for (; r + 3 * rows_per_iter < r1; r += 4 * rows_per_iter) {
-        bf16x8 v[4];
+      for (; r + (GN_U - 1) * rows_per_iter < r1; r += GN_U * rows_per_iter) {
+        bf16x8 v[GN_U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < GN_U; ++u)
           v[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, r + u * rows_per_iter) + vbase * 8);
         float fs[8], fq[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) fs[j] = fq[j] = 0.f;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < GN_U; ++u) {
           float f[8];
           unpack8(v[u], f);
 #pragma unroll
@@ -130,57 +134,62 @@ __global__ void gn_finalize_kernel(const double2* partial, int frames, int split
   }
 }
 
-// y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]); one block covers a
-// chunk of one frame's rows with the frame's per-channel tables in shared memory.
-constexpr int GNA_THREADS = 256, GNA_VEC_PER_THREAD = 16;
-__global__ void __launch_bounds__(GNA_THREADS) gn_apply_kernel(sf_view_t x, sf_view_t y, int n_inner, int C,
-                                                               int groups, int chunks,
-                                                               const float* __restrict__ mean,
-                                                               const float* __restrict__ rstd,
-                                                               const float* __restrict__ gamma,
-                                                               const float* __restrict__ beta, int act) {
-  extern __shared__ float tab[];  // [3][C]: mean, scale, beta per channel
+// y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]).  One block
+// covers a chunk of one frame's rows; each thread owns one 8-channel vector
+// (its mean / scale / shift live in registers) and walks rows with four
+// 16-byte loads in flight -- no per-element index arithmetic.
+__global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y, int n_inner, int C, int groups,
+                                                       int chunks, const float* __restrict__ mean,
+                                                       const float* __restrict__ rstd,
+                                                       const float* __restrict__ gamma,
+                                                       const float* __restrict__ beta, int act) {
   const int frame = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
   const int cg = C / groups, nvec = C / 8;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    const int g = c / cg;
-    tab[c] = mean[frame * groups + g];
-    tab[C + c] = rstd[frame * groups + g] * gamma[c];
-    tab[2 * C + c] = beta[c];
-  }
-  __syncthreads();
-  const int64_t total = (int64_t)n_inner * nvec;
-  const int64_t per = (total + chunks - 1) / chunks;
-  const int64_t e0 = chunk * per, e1 = min(total, e0 + per);
-  constexpr int U = 4;
-  for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += U * blockDim.x) {
-    bf16x8 in[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = eb + u * blockDim.x;
-      if (e < e1) in[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, frame, e / nvec) + (e % nvec) * 8);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-    const int64_t e = eb + u * blockDim.x;
-    if (e >= e1) break;
-    const int v = (int)(e % nvec);
-    const int64_t r = e / nvec;
-    float f[8];
-    unpack8(in[u], f);
-    const float4* m4 = reinterpret_cast<const float4*>(tab + v * 8);
-    const float4* s4 = reinterpret_cast<const float4*>(tab + C + v * 8);
-    const float4* b4 = reinterpret_cast<const float4*>(tab + 2 * C + v * 8);
-    const float4 m0 = m4[0], m1 = m4[1], s0 = s4[0], s1 = s4[1], b0 = b4[0], b1 = b4[1];
-    const float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-    const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  const int rpi = nvec <= (int)blockDim.x ? (int)blockDim.x / nvec : 1;   // rows per iteration
+  const int per = (n_inner + chunks - 1) / chunks;
+  const int r0 = chunk * per, r1 = min(n_inner, r0 + per);
+  for (int v = nvec <= (int)blockDim.x ? (int)threadIdx.x % nvec : (int)threadIdx.x; v < nvec;
+       v += nvec <= (int)blockDim.x ? nvec : (int)blockDim.x) {
+    const int lr = nvec <= (int)blockDim.x ? (int)threadIdx.x / nvec : 0;
+    if (lr >= rpi) return;
+    float mm[8], ss[8], bb[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float t = (f[j] - mm[j]) * ss[j] + bb[j];
-      f[j] = act ? silu_f(t) : t;
+      const int c = v * 8 + j, g = c / cg;
+      mm[j] = __ldg(mean + frame * groups + g);
+      ss[j] = __ldg(rstd + frame * groups + g) * __ldg(gamma + c);
+      bb[j] = __ldg(beta + c);
     }
-    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, frame, r) + v * 8) = pack8(f);
+    const bf16* src = row_ptr<const bf16>(x, frame, 0) + v * 8;
+    bf16* dst = row_ptr<bf16>(y, frame, 0) + v * 8;
+    const int64_t xld = x.ld, yld = y.ld;
+    constexpr int U = 8;
+    int r = r0 + lr;
+    for (; r + (U - 1) * rpi < r1; r += U * rpi) {
+      bf16x8 in[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) in[u] = *reinterpret_cast<const bf16x8*>(src + (int64_t)(r + u * rpi) * xld);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float f[8];
+        unpack8(in[u], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float t = (f[j] - mm[j]) * ss[j] + bb[j];
+          f[j] = act ? silu_f(t) : t;
+        }
+        *reinterpret_cast<bf16x8*>(dst + (int64_t)(r + u * rpi) * yld) = pack8(f);
+      }
+    }
+    for (; r < r1; r += rpi) {
+      float f[8];
+      unpack8(*reinterpret_cast<const bf16x8*>(src + (int64_t)r * xld), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float t = (f[j] - mm[j]) * ss[j] + bb[j];
+        f[j] = act ? silu_f(t) : t;
+      }
+      *reinterpret_cast<bf16x8*>(dst + (int64_t)r * yld) = pack8(f);
     }
   }
 }
@@ -1008,14 +1017,16 @@ sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t 
   SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
   SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
   SF_CHECK_ARG(aligned16(gamma) && aligned16(beta), SF_ERR_PARAM, "gamma/beta must be 16-byte aligned");
-  const int64_t per_frame = (int64_t)n_inner * (C / 8);
-  int chunks = (int)((per_frame + GNA_THREADS * GNA_VEC_PER_THREAD - 1) / (GNA_THREADS * GNA_VEC_PER_THREAD));
+  const int nvec = C / 8;
+  const int threads = nvec <= 256 ? (256 / nvec) * nvec : 256;
+  const int rpi = nvec <= 256 ? 256 / nvec : 1;
+  // ~32 rows per thread, but at least ~4 CTAs per SM on short frames (>= 4 rows per thread)
+  int chunks = (n_inner + rpi * 32 - 1) / (rpi * 32);
+  const int want = (4 * num_sms() + frames - 1) / frames, most = (n_inner + rpi * 4 - 1) / (rpi * 4);
+  if (chunks < std::min(want, most)) chunks = std::min(want, most);
   if (chunks < 1) chunks = 1;
-  const size_t smem = (size_t)3 * C * sizeof(float);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(gn_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  gn_apply_kernel<<<frames * chunks, GNA_THREADS, smem, (cudaStream_t)stream>>>(x, y, n_inner, C, groups, chunks, mean,
-                                                                               rstd, gamma, beta, act);
+  gn_apply_kernel<<<frames * chunks, threads, 0, (cudaStream_t)stream>>>(x, y, n_inner, C, groups, chunks, mean, rstd,
+                                                                        gamma, beta, act);
   return launch_status("sf_group_norm_apply");
 }
 

@@ -49,6 +49,11 @@ if a.detail:
             info = (f"mode={g.mode} M={g.n_outer * g.n_inner} N={g.N} K={g.cin * (9 if g.mode == 1 else 3 if g.mode == 2 else 1)}"
                     f" batch={g.batch} be={N.query('sf_gemm_backend', g)}")
             recs.append((name, info, s_, e_, gemm_flops(g)))
+        elif name in ("sf_group_norm_apply", "sf_layer_norm", "sf_group_norm_stats"):
+            fr, ni, c = args[2:5] if name != "sf_group_norm_stats" else args[1:4]
+            nbytes = fr * ni * c * 2 * (1 if name == "sf_group_norm_stats" else 2)
+            info = f"frames={fr} inner={ni} C={c} bytes={nbytes}"
+            recs.append((name, info, s_, e_, -nbytes))
         else:
             recs.append((name, info, s_, e_, 0.0))
     N.call = rec
@@ -57,4 +62,7 @@ if a.detail:
     N.call = orig
     for name, info, s_, e_, fl in recs:
         ms = s_.elapsed_time(e_)
-        print(f"{ms*1e3:9.1f} us  {fl/ (ms*1e9) if fl else 0:7.1f} TF  {name} {info}")
+        if fl < 0:
+            print(f"{ms*1e3:9.1f} us  {-fl / (ms * 1e6):7.1f} GB/s  {name} {info}")
+        else:
+            print(f"{ms*1e3:9.1f} us  {fl/ (ms*1e9) if fl else 0:7.1f} TF  {name} {info}")
