@@ -673,6 +673,43 @@ static int pick_bn(int N) {
   return 128;
 }
 
+// Tile width and CTA pairing from a wave-quantisation model: a persistent grid
+// of `slots` CTAs (pairs) runs ceil(tiles / slots) rounds, each as long as one
+// tile's per-CTA work (128 x BN x K) times a per-width efficiency factor.
+// Pairs and wide tiles win unless they cost whole extra rounds.
+static bool choose_tiling(int N, int64_t tiles_m, bool pair_ok, int* bn) {
+  // per-unit-work cost by tile width, measured on B200 conv/linear shapes:
+  // narrower MMAs pay a fixed issue cost (N=160 ~1.3x the cost of N=256)
+  auto eff = [](int b) { return b >= 256 ? 1.0 : b == 160 ? 1.3 : b == 128 ? 1.35 : 1.6; };
+  const int sms = num_sms();
+  int cands[4], nc = 0;
+  cands[nc++] = *bn;
+  if (N % 256 == 0 && N >= 1024 && *bn != 256) cands[nc++] = 256;
+  if (N % 160 == 0 && *bn != 160) cands[nc++] = 160;
+  if (N % 128 == 0 && *bn != 128) cands[nc++] = 128;
+  double best = 1e300;
+  bool best_pair = pair_ok;
+  int best_bn = *bn;
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool pr = pass == 0;
+    if (pr && !pair_ok) continue;
+    for (int c = 0; c < nc; ++c) {
+      const int b = cands[c];
+      const int64_t tn = (N + b - 1) / b;
+      const int64_t tiles = (pr ? (tiles_m + 1) / 2 : tiles_m) * tn;
+      const int64_t slots = pr ? sms / 2 : sms;
+      const double cost = (double)((tiles + slots - 1) / slots) * b * eff(b) * (pr ? 1.0 : 1.06);
+      if (cost < best * 0.999) {
+        best = cost;
+        best_pair = pr;
+        best_bn = b;
+      }
+    }
+  }
+  *bn = best_bn;
+  return best_pair;
+}
+
 }  // namespace tc
 
 bool gemm_tc_supported(const sf_gemm_args& a) {
@@ -772,10 +809,6 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   p.out = a.out;
   p.out_bstride = a.out_bstride;
   p.out_fp32 = a.out_fp32;
-  const int BN = pick_bn(a.N);
-  p.BN = BN;
-  p.tiles_n = (a.N + BN - 1) / BN;
-
   CUtensorMap ma, mb;
   const uint64_t es = 2;
   // CTA pairs (cta_group::2, M = 256) whenever there are two M-tiles to pair up;
@@ -842,6 +875,10 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   // the two CTAs of a pair share one B tile: with a per-batch B (attention scores) a
   // pair must not straddle two batches, i.e. each batch needs an even tile count
   if (a.batch > 1 && a.mode == SF_GEMM_PLAIN && ((int64_t)p.tiles_i * p.tiles_o) % 2) pair = false;
+  int BN = pick_bn(a.N);
+  pair = choose_tiling(a.N, p.tiles_m, pair, &BN);
+  p.BN = BN;
+  p.tiles_n = (a.N + BN - 1) / BN;
   {
     const int taps = p.taps;
     uint64_t dims[3] = {(uint64_t)taps * a.cin, (uint64_t)a.N, (uint64_t)(a.batch > 1 ? a.batch : 1)};
