@@ -450,13 +450,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
-        } else if (tcount == 0 && has_res && store_leader) {
-          // double staging: residual of the first tile; later ones are prefetched a tile ahead
-          mbar_expect_tx(&res_full[0], L::OUT_TILE);
-          if (p.mode == SF_GEMM_CONV3X3)
-            tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
-          else
-            tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
+        } else if (has_res && store_leader) {
+          // double staging: the first tile's residual now; every epilogue then
+          // prefetches the next tile's residual into the other buffer as soon
+          // as that buffer's previous store has been read out
+          if (tcount == 0) {
+            mbar_expect_tx(&res_full[0], L::OUT_TILE);
+            if (p.mode == SF_GEMM_CONV3X3)
+              tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
+            else
+              tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
+          }
+          const int64_t nt = tile + t_step;
+          if (nt < n_tiles) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            const MTile nm = decode_m(p, my_tm(nt));
+            const int nn0 = (int)(nt % p.tiles_n) * BN;
+            uint8_t* nbuf = sOut + (ob ^ 1) * L::OUT_TILE;
+            mbar_expect_tx(&res_full[ob ^ 1], L::OUT_TILE);
+            if (p.mode == SF_GEMM_CONV3X3)
+              tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.x0, nm.y0, nm.f);
+            else
+              tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.i0, nm.o0, nm.z);
+          }
         }
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -511,21 +527,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           else
             tma_store_4d(&mapO, sbuf, n0, mt.i0, mt.o0, mt.z);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          if (EPI == 2) {
-            // the other buffer's store (tile t-1) must drain before it is refilled
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            const int64_t nt = tile + t_step;
-            if (has_res && nt < n_tiles) {
-              const MTile nm = decode_m(p, my_tm(nt));
-              const int nn0 = (int)(nt % p.tiles_n) * BN;
-              uint8_t* nbuf = sOut + (ob ^ 1) * L::OUT_TILE;
-              mbar_expect_tx(&res_full[ob ^ 1], L::OUT_TILE);
-              if (p.mode == SF_GEMM_CONV3X3)
-                tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.x0, nm.y0, nm.f);
-              else
-                tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.i0, nm.o0, nm.z);
-            }
-          }
+          // the other buffer's store (tile t-1) must drain before it is refilled
+          if (EPI == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         }
         if (EPI == 2) asm volatile("bar.sync 1, 128;" ::: "memory");
         if (++acc == 2) {
