@@ -277,7 +277,7 @@ def run_ours(args, world, rank, local):
     roofline_attn = None
     if fa and fa["ms"]:
         fa_tf = fa["flops"] / (fa["ms"] * 1e9)
-        roofline_attn = {"bound": "tensor", "kernel": "flash3_kernel (fused spatial attention, CTA pairs)",
+        roofline_attn = {"bound": "tensor", "kernel": "flash5_kernel (fused spatial attention, CTA pairs, 96-key blocks)",
                          "achieved": round(fa_tf, 2), "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": round(fa_tf / peak_tf, 4), "share_of_step": round(fa["ms"] / pf["total_ms"], 4),
                          "flops_per_key_step": fa["flops"]}

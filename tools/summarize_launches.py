@@ -22,8 +22,11 @@ for r in data:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(",", ""))
+    name = r[ki].split("(")[0]
+    if name.startswith(("void at::", "at::")):
+        continue  # torch's own setup kernels (weight conversion), not the step
     launch[r[ii]][r[mi]] = v
-    names[r[ii]] = r[ki].split("(")[0]
+    names[r[ii]] = name
 agg = defaultdict(lambda: defaultdict(float))
 for lid, m in launch.items():
     n = names[lid]
