@@ -156,6 +156,13 @@ sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, 
 sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t W, int32_t cin,
                               const float* w /*[3][3][ci][co] fp32*/, const float* bias, int32_t cout,
                               sf_view_t y, void* stream);
+/* out_conv with tiny cout, second half: y holds the per-tap projections
+ * Y[f][p][tap*cout + co] = x[f][p] . W_tap[co] (fp32, row stride ldy, written by
+ * sf_gemm with the tap-major weight matrix); this sums the 9 shifted taps with
+ * zero padding: out[f][p][co] = bias[co] + sum_tap Y[f][p + off(tap)][tap*cout + co]
+ * (kernels.py:181-201 regrouped; fixed tap order).  out: fp32 rows view. */
+sf_status sf_conv3x3_tapsum(const float* y, int32_t ldy, int32_t frames, int32_t H, int32_t W, int32_t cout,
+                            const float* bias, sf_view_t out, void* stream);
 /* y[n] = W[n][:] . e + b[n] for a batch of step embeddings (res-block emb_proj) */
 sf_status sf_gemv_f32(const float* W, const float* e, const float* b, float* y, int32_t N, int32_t K,
                       void* stream);

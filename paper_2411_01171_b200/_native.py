@@ -64,6 +64,7 @@ _PROTOS = {
     "sf_spatial_attention_core": [View, View, vp, View, i32, i32, i32, f32, vp],
     "sf_temporal_attention_core": [View, i32, i32, View, i32, i32, i32, i32, f32, vp],
     "sf_conv3x3_smallcin": [vp, i32, i32, i32, i32, vp, vp, i32, View, vp],
+    "sf_conv3x3_tapsum": [vp, i32, i32, i32, i32, i32, vp, View, vp],
     "sf_gemv_f32": [vp, vp, vp, vp, i32, i32, vp],
     "sf_bcthw_to_rows_f32": [vp, vp, i32, i32, i32, vp],
     "sf_rows_to_bcthw_f32": [vp, vp, i32, i32, i32, vp],

@@ -832,6 +832,29 @@ static sf_status conv_smallcin_mma_launch(const float* x, int frames, int H, int
   return launch_status("sf_conv3x3_smallcin(mma)");
 }
 
+// out_conv (cout < 16) as "project then shift-and-sum": y = per-tap projections
+// [f][p][tap*cout + co] from one plain GEMM; each output sums its 9 shifted taps.
+__global__ void conv_tapsum_kernel(const float* __restrict__ y, int ldy, int frames, int H, int W, int cout,
+                                   const float* __restrict__ bias, sf_view_t out) {
+  const int HW = H * W;
+  const int64_t total = (int64_t)frames * HW * cout;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int co = (int)(idx % cout);
+    const int64_t pp = idx / cout;
+    const int f = (int)(pp / HW), pix = (int)(pp - (int64_t)f * HW);
+    const int py = pix / W, px = pix - py * W;
+    float acc = bias ? __ldg(bias + co) : 0.f;
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+      const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+      if (yy >= 0 && yy < H && xx >= 0 && xx < W)
+        acc += __ldg(y + ((int64_t)f * HW + (int64_t)yy * W + xx) * ldy + tap * cout + co);
+    }
+    row_ptr<float>(out, f, pix)[co] = acc;
+  }
+}
+
 __global__ void gemv_kernel(const float* __restrict__ Wm, const float* __restrict__ e, const float* __restrict__ b,
                             float* __restrict__ y, int N, int K) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -1180,6 +1203,15 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
                                                                                   cout, y);
   }
   return launch_status("sf_conv3x3_smallcin");
+}
+
+sf_status sf_conv3x3_tapsum(const float* y, int32_t ldy, int32_t frames, int32_t H, int32_t W, int32_t cout,
+                            const float* bias, sf_view_t out, void* stream) {
+  SF_CHECK_ARG(frames >= 1 && H >= 1 && W >= 1 && cout >= 1 && ldy >= 9 * cout, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(y && out.ptr, SF_ERR_PARAM, "null buffer");
+  const int64_t total = (int64_t)frames * H * W * cout;
+  conv_tapsum_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(y, ldy, frames, H, W, cout, bias, out);
+  return launch_status("sf_conv3x3_tapsum");
 }
 
 sf_status sf_gemv_f32(const float* W, const float* e, const float* b, float* y, int32_t N, int32_t K, void* stream) {

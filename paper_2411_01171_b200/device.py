@@ -88,6 +88,9 @@ class DeviceWeights:
                    "wt32": f32(w.transpose(2, 3, 1, 0).reshape(9, ci, co), d)}
             if ci % 8 == 0:
                 out["w"] = bf16(w.transpose(0, 2, 3, 1).reshape(co, 9 * ci), d)
+                if co < TAPWISE_MAX_COUT:
+                    # tap-major [(tap, co)][ci] for conv2d_tapwise (row = tap * co + c)
+                    out["w_taps"] = bf16(w.transpose(2, 3, 0, 1).reshape(9 * co, ci), d)
             return out
         if k is OpKind.TEMPORAL_CONV:
             w = np.asarray(prm["weight"], dtype=np.float64)
@@ -147,6 +150,25 @@ def conv2d(stream, x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue
     return gemm(stream, mode=N.GEMM_CONV3X3, n_outer=frames, n_inner=H * W, H=H, W=W, cin=cin, n=cout, a=x,
                 w=prm["w"], out=y, out_fp32=out_fp32, bias=prm["bias"], rowbias=epi.rowbias, act=epi.act,
                 res=epi.res, backend=backend)
+
+
+TAPWISE_MAX_COUT = 16
+
+
+def conv2d_tapwise(stream, x: Rows, out: Rows, frames, H, W, cin, cout, prm, ybuf: torch.Tensor, backend=0):
+    """3x3 conv with few output channels (the network's out_conv, 320 -> 4) into fp32 rows.
+
+    A padded-N implicit GEMM would issue 9*cin/16 narrow MMAs per 128 rows for 4 useful
+    columns; instead one plain GEMM projects every pixel onto all 9 taps,
+    Y[p][tap*cout + c] = x[p] . W_tap[c] (K = cin, N = 9*cout), and sf_conv3x3_tapsum adds the
+    9 shifted taps (zero padding) plus the bias: the same sum as kernels.py:181-201 regrouped.
+    ``ybuf``: fp32 scratch with >= frames*H*W rows of >= 9*cout columns.
+    """
+    HW = H * W
+    gemm(stream, mode=N.GEMM_PLAIN, n_outer=frames, n_inner=HW, cin=cin, n=9 * cout, a=x, w=prm["w_taps"],
+         out=Rows(ybuf, 0, HW), out_fp32=True, backend=backend)
+    N.call("sf_conv3x3_tapsum", ybuf.data_ptr(), ybuf.stride(0), frames, H, W, cout, prm["bias"].data_ptr(),
+           out.view(), stream)
 
 
 def temporal_conv(stream, x: Rows, y: Rows, bt, T, n_inner, cin, cout, prm, epi: Epilogue, backend=0):

@@ -491,6 +491,8 @@ class Plan:
             if o.kind is OpKind.SPATIAL_ATTENTION:
                 hw = shape.h * shape.w
                 specs.update(D.spatial_attention_scratch(fmax * hw, hw, shape.c))
+            if o.kind is OpKind.CONV2D and "w_taps" in self.dw.p.get(o.id, {}):
+                specs["taps_y"] = (fmax * out_shape.h * out_shape.w, 9 * out_shape.c, torch.float32)
             shape = out_shape
             i += 2 if fuse_act else 1
         if gn_need:
@@ -536,9 +538,14 @@ class Plan:
                             N.call("sf_conv3x3_smallcin", lat.data_ptr(), nf, ish.h, ish.w, ish.c,
                                    prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), st)
                         elif last and eps_out:
-                            # out_conv: fp32 network output straight from the GEMM epilogue
+                            # out_conv: fp32 network output (per-tap projection + shifted sum for tiny cout)
                             out = Rows(self.eps, sl[0] * ohw, ohw)
-                            D.conv2d(st, X, out, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend, out_fp32=True)
+                            if "w_taps" in prm and epi.res is None and epi.rowbias is None and not act:
+                                D.conv2d_tapwise(st, X, out, nf, ish.h, ish.w, ish.c, osh.c, prm, scratch["taps_y"],
+                                                 backend)
+                            else:
+                                D.conv2d(st, X, out, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend,
+                                         out_fp32=True)
                         else:
                             D.conv2d(st, X, Y, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend)
                     elif k is OpKind.LINEAR:

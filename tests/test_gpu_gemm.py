@@ -69,6 +69,23 @@ def test_conv3x3(backend, F_, H, W, C, Co):
 
 
 @pytest.mark.parametrize("backend", [1, 2])
+@pytest.mark.parametrize("F_,H,W,C,Co", [(3, 72, 128, 320, 4), (2, 9, 13, 64, 8), (1, 5, 7, 128, 3)])
+def test_conv3x3_tapwise(backend, F_, H, W, C, Co):
+    """out_conv path: per-tap projection GEMM + shifted sum, fp32 out, vs torch conv2d."""
+    torch.manual_seed(5)
+    x = rnd(F_, H, W, C)
+    w = rnd(Co, C, 3, 3, scale=(9 * C) ** -0.5)
+    bias = torch.randn(Co, device=dev)
+    prm = {"w_taps": w.permute(2, 3, 0, 1).reshape(9 * Co, C).contiguous(), "bias": bias}
+    ybuf = torch.empty(F_ * H * W, 9 * Co, dtype=torch.float32, device=dev)
+    out = torch.empty(F_ * H * W, Co, dtype=torch.float32, device=dev)
+    D.conv2d_tapwise(torch.cuda.current_stream().cuda_stream, Rows(x.view(-1, C), 0, H * W), Rows(out, 0, H * W),
+                     F_, H, W, C, Co, prm, ybuf, backend=backend)
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float(), bias, padding=1).permute(0, 2, 3, 1).reshape(-1, Co)
+    assert rel(out, ref) <= 1e-3
+
+
+@pytest.mark.parametrize("backend", [1, 2])
 @pytest.mark.parametrize("B,T,P,C,band", [(1, 25, 576, 320, None), (1, 25, 144, 128, None), (2, 8, 64, 64, None),
                                           (1, 16, 1024, 64, (100, 612))])
 def test_tconv(backend, B, T, P, C, band):

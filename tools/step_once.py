@@ -21,6 +21,7 @@ ap.add_argument("--backend", type=int, default=0)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--detail", action="store_true")
 ap.add_argument("--key-only", action="store_true", help="one key step, no tail step")
+ap.add_argument("--tail", action="store_true", help="--detail profiles the tail (rehash) step instead")
 a = ap.parse_args()
 cfg = UNetConfig(**CONFIGS[a.config])
 den = Denoiser(cfg, ExecConfig(gemm_backend=a.backend), K=2)
@@ -57,7 +58,10 @@ if a.detail:
         else:
             recs.append((name, info, s_, e_, 0.0))
     N.call = rec
-    den.plan.run_full(st, den.emb_table[0].data_ptr())
+    if a.tail:
+        den.plan.run_tail(st)
+    else:
+        den.plan.run_full(st, den.emb_table[0].data_ptr())
     torch.cuda.synchronize()
     N.call = orig
     for name, info, s_, e_, fl in recs:
