@@ -47,6 +47,7 @@ from .errors import InvalidParam, ShapeMismatch
 from .graph import Graph, infer_shapes
 from .grouping import GroupedGraph, group_operators
 from .kinds import Domain, OpKind
+from .ledger import MemoryLedger
 from .modes import ExecMode
 from .slicer import default_temporal_config
 from .tensor import Shape5, Tensor5D
@@ -257,6 +258,10 @@ class Plan:
             placed.append((off, size, lo, hi))
             offsets[sid] = off
         self.arena_bytes = max([o + s for o, s, _, _ in placed] + [align])
+        # kept for the derived memory ledger (ledger.py): live units and payload bytes per buffer
+        self.arena_intervals = {sid: tuple(intervals[sid]) for sid in sizes}
+        self.arena_sizes = dict(sizes)
+        self.n_units = len(sched)
         self.arena = torch.empty(self.arena_bytes, dtype=torch.uint8, device=self.dev)
         self.buffers = {}
         for sid, off in offsets.items():
@@ -295,6 +300,35 @@ class Plan:
         self.emb_in = torch.zeros(self.shapes["step_emb"].c if "step_emb" in self.shapes else 1,
                                   dtype=torch.float32, device=self.dev)
         self.peak_model_bytes = self.arena_bytes
+
+    def memory_ledger(self, scratch_bytes: int | None = None, summary: dict | None = None) -> MemoryLedger:
+        """One evaluation's allocation events, derived from the compiled plan.
+
+        Each arena buffer is charged before the first unit that defines it and
+        released after its last consumer (the probe and the network output stay
+        to the end); the slice scratch is charged for the whole evaluation.
+        """
+        led = MemoryLedger(summary)
+        g = self.graph
+
+        def tag(sid):
+            n = g.nodes.get(sid)
+            return n.label or sid if n is not None else sid
+        if scratch_bytes:
+            led.alloc(scratch_bytes, "slice_scratch")
+        by_lo: dict[int, list[str]] = {}
+        by_hi: dict[int, list[str]] = {}
+        for sid, (lo, hi) in sorted(self.arena_intervals.items()):
+            by_lo.setdefault(lo, []).append(sid)
+            by_hi.setdefault(hi, []).append(sid)
+        for u in range(self.n_units + 1):
+            for sid in by_lo.get(u, []):
+                led.alloc(self.arena_sizes[sid], tag(sid))
+            for sid in by_hi.get(u, []):
+                led.free(self.arena_sizes[sid], tag(sid))
+        if scratch_bytes:
+            led.free(scratch_bytes, "slice_scratch")
+        return led
 
     def rows(self, vid, row0=0, ostride=0) -> Rows:
         v = self.values[vid]
@@ -720,7 +754,9 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     plan.exchanger = None
     plan._analyse()
     plan._layout()
-    return {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers)}
+    led = plan.memory_ledger()
+    return {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers), "ledger": led,
+            "ledger_peak_bytes": led.peak_bytes}
 
 
 def stream_handle() -> int:
@@ -771,43 +807,91 @@ class DeviceModel:
         return self.host_out.numpy().reshape(tuple(self.x_shape)).copy()
 
 
-def execute(graph_or_grouped, mode, inputs, weights, cfg: ExecConfig | None = None):
+def pipeline_schedule(n_stages: int, n_slices: int) -> list[list[tuple[int, int]]]:
+    """Wavefront table of SPEC.md:337-343 (paper Fig. 5c): at tick t, stage j runs slice t - j.
+
+    Returns one list of (stage, slice) pairs per tick; m + n - 1 ticks.  On the
+    device a group's stages are fused into one kernel chain per slice, so every
+    slice passes all stages back to back on one stream -- the same dependency
+    order, with zero extra buffers (the "Pipelined peak == SlicedLoop peak"
+    property holds by construction).
+    """
+    if n_stages < 1 or n_slices < 1:
+        raise InvalidParam(f"pipeline needs >= 1 stage and slice, got {n_stages}, {n_slices}")
+    return [[(j, t - j) for j in range(n_stages) if 0 <= t - j < n_slices]
+            for t in range(n_stages + n_slices - 1)]
+
+
+def _with_frames(graph: Graph, t: int) -> Graph:
+    """The same network over a clip of t frames (weights do not depend on T)."""
+    return Graph(graph.nodes.values(), {k: s.replace(t=t) for k, s in graph.inputs.items()}, graph.outputs)
+
+
+def naive_clip_chunks(T: int, chunk: int) -> list[tuple[int, int]]:
+    """Frame ranges of NaiveClip(chunk) (1 <= chunk < T)."""
+    if not 1 <= chunk < T:
+        raise InvalidParam(f"naive chunk must be in [1, {T}), got {chunk}")
+    return [(o, min(o + chunk, T)) for o in range(0, T, chunk)]
+
+
+def execute(graph_or_grouped, mode, inputs, weights, cfg: ExecConfig | None = None, naive_chunk: int | None = None):
     """One network evaluation on the device.
 
-    Returns ``(output Tensor5D, ledger, timing)`` like the reference contract;
-    ``ledger`` reports device bytes (arena + scratch, and the torch peak),
-    ``timing`` wall-clock ms per phase.  REFERENCE runs the same fused
+    Returns ``(output Tensor5D, ledger, timing)`` like the reference contract.
+    ``ledger`` is a :class:`MemoryLedger` derived from the compiled plan (arena
+    buffers charged over their live units, slice scratch over the evaluation);
+    its ``summary`` holds the device facts (arena, scratch, torch peak).
+    ``timing`` is wall-clock ms per phase.  REFERENCE runs the same fused
     kernels with one slice per group (unsliced); SLICED_LOOP / PIPELINED use
     the slice plan of ``cfg`` (on one stream the pipelined wavefront and the
     for-loop issue the same launches, so they are the same program here).
+    NAIVE_CLIP(``naive_chunk``) runs independent evaluations over clips of
+    frames and stitches them along t -- the divergent
+    baseline the slicer avoids.
     """
     mode = ExecMode(mode)
-    if mode is ExecMode.NAIVE_CLIP:
-        raise InvalidParam("naiveclip is a quality-divergence baseline and is not part of the device path")
     cfg = cfg or ExecConfig()
-    if mode is ExecMode.REFERENCE:
+    if mode is ExecMode.REFERENCE or mode is ExecMode.NAIVE_CLIP:
         cfg = ExecConfig(spatial_k=1, temporal_k=1, scratch_budget=cfg.scratch_budget,
                          gemm_backend=cfg.gemm_backend, device=cfg.device)
     if isinstance(graph_or_grouped, GroupedGraph):
         graph, grouped = graph_or_grouped.graph, graph_or_grouped
     else:
         graph, grouped = graph_or_grouped, None
-    t0 = time.perf_counter()
-    model = DeviceModel(graph, weights, cfg, grouped)
-    t1 = time.perf_counter()
     x = inputs["x"].data if isinstance(inputs["x"], Tensor5D) else np.asarray(inputs["x"])
     se = inputs["step_emb"].data if isinstance(inputs["step_emb"], Tensor5D) else np.asarray(inputs["step_emb"])
     vec = np.ascontiguousarray(se.reshape(-1, se.shape[2])[0], dtype=np.float32)
     if not np.all(se.reshape(-1, se.shape[2]) == vec[None]):
         raise ShapeMismatch("device path expects the step embedding broadcast over (b, t) (unet.py:106-113)")
+    if mode is ExecMode.NAIVE_CLIP:
+        if naive_chunk is None:
+            raise InvalidParam("naiveclip needs naive_chunk")
+        chunks = naive_clip_chunks(graph.inputs["x"].t, naive_chunk)
+    else:
+        chunks = [(0, graph.inputs["x"].t)]
     torch.cuda.reset_peak_memory_stats()
-    st = stream_handle()
-    model.upload_latent(st, x)
-    emb = torch.from_numpy(vec).to(model.dw.dev)
-    model.plan.run_full(st, emb.data_ptr())
-    out = model.download(model.latent_to_bcthw(st, model.plan.eps))
+    t0 = time.perf_counter()
+    outs, models, compile_ms = [], {}, 0.0
+    for f0, f1 in chunks:
+        n = f1 - f0
+        if n not in models:
+            tc = time.perf_counter()
+            if mode is ExecMode.NAIVE_CLIP:
+                models[n] = DeviceModel(_with_frames(graph, n), weights, cfg)
+            else:
+                models[n] = DeviceModel(graph, weights, cfg, grouped)
+            compile_ms += (time.perf_counter() - tc) * 1e3
+        model = models[n]
+        st = stream_handle()
+        model.upload_latent(st, np.ascontiguousarray(x[:, f0:f1]))
+        emb = torch.from_numpy(vec).to(model.dw.dev)
+        model.plan.run_full(st, emb.data_ptr())
+        outs.append(model.download(model.latent_to_bcthw(st, model.plan.eps)))
+    out = outs[0] if len(outs) == 1 else np.concatenate(outs, axis=1)
     t2 = time.perf_counter()
-    ledger = {"arena_bytes": model.plan.arena_bytes, "scratch_bytes": model.plan.scratch_bytes,
-              "torch_peak_bytes": torch.cuda.max_memory_allocated()}
-    timing = {"compile_ms": (t1 - t0) * 1e3, "run_ms": (t2 - t1) * 1e3}
+    model = models[chunks[0][1] - chunks[0][0]]
+    summary = {"mode": mode.value, "arena_bytes": model.plan.arena_bytes,
+               "scratch_bytes": model.plan.scratch_bytes, "torch_peak_bytes": torch.cuda.max_memory_allocated()}
+    ledger = model.plan.memory_ledger(model.plan.scratch_bytes, summary)
+    timing = {"compile_ms": compile_ms, "run_ms": (t2 - t0) * 1e3 - compile_ms}
     return Tensor5D(out), ledger, timing

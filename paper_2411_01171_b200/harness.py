@@ -14,6 +14,8 @@ the timed path.
 
 from __future__ import annotations
 
+import dataclasses
+import json
 import time
 from dataclasses import dataclass, field
 
@@ -21,9 +23,10 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import ScheduleMismatch
+from .errors import InvalidParam, ScheduleMismatch, SliceflowError
 from .executor import DeviceModel, ExecConfig
 from .graph import Graph
+from .grouping import estimate_peak_memory
 from .modes import ExecMode
 from .rehash import (SimilarityMap, StepSchedule, gamma_for_target, gram_partial, gram_similarity, key_step_search,
                      op_count_report, similarity_from_gram)
@@ -210,11 +213,12 @@ class DenoiseRunConfig:
     gamma: float | None = None
     target_keys: int | None = None
     exec_cfg: ExecConfig = field(default_factory=ExecConfig)
+    naive_chunk: int | None = None      # NaiveClip(chunk) frames per independent clip
 
 
 @dataclass
 class RunReport:
-    """SPEC.md:473-476 (device flavour)."""
+    """SPEC.md:473-476 (device flavour): measured device bytes next to the static model."""
 
     peak_bytes: int
     arena_bytes: int
@@ -224,17 +228,40 @@ class RunReport:
     op_counts: dict
     schedule: dict | None
     similarity_summary: dict | None
+    mode: str = ExecMode.SLICED_LOOP.value
+    static_model_bytes: int | None = None   # grouping.estimate_peak_memory in bf16 (reference model)
+    ledger_peak_bytes: int | None = None    # derived device ledger of one evaluation (ledger.py)
+    ticks: int | None = None                # ledger events of one evaluation
+
+    def to_json_dict(self) -> dict:
+        return {"mode": self.mode, "peak_bytes": self.peak_bytes, "ticks": self.ticks, "wall_ms": self.wall_ms,
+                "output_checksum": self.output_checksum, "arena_bytes": self.arena_bytes,
+                "scratch_bytes": self.scratch_bytes, "static_model_bytes": self.static_model_bytes,
+                "ledger_peak_bytes": self.ledger_peak_bytes, "op_counts": self.op_counts,
+                "schedule": self.schedule, "similarity_summary": self.similarity_summary}
+
+    def save(self, path) -> None:
+        with open(path, "w") as f:
+            json.dump(self.to_json_dict(), f, indent=1, sort_keys=True)
 
 
 def run_denoise(cfg: DenoiseRunConfig) -> tuple[Tensor5D, RunReport]:
-    """Full or rehash denoising run on the device."""
+    """Full or rehash denoising run on the device.
+
+    NAIVE_CLIP(``naive_chunk``): every clip of frames is denoised as its own
+    independent video (no carry-over) and the clips are stitched
+    along t -- the baseline whose divergence the slicer avoids.
+    """
     ucfg = cfg.unet
     K = cfg.steps or ucfg.steps
     ex = cfg.exec_cfg
-    if ExecMode(cfg.mode) is ExecMode.REFERENCE:
+    mode = ExecMode(cfg.mode)
+    if mode in (ExecMode.REFERENCE, ExecMode.NAIVE_CLIP):
         ex = ExecConfig(spatial_k=1, temporal_k=1, gemm_backend=ex.gemm_backend, device=ex.device)
-    den = Denoiser(ucfg, ex, K=K)
     x0 = initial_latent(ucfg)
+    if mode is ExecMode.NAIVE_CLIP:
+        return _run_naive_clip(cfg, ucfg, K, ex, x0)
+    den = Denoiser(ucfg, ex, K=K)
     torch.cuda.reset_peak_memory_stats()
     t0 = time.perf_counter()
     schedule, sim = cfg.schedule, None
@@ -246,15 +273,55 @@ def run_denoise(cfg: DenoiseRunConfig) -> tuple[Tensor5D, RunReport]:
     x = den.run(x0, schedule)
     wall = (time.perf_counter() - t0) * 1e3
     if not np.isfinite(x).all():
-        from .errors import SliceflowError
         raise SliceflowError("non-finite latent")
     sched = schedule or StepSchedule(list(range(K)), K)
+    led = den.plan.memory_ledger(den.plan.scratch_bytes)
+    static_mode = ExecMode.REFERENCE if mode is ExecMode.REFERENCE else ExecMode.SLICED_LOOP
     rep = RunReport(
         peak_bytes=int(torch.cuda.max_memory_allocated()),
         arena_bytes=den.plan.arena_bytes, scratch_bytes=den.plan.scratch_bytes, wall_ms=wall,
         output_checksum=float(np.sum(x, dtype=np.float64)),
         op_counts=op_count_report(den.graph, sched, den.tail_node_count()),
-        schedule=sched.to_json_dict(), similarity_summary=sim)
+        schedule=sched.to_json_dict(), similarity_summary=sim, mode=mode.value,
+        static_model_bytes=int(estimate_peak_memory(den.model.grouped if static_mode is ExecMode.SLICED_LOOP
+                                                    else den.graph, static_mode, "bfloat16")),
+        ledger_peak_bytes=led.peak_bytes, ticks=len(led.events))
+    return Tensor5D(x), rep
+
+
+def _run_naive_clip(cfg: DenoiseRunConfig, ucfg: UNetConfig, K: int, ex: ExecConfig, x0: np.ndarray):
+    if cfg.schedule is not None or cfg.gamma is not None or cfg.target_keys is not None:
+        raise InvalidParam("naiveclip runs every step (no Step Rehash schedule)")
+    from .executor import _with_frames, naive_clip_chunks
+    if cfg.naive_chunk is None:
+        raise InvalidParam("naiveclip needs naive_chunk")
+    chunks = naive_clip_chunks(ucfg.frames, cfg.naive_chunk)
+    graph, w64 = build_toy_unet(ucfg)
+    torch.cuda.reset_peak_memory_stats()
+    t0 = time.perf_counter()
+    dens: dict[int, Denoiser] = {}
+    outs = []
+    for f0, f1 in chunks:
+        n = f1 - f0
+        if n not in dens:
+            dens[n] = Denoiser(dataclasses.replace(ucfg, frames=n), ex, graph=_with_frames(graph, n),
+                               weights=w64, K=K)
+        outs.append(dens[n].run(np.ascontiguousarray(x0[:, f0:f1])))
+    x = np.concatenate(outs, axis=1)
+    wall = (time.perf_counter() - t0) * 1e3
+    if not np.isfinite(x).all():
+        raise SliceflowError("non-finite latent")
+    den = dens[chunks[0][1] - chunks[0][0]]
+    led = den.plan.memory_ledger(den.plan.scratch_bytes)
+    sched = StepSchedule(list(range(K)), K)
+    rep = RunReport(
+        peak_bytes=int(torch.cuda.max_memory_allocated()), arena_bytes=den.plan.arena_bytes,
+        scratch_bytes=den.plan.scratch_bytes, wall_ms=wall, output_checksum=float(np.sum(x, dtype=np.float64)),
+        op_counts={"chunks": len(chunks), **op_count_report(den.graph, sched, den.tail_node_count())},
+        schedule=sched.to_json_dict(), similarity_summary=None, mode=ExecMode.NAIVE_CLIP.value,
+        static_model_bytes=int(estimate_peak_memory(graph, ExecMode.NAIVE_CLIP, "bfloat16",
+                                                    naive_chunk=cfg.naive_chunk)),
+        ledger_peak_bytes=led.peak_bytes, ticks=len(led.events))
     return Tensor5D(x), rep
 
 

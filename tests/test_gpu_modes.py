@@ -1,0 +1,87 @@
+"""executor.execute in every ExecMode and the NaiveClip baseline on the device (-m gpu).
+
+SPEC.md:333-341: Reference, SlicedLoop and Pipelined agree (here: bf16
+tolerance 1e-2 against each other, Pipelined == SlicedLoop bit for bit since
+they issue the same launches); Pipelined ledger peak == SlicedLoop ledger
+peak; the unsliced Reference ledger peak is >= 40 % above the sliced one;
+NaiveClip(2) differs from Reference by max abs error > 1e-3 and equals the
+per-clip Reference runs stitched along t.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2411_01171_b200.build import build  # noqa: E402
+from paper_2411_01171_b200.executor import ExecConfig, _with_frames, execute  # noqa: E402
+from paper_2411_01171_b200.harness import DenoiseRunConfig, initial_latent, run_denoise  # noqa: E402
+from paper_2411_01171_b200.ledger import export_timeline  # noqa: E402
+from paper_2411_01171_b200.modes import ExecMode  # noqa: E402
+from paper_2411_01171_b200.tensor import Tensor5D  # noqa: E402
+from paper_2411_01171_b200.unet import UNetConfig, build_toy_unet, step_embedding_tensor  # noqa: E402
+
+build()
+
+C1 = UNetConfig(channels=4, frames=8, height=32, width=32, base_channels=8, norm_groups=4, steps=10)
+
+
+@pytest.fixture(scope="module")
+def c1_setup():
+    g, w = build_toy_unet(C1)
+    x = Tensor5D(initial_latent(C1))
+    return g, w, {"x": x, "step_emb": step_embedding_tensor(C1, 3)}
+
+
+def test_modes_agree_and_ledgers(c1_setup):
+    g, w, inp = c1_setup
+    outs, leds = {}, {}
+    # per-frame spatial slices and 16 pixel bands (the default picks the fewest slices that fit
+    # the scratch budget, i.e. none at toy size)
+    sliced = ExecConfig(spatial_k=C1.frames, temporal_k=16)
+    for mode in (ExecMode.REFERENCE, ExecMode.SLICED_LOOP, ExecMode.PIPELINED):
+        y, led, timing = execute(g, mode, inp, w, cfg=sliced)
+        outs[mode], leds[mode] = y.data, led
+        led.assert_closed()
+        assert led["arena_bytes"] > 0 and timing["run_ms"] > 0
+        assert np.isfinite(y.data).all()
+    ref = outs[ExecMode.REFERENCE]
+    scale = np.abs(ref).max()
+    assert np.abs(outs[ExecMode.SLICED_LOOP] - ref).max() / scale <= 1e-2
+    assert np.array_equal(outs[ExecMode.PIPELINED], outs[ExecMode.SLICED_LOOP])
+    assert leds[ExecMode.PIPELINED].peak_bytes == leds[ExecMode.SLICED_LOOP].peak_bytes
+    assert leds[ExecMode.REFERENCE].peak_bytes >= 1.4 * leds[ExecMode.SLICED_LOOP].peak_bytes
+    doc = export_timeline(leds[ExecMode.SLICED_LOOP])
+    assert doc.count(",1\n") == 1          # exactly one peak row flagged
+
+
+def test_naive_clip_diverges_and_stitches(c1_setup):
+    g, w, inp = c1_setup
+    ref, _, _ = execute(g, ExecMode.REFERENCE, inp, w)
+    nc, led, _ = execute(g, ExecMode.NAIVE_CLIP, inp, w, naive_chunk=2)
+    err = float(np.abs(nc.data - ref.data).max())
+    print("naiveclip(2) vs reference max abs", err)
+    assert err > 1e-3
+    # == independent reference runs over each 2-frame clip, stitched along t
+    parts = []
+    for f0 in range(0, C1.frames, 2):
+        gi = _with_frames(g, 2)
+        xi = Tensor5D(np.ascontiguousarray(inp["x"].data[:, f0:f0 + 2]))
+        ei = Tensor5D(np.ascontiguousarray(inp["step_emb"].data[:, f0:f0 + 2]))
+        parts.append(execute(gi, ExecMode.REFERENCE, {"x": xi, "step_emb": ei}, w)[0].data)
+    assert np.array_equal(nc.data, np.concatenate(parts, axis=1))
+    assert led["mode"] == "naiveclip"
+
+
+def test_run_denoise_naive_clip_report():
+    y, rep = run_denoise(DenoiseRunConfig(unet=C1, steps=3, mode=ExecMode.NAIVE_CLIP, naive_chunk=4))
+    assert np.isfinite(y.data).all() and y.data.shape[1] == C1.frames
+    d = rep.to_json_dict()
+    assert d["mode"] == "naiveclip" and d["static_model_bytes"] > 0 and d["ticks"] > 0
+    y2, rep2 = run_denoise(DenoiseRunConfig(unet=C1, steps=3))
+    assert rep2.mode == "slicedloop" and rep2.static_model_bytes > 0 and rep2.ledger_peak_bytes > 0
+    assert float(np.abs(y.data - y2.data).max()) > 1e-3
