@@ -35,7 +35,11 @@ struct Params {
   int n_inner, n_outer, T;   // PLAIN: o over n_outer (and z over batch); TCONV: o = b*T + t
   int bi, bo;                // rows of a tile = bo outer x bi inner (PLAIN/TCONV)
   int tiles_i, tiles_o, n_z; // PLAIN: tiles_o over n_outer, n_z = batch; TCONV: tiles_o over T, n_z = B
-  int H, W, w_t, h_t, tiles_x, tiles_y;  // CONV
+  int H, W, w_t, h_t, tiles_x, tiles_y;  // CONV (tiles_y = full h_t-row bands per frame)
+  // CONV tail tiles: when H % h_t = tail_rows divides h_t, the last tail_rows rows of
+  // tail_fb consecutive frames form one 128-row tile (M tiles >= n_main; maps *T)
+  int64_t n_main;
+  int tail_y0, tail_rows, tail_fb, n_frames;
   int64_t tiles_m;
   int tiles_n, N, BN;
   int taps, cblocks;         // K loop = taps x cblocks (64-channel blocks)
@@ -205,15 +209,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 struct MTile {
   int z, o0, i0;   // PLAIN/TCONV: batch/b, outer start (t0 or o0), inner start
   int f, y0, x0;   // CONV
+  int tail;        // CONV: a tail tile (rows tail_y0.. of tail_fb frames starting at f)
 };
 
 __device__ __forceinline__ MTile decode_m(const Params& p, int64_t tm) {
   MTile t{};
   if (p.mode == SF_GEMM_CONV3X3) {
-    t.x0 = (int)(tm % p.tiles_x) * p.w_t;
-    int64_t r = tm / p.tiles_x;
-    t.y0 = (int)(r % p.tiles_y) * p.h_t;
-    t.f = (int)(r / p.tiles_y);
+    if (p.tail_rows && tm >= p.n_main) {
+      const int64_t tt = tm - p.n_main;
+      t.x0 = (int)(tt % p.tiles_x) * p.w_t;
+      t.f = (int)(tt / p.tiles_x) * p.tail_fb;
+      t.y0 = p.tail_y0;
+      t.tail = 1;
+    } else {
+      t.x0 = (int)(tm % p.tiles_x) * p.w_t;
+      int64_t r = tm / p.tiles_x;
+      t.y0 = (int)(r % p.tiles_y) * p.h_t;
+      t.f = (int)(r / p.tiles_y);
+    }
   } else {
     t.i0 = (int)(tm % p.tiles_i) * p.bi;
     int64_t r = tm / p.tiles_i;
@@ -242,7 +255,8 @@ template <int BN, int STAGES, int EPI, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapR,
-                   const __grid_constant__ CUtensorMap mapO) {
+                   const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapAT,
+                   const __grid_constant__ CUtensorMap mapRT, const __grid_constant__ CUtensorMap mapOT) {
   using L = SmemLayout<BN, STAGES, EPI, PAIR>;
   constexpr bool TMA_EPI = EPI > 0;
   extern __shared__ uint8_t smem_raw[];
@@ -265,6 +279,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     prefetch_map(&mapA);
     prefetch_map(&mapB);
+    if (p.tail_rows) prefetch_map(&mapAT);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -277,6 +292,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (TMA_EPI) {
       prefetch_map(&mapO);
       if (has_res) prefetch_map(&mapR);
+      if (p.tail_rows) {
+        prefetch_map(&mapOT);
+        if (has_res) prefetch_map(&mapRT);
+      }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -330,7 +349,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
             const uint32_t fb = leader_addr(&full[stage]);
             if (p.mode == SF_GEMM_CONV3X3)
-              tma_load_4d_2sm(&mapA, fb, dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1, mt.f);
+              tma_load_4d_2sm(mt.tail ? &mapAT : &mapA, fb, dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1,
+                              mt.f);
             else if (p.mode == SF_GEMM_TCONV3)
               tma_load_4d_2sm(&mapA, fb, dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
             else
@@ -344,7 +364,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           mbar_expect_tx(&full[stage], L::STAGE_BYTES);
           if (p.mode == SF_GEMM_CONV3X3) {
-            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1, mt.f);
+            tma_load_4d(mt.tail ? &mapAT : &mapA, &full[stage], dA, cb * BK, mt.x0 + tap % 3 - 1,
+                        mt.y0 + tap / 3 - 1, mt.f);
           } else if (p.mode == SF_GEMM_TCONV3) {
             tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
           } else {
@@ -414,9 +435,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int64_t o, i;
       int z = 0;
       if (p.mode == SF_GEMM_CONV3X3) {
-        const int y = mt.y0 + row / p.w_t, x = mt.x0 + row % p.w_t;
-        valid = y < p.H && x < p.W;
-        o = mt.f;
+        // main tile: rows (y, x) of one frame; tail tile: (frame, y, x) over tail_fb frames
+        const int per = mt.tail ? p.tail_rows * p.w_t : BM;
+        const int fr = mt.f + row / per, rr = row % per;
+        const int y = mt.y0 + rr / p.w_t, x = mt.x0 + rr % p.w_t;
+        valid = y < p.H && x < p.W && fr < p.n_frames;
+        o = fr;
         i = (int64_t)y * p.W + x;
       } else {
         const int oo = mt.o0 + row / p.bi, ii = mt.i0 + row % p.bi;
@@ -444,7 +468,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (has_res) {
               mbar_expect_tx(&res_full[0], L::OUT_TILE);
               if (p.mode == SF_GEMM_CONV3X3)
-                tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
+                tma_load_4d(mt.tail ? &mapRT : &mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
               else
                 tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
             }
@@ -457,7 +481,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (tcount == 0) {
             mbar_expect_tx(&res_full[0], L::OUT_TILE);
             if (p.mode == SF_GEMM_CONV3X3)
-              tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
+              tma_load_4d(mt.tail ? &mapRT : &mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
             else
               tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
           }
@@ -469,7 +493,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint8_t* nbuf = sOut + (ob ^ 1) * L::OUT_TILE;
             mbar_expect_tx(&res_full[ob ^ 1], L::OUT_TILE);
             if (p.mode == SF_GEMM_CONV3X3)
-              tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.x0, nm.y0, nm.f);
+              tma_load_4d(nm.tail ? &mapRT : &mapR, &res_full[ob ^ 1], nbuf, nn0, nm.x0, nm.y0, nm.f);
             else
               tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.i0, nm.o0, nm.z);
           }
@@ -523,7 +547,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (store_leader) {
           if (p.mode == SF_GEMM_CONV3X3)
-            tma_store_4d(&mapO, sbuf, n0, mt.x0, mt.y0, mt.f);
+            tma_store_4d(mt.tail ? &mapOT : &mapO, sbuf, n0, mt.x0, mt.y0, mt.f);
           else
             tma_store_4d(&mapO, sbuf, n0, mt.i0, mt.o0, mt.z);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -713,6 +737,11 @@ static bool choose_tiling(int N, int64_t tiles_m, bool pair_ok, int* bn) {
   return best_pair;
 }
 
+// every tensor map a launch needs (the *T maps: conv tail tiles, see Params)
+struct Maps {
+  CUtensorMap a, b, r, o, at, rt, ot;
+};
+
 }  // namespace tc
 
 bool gemm_tc_supported(const sf_gemm_args& a) {
@@ -730,8 +759,7 @@ bool gemm_tc_supported(const sf_gemm_args& a) {
 }
 
 template <int BN, int STAGES, int EPI, bool PAIR = false>
-static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mr,
-                            const CUtensorMap& mo, cudaStream_t st) {
+static sf_status launch_cfg(const tc::Params& p, const tc::Maps& m, cudaStream_t st) {
   constexpr int smem = tc::SmemLayout<BN, STAGES, EPI, PAIR>::TOTAL;
   static_assert(smem <= 232448, "shared memory budget");
   static bool init = false;
@@ -743,7 +771,7 @@ static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CU
   if (!PAIR) {
     int64_t tiles = p.tiles_m * p.tiles_n;
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    kern<<<grid, tc::NUM_THREADS, smem, st>>>(p, ma, mb, mr, mo);
+    kern<<<grid, tc::NUM_THREADS, smem, st>>>(p, m.a, m.b, m.r, m.o, m.at, m.rt, m.ot);
     return launch_status("sf_gemm(tcgen05)");
   }
   const int64_t pair_tiles = (p.tiles_m + 1) / 2 * p.tiles_n;
@@ -760,19 +788,20 @@ static sf_status launch_cfg(const tc::Params& p, const CUtensorMap& ma, const CU
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, p, ma, mb, mr, mo);
+  cudaLaunchKernelEx(&cfg, kern, p, m.a, m.b, m.r, m.o, m.at, m.rt, m.ot);
   return launch_status("sf_gemm(tcgen05 pair)");
 }
 
 // Output / residual maps share the M tiling of A: box {BN cols, tile rows}.
 static bool encode_rows_map(CUtensorMap* m, const sf_gemm_args& a, const tc::Params& p, const sf_view_t& v,
-                            int64_t bstride, int BN) {
+                            int64_t bstride, int BN, bool tail = false) {
   const uint64_t es = 2, ld = (uint64_t)v.ld;
   if (a.mode == SF_GEMM_CONV3X3) {
     uint64_t dims[4] = {(uint64_t)a.N, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.n_outer};
     uint64_t str[3] = {ld * es, (uint64_t)a.W * ld * es,
                        (uint64_t)(v.ostride ? v.ostride : (int64_t)a.H * a.W) * ld * es};
-    uint32_t box[4] = {(uint32_t)BN, (uint32_t)p.w_t, (uint32_t)p.h_t, 1};
+    uint32_t box[4] = {(uint32_t)BN, (uint32_t)p.w_t, (uint32_t)(tail ? p.tail_rows : p.h_t),
+                       (uint32_t)(tail ? p.tail_fb : 1)};
     return tc::encode(m, v.ptr, 4, dims, str, box, false);
   }
   uint64_t dims[4], str[3];
@@ -812,7 +841,7 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   p.out = a.out;
   p.out_bstride = a.out_bstride;
   p.out_fp32 = a.out_fp32;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mat;
   const uint64_t es = 2;
   // CTA pairs (cta_group::2, M = 256) whenever there are two M-tiles to pair up;
   // SF_GEMM_PAIR=0 forces single-CTA tiles (A/B runs)
@@ -832,6 +861,24 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
     uint32_t box[4] = {BK, (uint32_t)p.w_t, (uint32_t)p.h_t, 1};
     if (a.n_outer == 1) str[2] = (uint64_t)a.H * a.W * ld * es;
     SF_CHECK_ARG(encode(&ma, a.a.ptr, 4, dims, str, box), SF_ERR_CUDA, "tensor map A (conv)");
+    // tail tiles: the H % h_t leftover rows of h_t / rem consecutive frames as one tile
+    // (e.g. 9x16 frames: 8-row tiles + the 9th row of 8 frames instead of 25 near-empty tiles)
+    p.n_frames = a.n_outer;
+    p.n_main = p.tiles_m;
+    const int rem = a.H % p.h_t;
+    static const char* tail_env = getenv("SF_GEMM_TAIL");
+    if (rem && p.h_t % rem == 0 && !(tail_env && tail_env[0] == '0')) {
+      const int fb = p.h_t / rem;
+      uint32_t tbox[4] = {BK, (uint32_t)p.w_t, (uint32_t)rem, (uint32_t)fb};
+      if (encode(&mat, a.a.ptr, 4, dims, str, tbox)) {
+        p.tail_rows = rem;
+        p.tail_fb = fb;
+        p.tiles_y = a.H / p.h_t;
+        p.tail_y0 = p.tiles_y * p.h_t;
+        p.n_main = (int64_t)p.tiles_x * p.tiles_y * a.n_outer;
+        p.tiles_m = p.n_main + (int64_t)p.tiles_x * ((a.n_outer + fb - 1) / fb);
+      }
+    }
   } else {
     int n_inner = a.n_inner, n_outer = a.n_outer;
     int64_t ostride = a.a.ostride;
@@ -891,56 +938,69 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
     SF_CHECK_ARG(encode(&mb, a.w, 3, dims, str, box), SF_ERR_CUDA, "tensor map B");
   }
   CUtensorMap mr = mb, mo = mb;
+  tc::Maps M;
+  M.a = ma;
+  M.b = mb;
+  M.at = p.tail_rows ? mat : ma;
+  M.r = M.o = M.rt = M.ot = mb;
   if (!a.out_fp32) {
     SF_CHECK_ARG(encode_rows_map(&mo, a, p, a.out, a.out_bstride, BN), SF_ERR_CUDA, "tensor map out");
     if (a.res.ptr) SF_CHECK_ARG(encode_rows_map(&mr, a, p, a.res, a.res_bstride, BN), SF_ERR_CUDA, "tensor map res");
+    M.o = M.ot = mo;
+    M.r = M.rt = mr;
+    if (p.tail_rows) {
+      SF_CHECK_ARG(encode_rows_map(&M.ot, a, p, a.out, a.out_bstride, BN, true), SF_ERR_CUDA, "tensor map out tail");
+      if (a.res.ptr)
+        SF_CHECK_ARG(encode_rows_map(&M.rt, a, p, a.res, a.res_bstride, BN, true), SF_ERR_CUDA,
+                     "tensor map res tail");
+    }
     // long K: deep operand ring + one staging buffer; short K: double staging so the
     // epilogue (residual prefetch + TMA store) overlaps the next tile
     const bool long_k = p.taps * p.cblocks >= 32;
     if (pair) {
       if (long_k) {
         switch (BN) {
-          case 256: return launch_cfg<256, 5, 1, true>(p, ma, mb, mr, mo, st);
-          case 160: return launch_cfg<160, 7, 1, true>(p, ma, mb, mr, mo, st);
-          case 128: return launch_cfg<128, 8, 1, true>(p, ma, mb, mr, mo, st);
-          default: return launch_cfg<64, 10, 1, true>(p, ma, mb, mr, mo, st);
+          case 256: return launch_cfg<256, 5, 1, true>(p, M, st);
+          case 160: return launch_cfg<160, 7, 1, true>(p, M, st);
+          case 128: return launch_cfg<128, 8, 1, true>(p, M, st);
+          default: return launch_cfg<64, 10, 1, true>(p, M, st);
         }
       }
       switch (BN) {
-        case 256: return launch_cfg<256, 3, 2, true>(p, ma, mb, mr, mo, st);
-        case 160: return launch_cfg<160, 5, 2, true>(p, ma, mb, mr, mo, st);
-        case 128: return launch_cfg<128, 6, 2, true>(p, ma, mb, mr, mo, st);
-        default: return launch_cfg<64, 9, 2, true>(p, ma, mb, mr, mo, st);
+        case 256: return launch_cfg<256, 3, 2, true>(p, M, st);
+        case 160: return launch_cfg<160, 5, 2, true>(p, M, st);
+        case 128: return launch_cfg<128, 6, 2, true>(p, M, st);
+        default: return launch_cfg<64, 9, 2, true>(p, M, st);
       }
     }
     if (long_k) {
       switch (BN) {
-        case 256: return launch_cfg<256, 3, 1>(p, ma, mb, mr, mo, st);
-        case 160: return launch_cfg<160, 5, 1>(p, ma, mb, mr, mo, st);
-        case 128: return launch_cfg<128, 6, 1>(p, ma, mb, mr, mo, st);
-        default: return launch_cfg<64, 8, 1>(p, ma, mb, mr, mo, st);
+        case 256: return launch_cfg<256, 3, 1>(p, M, st);
+        case 160: return launch_cfg<160, 5, 1>(p, M, st);
+        case 128: return launch_cfg<128, 6, 1>(p, M, st);
+        default: return launch_cfg<64, 8, 1>(p, M, st);
       }
     }
     switch (BN) {
-      case 256: return launch_cfg<256, 2, 2>(p, ma, mb, mr, mo, st);
-      case 160: return launch_cfg<160, 4, 2>(p, ma, mb, mr, mo, st);
-      case 128: return launch_cfg<128, 5, 2>(p, ma, mb, mr, mo, st);
-      default: return launch_cfg<64, 7, 2>(p, ma, mb, mr, mo, st);
+      case 256: return launch_cfg<256, 2, 2>(p, M, st);
+      case 160: return launch_cfg<160, 4, 2>(p, M, st);
+      case 128: return launch_cfg<128, 5, 2>(p, M, st);
+      default: return launch_cfg<64, 7, 2>(p, M, st);
     }
   }
   if (pair) {
     switch (BN) {
-      case 256: return launch_cfg<256, 6, 0, true>(p, ma, mb, mr, mo, st);
-      case 160: return launch_cfg<160, 8, 0, true>(p, ma, mb, mr, mo, st);
-      case 128: return launch_cfg<128, 8, 0, true>(p, ma, mb, mr, mo, st);
-      default: return launch_cfg<64, 10, 0, true>(p, ma, mb, mr, mo, st);
+      case 256: return launch_cfg<256, 6, 0, true>(p, M, st);
+      case 160: return launch_cfg<160, 8, 0, true>(p, M, st);
+      case 128: return launch_cfg<128, 8, 0, true>(p, M, st);
+      default: return launch_cfg<64, 10, 0, true>(p, M, st);
     }
   }
   switch (BN) {
-    case 256: return launch_cfg<256, 4, 0>(p, ma, mb, mr, mo, st);
-    case 160: return launch_cfg<160, 5, 0>(p, ma, mb, mr, mo, st);
-    case 128: return launch_cfg<128, 6, 0>(p, ma, mb, mr, mo, st);
-    default: return launch_cfg<64, 8, 0>(p, ma, mb, mr, mo, st);
+    case 256: return launch_cfg<256, 4, 0>(p, M, st);
+    case 160: return launch_cfg<160, 5, 0>(p, M, st);
+    case 128: return launch_cfg<128, 6, 0>(p, M, st);
+    default: return launch_cfg<64, 8, 0>(p, M, st);
   }
 }
 

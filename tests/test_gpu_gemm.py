@@ -68,6 +68,35 @@ def test_conv3x3(backend, F_, H, W, C, Co):
     assert rel(out, ref) <= 1e-2
 
 
+@pytest.mark.parametrize("F_,H,W,C,Co", [(25, 9, 16, 128, 256), (5, 18, 32, 64, 128), (10, 9, 16, 64, 64),
+                                         (3, 9, 16, 64, 128), (7, 4, 16, 64, 64)])
+def test_conv3x3_tail_tiles(F_, H, W, C, Co):
+    """Frames whose height is not a multiple of the tile height: the leftover rows of several frames
+    share one tile (tcgen05 path), with residual + per-frame bias in the epilogue."""
+    torch.manual_seed(6)
+    x = rnd(F_, H, W, C)
+    w = rnd(Co, C, 3, 3, scale=(9 * C) ** -0.5)
+    wk = w.permute(0, 2, 3, 1).reshape(Co, 9 * C).contiguous()
+    bias = torch.randn(Co, device=dev)
+    emb = torch.randn(F_, Co, device=dev)
+    res = rnd(F_ * H * W, Co)
+    out = torch.empty(F_ * H * W, Co, dtype=torch.bfloat16, device=dev)
+    args = D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_CONV3X3, n_outer=F_, n_inner=H * W, H=H,
+                  W=W, cin=C, n=Co, a=Rows(x.view(-1, C), 0, H * W), w=wk, out=Rows(out, 0, H * W), bias=bias,
+                  rowbias=emb, rowbias_stride=Co, res=Rows(res, 0, H * W), backend=2)
+    assert N.query("sf_gemm_backend", args) == 2
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float(), bias, padding=1) + emb[:, :, None, None]
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Co) + res.float()
+    assert rel(out, ref) <= 1e-2
+    # fp32 direct-store epilogue over the same tiling
+    out32 = torch.empty(F_ * H * W, Co, dtype=torch.float32, device=dev)
+    D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_CONV3X3, n_outer=F_, n_inner=H * W, H=H, W=W,
+           cin=C, n=Co, a=Rows(x.view(-1, C), 0, H * W), w=wk, out=Rows(out32, 0, H * W), out_fp32=True,
+           bias=bias, backend=2)
+    ref32 = F.conv2d(x.float().permute(0, 3, 1, 2), w.float(), bias, padding=1).permute(0, 2, 3, 1)
+    assert rel(out32, ref32.reshape(-1, Co)) <= 1e-2
+
+
 @pytest.mark.parametrize("backend", [1, 2])
 @pytest.mark.parametrize("F_,H,W,C,Co", [(3, 72, 128, 320, 4), (2, 9, 13, 64, 8), (1, 5, 7, 128, 3)])
 def test_conv3x3_tapwise(backend, F_, H, W, C, Co):
