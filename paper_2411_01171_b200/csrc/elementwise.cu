@@ -523,6 +523,30 @@ __device__ __forceinline__ void tq_load(bf16 (*dst)[TQ_LD], const sf_view_t& v, 
   }
 }
 
+// register-staged variant: issue a chunk's loads early (tq_fetch), store them to smem later (tq_put),
+// so the next chunk is in flight while the current one is in the MMAs
+struct TqChunk {
+  bf16x8 v[8];
+};
+__device__ __forceinline__ void tq_fetch(TqChunk& r, const sf_view_t& v, int b, int T, int pix, int col0, int cvalid,
+                                         int lane) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int idx = lane + 32 * k, t = idx >> 3, c = (idx & 7) * 8;
+    if (t < T && c < cvalid)
+      r.v[k] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(v, (int64_t)b * T + t, pix) + col0 + c);
+    else
+      r.v[k].u = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+__device__ __forceinline__ void tq_put(bf16 (*dst)[TQ_LD], const TqChunk& r, int lane) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int idx = lane + 32 * k;
+    *reinterpret_cast<bf16x8*>(&dst[idx >> 3][(idx & 7) * 8]) = r.v[k];
+  }
+}
+
 __global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
                                                                           sf_view_t out, int B, int T, int n_inner,
                                                                           int C, float scale_log2) {
@@ -541,11 +565,18 @@ __global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_vie
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) sacc[i][j][e] = 0.f;
+  TqChunk rq, rk;
+  tq_fetch(rq, qkv, b, T, pix, 0, min(TQ_CH, C), lane);
+  tq_fetch(rk, qkv, b, T, pix, koff, min(TQ_CH, C), lane);
   for (int c0 = 0; c0 < C; c0 += TQ_CH) {
-    const int cv = min(TQ_CH, C - c0);
-    tq_load(qs, qkv, b, T, pix, c0, cv, lane);
-    tq_load(ks, qkv, b, T, pix, koff + c0, cv, lane);
+    tq_put(qs, rq, lane);
+    tq_put(ks, rk, lane);
     __syncwarp();
+    if (c0 + TQ_CH < C) {
+      const int nv = min(TQ_CH, C - c0 - TQ_CH);
+      tq_fetch(rq, qkv, b, T, pix, c0 + TQ_CH, nv, lane);
+      tq_fetch(rk, qkv, b, T, pix, koff + c0 + TQ_CH, nv, lane);
+    }
 #pragma unroll
     for (int kk = 0; kk < TQ_CH; kk += 16) {
       unsigned a[2][4];
@@ -608,10 +639,13 @@ __global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_vie
       pa[mi][kk][2] = pack_bf2(sacc[mi][2 * kk + 1][0], sacc[mi][2 * kk + 1][1]);
       pa[mi][kk][3] = pack_bf2(sacc[mi][2 * kk + 1][2], sacc[mi][2 * kk + 1][3]);
     }
+  TqChunk rv;
+  tq_fetch(rv, qkv, b, T, pix, voff, min(TQ_CH, C), lane);
   for (int c0 = 0; c0 < C; c0 += TQ_CH) {
     const int cv = min(TQ_CH, C - c0);
-    tq_load(vs, qkv, b, T, pix, voff + c0, cv, lane);
+    tq_put(vs, rv, lane);
     __syncwarp();
+    if (c0 + TQ_CH < C) tq_fetch(rv, qkv, b, T, pix, voff + c0 + TQ_CH, min(TQ_CH, C - c0 - TQ_CH), lane);
     float oacc[2][8][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -633,22 +667,26 @@ __global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_vie
         }
       }
     }
-    __syncwarp();
+    // O chunk -> smem (the q tile is free) -> 16-byte row stores
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int t = mi * 16 + (lane >> 2) + h * 8;
-        if (t >= T) continue;
-        bf16* dst = row_ptr<bf16>(out, (int64_t)b * T + t, pix) + c0;
 #pragma unroll
-        for (int nj = 0; nj < 8; ++nj) {
-          const int c = nj * 8 + colq;
-          if (c < cv)
-            *reinterpret_cast<bf162*>(dst + c) =
-                __floats2bfloat162_rn(oacc[mi][nj][h * 2] * rsum[mi][h], oacc[mi][nj][h * 2 + 1] * rsum[mi][h]);
-        }
+        for (int nj = 0; nj < 8; ++nj)
+          *reinterpret_cast<unsigned*>(&qs[t][nj * 8 + colq]) =
+              pack_bf2(oacc[mi][nj][h * 2] * rsum[mi][h], oacc[mi][nj][h * 2 + 1] * rsum[mi][h]);
       }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = lane + 32 * k, t = idx >> 3, c = (idx & 7) * 8;
+      if (t < T && c < cv)
+        *reinterpret_cast<bf16x8*>(row_ptr<bf16>(out, (int64_t)b * T + t, pix) + c0 + c) =
+            *reinterpret_cast<const bf16x8*>(&qs[t][c]);
+    }
+    __syncwarp();
   }
 }
 
