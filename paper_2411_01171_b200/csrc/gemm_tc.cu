@@ -892,8 +892,22 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
       p.collapsed = 1;
     }
     p.n_inner = n_inner;
-    p.bi = n_inner >= BM ? BM : pow2_floor(n_inner);
-    p.bo = BM / p.bi;
+    // rows of a tile = bo outer x bi inner: the power-of-two split with the fewest padded
+    // rows (ties -> wider bi), e.g. 144 pixels x 25 frames: 32 x 4 (80 % useful) instead
+    // of 128 x 1 (56 %)
+    {
+      const int64_t outer = a.mode == SF_GEMM_TCONV3 ? a.T : n_outer;
+      int64_t best = -1;
+      for (int bi = BM; bi >= 8; bi >>= 1) {
+        const int bo = BM / bi;
+        const int64_t padded = (int64_t)((n_inner + bi - 1) / bi) * bi * ((outer + bo - 1) / bo) * bo;
+        if (best < 0 || padded < best) {
+          best = padded;
+          p.bi = bi;
+        }
+      }
+      p.bo = BM / p.bi;
+    }
     p.tiles_i = (n_inner + p.bi - 1) / p.bi;
     uint64_t dims[4], str[3];
     dims[0] = (uint64_t)a.cin * p.taps / p.taps;  // channels of one tap
