@@ -26,6 +26,7 @@ namespace sf {
 namespace tc {
 
 constexpr int BM = 128, BK = 64;
+constexpr int F32_CHUNK_BYTES = 128 * 32 * 4;   // EPI 3: one 32-column fp32 chunk of a tile
 constexpr int NUM_THREADS = 192;
 constexpr int EPI_W0 = 2;  // first epilogue warp
 
@@ -243,7 +244,8 @@ struct SmemLayout {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // epilogue staging tile [128 rows][BN] bf16 (residual in, output out), row-major
   static constexpr int OUT_TILE = BM * BN * 2;
-  static constexpr int OUT_BYTES = EPI * OUT_TILE;   // EPI staging buffers (0 = direct stores)
+  // EPI staging buffers: 0 = direct stores; 1/2 = bf16 tiles; 3 = two 128 x 32 fp32 chunks (SW128)
+  static constexpr int OUT_BYTES = EPI == 3 ? 2 * F32_CHUNK_BYTES : EPI * OUT_TILE;
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + OUT_BYTES + 256 /*barriers*/;
 };
 
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapAT,
                    const __grid_constant__ CUtensorMap mapRT, const __grid_constant__ CUtensorMap mapOT) {
   using L = SmemLayout<BN, STAGES, EPI, PAIR>;
-  constexpr bool TMA_EPI = EPI > 0;
+  constexpr bool TMA_EPI = EPI == 1 || EPI == 2;   // bf16 staging + TMA store (EPI 3: fp32 chunks)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tempty[s], PAIR ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
     }
     for (int b = 0; b < 2; ++b) mbar_init(&res_full[b], 1);
-    if (TMA_EPI) {
+    if (TMA_EPI || EPI == 3) {
       prefetch_map(&mapO);
       if (has_res) prefetch_map(&mapR);
       if (p.tail_rows) {
@@ -456,6 +458,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       valid = valid && !phantom;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (EPI == 3) {
+        // fp32 output through two 16 KB staging chunks (128 rows x 32 cols, 128-byte swizzle:
+        // a thread's row lands in a different bank group than its 7 neighbours), one TMA
+        // store per chunk; a chunk buffer is refilled once its store from two chunks ago is read
+        const bool store_leader = warp == EPI_W0 && lane == 0;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          const int nb = n0 + c;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+          if (p.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(p.bias + nb + j) : 0.f;
+          }
+          if (p.rowbias) {
+            const float* rb = p.rowbias + o * p.rowbias_stride + nb;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(rb + j) : 0.f;
+          }
+          if (p.act == SF_ACT_SILU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+          }
+          uint8_t* buf = sOut + ((c >> 5) & 1) * F32_CHUNK_BYTES;
+          if (store_leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          uint8_t* srow = buf + row * 128;
+          const int sw = row & 7;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<float4*>(srow + ((u ^ sw) << 4)) =
+                make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (store_leader && nb < p.N) {
+            if (p.mode == SF_GEMM_CONV3X3)
+              tma_store_4d(mt.tail ? &mapOT : &mapO, buf, nb, mt.x0, mt.y0, mt.f);
+            else
+              tma_store_4d(&mapO, buf, nb, mt.i0, mt.o0, mt.z);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR) arrive_remote(tempty_l + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       if constexpr (TMA_EPI) {
         const bool store_leader = warp == EPI_W0 && lane == 0;
         const int ob = EPI == 2 ? (int)(tcount & 1) : 0;
@@ -668,7 +728,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 static bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                   const uint32_t* box, bool swizzle = true) {
+                   const uint32_t* box, bool swizzle = true, bool fp32 = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], s[4];
@@ -679,7 +739,8 @@ static bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* d
     e[i] = 1;
   }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b, e,
+  CUresult r = fn(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                  const_cast<void*>(base), d, s, b, e,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -794,15 +855,16 @@ static sf_status launch_cfg(const tc::Params& p, const tc::Maps& m, cudaStream_t
 
 // Output / residual maps share the M tiling of A: box {BN cols, tile rows}.
 static bool encode_rows_map(CUtensorMap* m, const sf_gemm_args& a, const tc::Params& p, const sf_view_t& v,
-                            int64_t bstride, int BN, bool tail = false) {
-  const uint64_t es = 2, ld = (uint64_t)v.ld;
+                            int64_t bstride, int BN, bool tail = false, bool fp32 = false) {
+  // fp32 (EPI 3): 32-column boxes in the 128-byte swizzle; bf16: one BN-wide unswizzled box
+  const uint64_t es = fp32 ? 4 : 2, ld = (uint64_t)v.ld;
+  const uint32_t bw = fp32 ? 32u : (uint32_t)BN;
   if (a.mode == SF_GEMM_CONV3X3) {
     uint64_t dims[4] = {(uint64_t)a.N, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.n_outer};
     uint64_t str[3] = {ld * es, (uint64_t)a.W * ld * es,
                        (uint64_t)(v.ostride ? v.ostride : (int64_t)a.H * a.W) * ld * es};
-    uint32_t box[4] = {(uint32_t)BN, (uint32_t)p.w_t, (uint32_t)(tail ? p.tail_rows : p.h_t),
-                       (uint32_t)(tail ? p.tail_fb : 1)};
-    return tc::encode(m, v.ptr, 4, dims, str, box, false);
+    uint32_t box[4] = {bw, (uint32_t)p.w_t, (uint32_t)(tail ? p.tail_rows : p.h_t), (uint32_t)(tail ? p.tail_fb : 1)};
+    return tc::encode(m, v.ptr, 4, dims, str, box, fp32, fp32);
   }
   uint64_t dims[4], str[3];
   dims[0] = (uint64_t)a.N;
@@ -819,8 +881,8 @@ static bool encode_rows_map(CUtensorMap* m, const sf_gemm_args& a, const tc::Par
     dims[3] = (uint64_t)p.n_z;
     str[2] = p.n_z > 1 ? (uint64_t)bstride * es : (uint64_t)p.n_outer * str[1];
   }
-  uint32_t box[4] = {(uint32_t)BN, (uint32_t)p.bi, (uint32_t)p.bo, 1};
-  return tc::encode(m, v.ptr, 4, dims, str, box, false);
+  uint32_t box[4] = {bw, (uint32_t)p.bi, (uint32_t)p.bo, 1};
+  return tc::encode(m, v.ptr, 4, dims, str, box, fp32, fp32);
 }
 
 sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
@@ -1000,6 +1062,27 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
       case 160: return launch_cfg<160, 4, 2>(p, M, st);
       case 128: return launch_cfg<128, 5, 2>(p, M, st);
       default: return launch_cfg<64, 7, 2>(p, M, st);
+    }
+  }
+  // fp32 output: TMA-store epilogue (EPI 3) when rows / strides are 16-byte aligned and there
+  // is no residual; otherwise direct stores (EPI 0)
+  const bool f32_tma = !a.res.ptr && aligned16(a.out.ptr) && a.out.ld % 4 == 0 && (a.out.ostride * a.out.ld * 4) % 16 == 0 &&
+                       (a.out_bstride * 4) % 16 == 0 && encode_rows_map(&M.o, a, p, a.out, a.out_bstride, BN, false, true) &&
+                       (!p.tail_rows || encode_rows_map(&M.ot, a, p, a.out, a.out_bstride, BN, true, true));
+  if (f32_tma) {
+    if (pair) {
+      switch (BN) {
+        case 256: return launch_cfg<256, 6, 3, true>(p, M, st);
+        case 160: return launch_cfg<160, 7, 3, true>(p, M, st);
+        case 128: return launch_cfg<128, 8, 3, true>(p, M, st);
+        default: return launch_cfg<64, 9, 3, true>(p, M, st);
+      }
+    }
+    switch (BN) {
+      case 256: return launch_cfg<256, 4, 3>(p, M, st);
+      case 160: return launch_cfg<160, 5, 3>(p, M, st);
+      case 128: return launch_cfg<128, 6, 3>(p, M, st);
+      default: return launch_cfg<64, 8, 3>(p, M, st);
     }
   }
   if (pair) {
