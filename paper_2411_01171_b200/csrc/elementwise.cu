@@ -134,62 +134,68 @@ __global__ void gn_finalize_kernel(const double2* partial, int frames, int split
   }
 }
 
-// y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]).  One block
-// covers a chunk of one frame's rows; each thread owns one 8-channel vector
-// (its mean / scale / shift live in registers) and walks rows with four
-// 16-byte loads in flight -- no per-element index arithmetic.
-__global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y, int n_inner, int C, int groups,
-                                                       int chunks, const float* __restrict__ mean,
+// y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]).  Persistent: each
+// block takes an equal contiguous share of all frames*n_inner rows (no tail wave);
+// each thread owns one 8-channel vector (mean / scale / shift in registers, reloaded
+// when its rows cross into the next frame) and walks rows with 8 loads in flight.
+__global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y, int frames, int n_inner, int C,
+                                                       int groups, const float* __restrict__ mean,
                                                        const float* __restrict__ rstd,
                                                        const float* __restrict__ gamma,
                                                        const float* __restrict__ beta, int act) {
-  const int frame = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
   const int cg = C / groups, nvec = C / 8;
   const int rpi = nvec <= (int)blockDim.x ? (int)blockDim.x / nvec : 1;   // rows per iteration
-  const int per = (n_inner + chunks - 1) / chunks;
-  const int r0 = chunk * per, r1 = min(n_inner, r0 + per);
+  const int64_t total = (int64_t)frames * n_inner;
+  const int64_t r0 = total * blockIdx.x / gridDim.x, r1 = total * (blockIdx.x + 1) / gridDim.x;
   for (int v = nvec <= (int)blockDim.x ? (int)threadIdx.x % nvec : (int)threadIdx.x; v < nvec;
        v += nvec <= (int)blockDim.x ? nvec : (int)blockDim.x) {
     const int lr = nvec <= (int)blockDim.x ? (int)threadIdx.x / nvec : 0;
     if (lr >= rpi) return;
-    float mm[8], ss[8], bb[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = v * 8 + j, g = c / cg;
-      mm[j] = __ldg(mean + frame * groups + g);
-      ss[j] = __ldg(rstd + frame * groups + g) * __ldg(gamma + c);
-      bb[j] = __ldg(beta + c);
-    }
-    const bf16* src = row_ptr<const bf16>(x, frame, 0) + v * 8;
-    bf16* dst = row_ptr<bf16>(y, frame, 0) + v * 8;
-    const int64_t xld = x.ld, yld = y.ld;
-    constexpr int U = 8;
-    int r = r0 + lr;
-    for (; r + (U - 1) * rpi < r1; r += U * rpi) {
-      bf16x8 in[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) in[u] = *reinterpret_cast<const bf16x8*>(src + (int64_t)(r + u * rpi) * xld);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        float f[8];
-        unpack8(in[u], f);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float t = (f[j] - mm[j]) * ss[j] + bb[j];
-          f[j] = act ? silu_f(t) : t;
-        }
-        *reinterpret_cast<bf16x8*>(dst + (int64_t)(r + u * rpi) * yld) = pack8(f);
-      }
-    }
-    for (; r < r1; r += rpi) {
-      float f[8];
-      unpack8(*reinterpret_cast<const bf16x8*>(src + (int64_t)r * xld), f);
+    // split this block's rows at frame boundaries: per segment one frame's tables
+    for (int64_t seg = r0; seg < r1;) {
+      const int f = (int)(seg / n_inner);
+      const int64_t seg_end = min(r1, (int64_t)(f + 1) * n_inner);
+      const int i0 = (int)(seg - (int64_t)f * n_inner), i1 = (int)(seg_end - (int64_t)f * n_inner);
+      seg = seg_end;
+      float mm[8], ss[8], bb[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float t = (f[j] - mm[j]) * ss[j] + bb[j];
-        f[j] = act ? silu_f(t) : t;
+        const int c = v * 8 + j, g = c / cg;
+        mm[j] = __ldg(mean + f * groups + g);
+        ss[j] = __ldg(rstd + f * groups + g) * __ldg(gamma + c);
+        bb[j] = __ldg(beta + c);
       }
-      *reinterpret_cast<bf16x8*>(dst + (int64_t)r * yld) = pack8(f);
+      const bf16* src = row_ptr<const bf16>(x, f, 0) + v * 8;
+      bf16* dst = row_ptr<bf16>(y, f, 0) + v * 8;
+      const int64_t xld = x.ld, yld = y.ld;
+      constexpr int U = 8;
+      int i = i0 + lr;
+      for (; i + (U - 1) * rpi < i1; i += U * rpi) {
+        bf16x8 in[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) in[u] = *reinterpret_cast<const bf16x8*>(src + (int64_t)(i + u * rpi) * xld);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float fv[8];
+          unpack8(in[u], fv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float t = (fv[j] - mm[j]) * ss[j] + bb[j];
+            fv[j] = act ? silu_f(t) : t;
+          }
+          *reinterpret_cast<bf16x8*>(dst + (int64_t)(i + u * rpi) * yld) = pack8(fv);
+        }
+      }
+      for (; i < i1; i += rpi) {
+        float fv[8];
+        unpack8(*reinterpret_cast<const bf16x8*>(src + (int64_t)i * xld), fv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float t = (fv[j] - mm[j]) * ss[j] + bb[j];
+          fv[j] = act ? silu_f(t) : t;
+        }
+        *reinterpret_cast<bf16x8*>(dst + (int64_t)i * yld) = pack8(fv);
+      }
     }
   }
 }
@@ -1080,13 +1086,19 @@ sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t 
   SF_CHECK_ARG(aligned16(gamma) && aligned16(beta), SF_ERR_PARAM, "gamma/beta must be 16-byte aligned");
   const int nvec = C / 8;
   const int threads = nvec <= 256 ? (256 / nvec) * nvec : 256;
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_apply_kernel, 256, 0);
+    if (occ < 1) occ = 1;
+  }
+  // persistent: every resident block gets an equal share (>= ~32 rows per thread)
+  const int64_t rows = (int64_t)frames * n_inner;
   const int rpi = nvec <= 256 ? 256 / nvec : 1;
-  // ~32 rows per thread, but at least ~4 CTAs per SM on short frames (>= 4 rows per thread)
-  int chunks = (n_inner + rpi * 32 - 1) / (rpi * 32);
-  const int want = (4 * num_sms() + frames - 1) / frames, most = (n_inner + rpi * 4 - 1) / (rpi * 4);
-  if (chunks < std::min(want, most)) chunks = std::min(want, most);
-  if (chunks < 1) chunks = 1;
-  gn_apply_kernel<<<frames * chunks, threads, 0, (cudaStream_t)stream>>>(x, y, n_inner, C, groups, chunks, mean, rstd,
+  int64_t grid = (int64_t)num_sms() * occ;
+  const int64_t most = (rows + rpi * 8 - 1) / (rpi * 8);
+  if (grid > most) grid = most;
+  if (grid < 1) grid = 1;
+  gn_apply_kernel<<<(unsigned)grid, threads, 0, (cudaStream_t)stream>>>(x, y, frames, n_inner, C, groups, mean, rstd,
                                                                         gamma, beta, act);
   return launch_status("sf_group_norm_apply");
 }
