@@ -206,6 +206,65 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+// issue-only TMEM load (no wait); pair with tmem_wait_ld before reading r
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// per-column epilogue terms for 32 columns starting at global column nb: alpha, bias, per-row
+// bias, SiLU.  Vector loads when the 32 columns are in range (bias rows are 16-byte aligned).
+__device__ __forceinline__ void epi_columns(const Params& p, float* v, int nb, int64_t o) {
+  if (p.alpha != 1.f) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+  }
+  const bool full = nb + 32 <= p.N;
+  if (p.bias) {
+    if (full) {
+      const float4* b4 = reinterpret_cast<const float4*>(p.bias + nb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 b = __ldg(b4 + j);
+        v[4 * j] += b.x;
+        v[4 * j + 1] += b.y;
+        v[4 * j + 2] += b.z;
+        v[4 * j + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(p.bias + nb + j) : 0.f;
+    }
+  }
+  if (p.rowbias) {
+    const float* rb = p.rowbias + o * p.rowbias_stride + nb;
+    if (full && ((reinterpret_cast<uintptr_t>(rb) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(rb) + j);
+        v[4 * j] += b.x;
+        v[4 * j + 1] += b.y;
+        v[4 * j + 2] += b.z;
+        v[4 * j + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(rb + j) : 0.f;
+    }
+  }
+  if (p.act == SF_ACT_SILU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+  }
+}
+
 // ---------------------------------------------------------------- tiling
 struct MTile {
   int z, o0, i0;   // PLAIN/TCONV: batch/b, outer start (t0 or o0), inner start
@@ -566,22 +625,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
-          const int nb = n0 + c;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
-          if (p.bias) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(p.bias + nb + j) : 0.f;
-          }
-          if (p.rowbias) {
-            const float* rb = p.rowbias + o * p.rowbias_stride + nb;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(rb + j) : 0.f;
-          }
-          if (p.act == SF_ACT_SILU) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
-          }
+          epi_columns(p, v, n0 + c, o);
           bf16x8* sp = reinterpret_cast<bf16x8*>(srow + c * 2);
           if (has_res) {
 #pragma unroll
