@@ -27,7 +27,7 @@ namespace tc {
 
 constexpr int BM = 128, BK = 64;
 constexpr int F32_CHUNK_BYTES = 128 * 32 * 4;   // EPI 3: one 32-column fp32 chunk of a tile
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_THREADS = 320;   // warp 0 TMA, 1 MMA, 2..9 epilogue (two per TMEM lane quarter)
 constexpr int EPI_W0 = 2;  // first epilogue warp
 
 struct Params {
@@ -304,7 +304,7 @@ struct SmemLayout {
   // epilogue staging tile [128 rows][BN] bf16 (residual in, output out), row-major
   static constexpr int OUT_TILE = BM * BN * 2;
   // EPI staging buffers: 0 = direct stores; 1/2 = bf16 tiles; 3 = two 128 x 32 fp32 chunks (SW128)
-  static constexpr int OUT_BYTES = EPI == 3 ? 2 * F32_CHUNK_BYTES : EPI * OUT_TILE;
+  static constexpr int OUT_BYTES = EPI == 3 ? 4 * F32_CHUNK_BYTES : EPI * OUT_TILE;
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + OUT_BYTES + 256 /*barriers*/;
 };
 
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], PAIR ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
+      mbar_init(&tempty[s], PAIR ? 16 : 8);  // one arrive per epilogue warp (of both CTAs)
     }
     for (int b = 0; b < 2; ++b) mbar_init(&res_full[b], 1);
     if (TMA_EPI || EPI == 3) {
@@ -481,6 +481,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ================= epilogue =================
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    const int eh = (warp - EPI_W0) >> 2;    // column half: 32-column chunks eh, eh+2, eh+4, ...
     const int row = q * 32 + lane;          // accumulator row == TMEM lane
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -521,11 +522,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // fp32 output through two 16 KB staging chunks (128 rows x 32 cols, 128-byte swizzle:
         // a thread's row lands in a different bank group than its 7 neighbours), one TMA
         // store per chunk; a chunk buffer is refilled once its store from two chunks ago is read
-        const bool store_leader = warp == EPI_W0 && lane == 0;
+        // each column half (4 warps) stages its own chunks: buffers 2*eh + (k & 1), its own
+        // leader and named barrier (2 + eh)
+        const bool store_leader = warp == EPI_W0 + 4 * eh && lane == 0;
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        int k = 0;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = eh * 32; c < BN; c += 64, ++k) {
           float v[32];
           tmem_ld32(tbase + c, v);
           const int nb = n0 + c;
@@ -544,9 +548,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
           }
-          uint8_t* buf = sOut + ((c >> 5) & 1) * F32_CHUNK_BYTES;
+          uint8_t* buf = sOut + (2 * eh + (k & 1)) * F32_CHUNK_BYTES;
           if (store_leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (eh) asm volatile("bar.sync 3, 128;" ::: "memory");
+          else asm volatile("bar.sync 2, 128;" ::: "memory");
           uint8_t* srow = buf + row * 128;
           const int sw = row & 7;
 #pragma unroll
@@ -554,7 +559,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             *reinterpret_cast<float4*>(srow + ((u ^ sw) << 4)) =
                 make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (eh) asm volatile("bar.sync 3, 128;" ::: "memory");
+          else asm volatile("bar.sync 2, 128;" ::: "memory");
           if (store_leader && nb < p.N) {
             if (p.mode == SF_GEMM_CONV3X3)
               tma_store_4d(mt.tail ? &mapOT : &mapO, buf, nb, mt.x0, mt.y0, mt.f);
@@ -592,7 +598,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
             }
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          asm volatile("bar.sync 1, 256;" ::: "memory");
         } else if (has_res && store_leader) {
           // double staging: the first tile's residual now; every epilogue then
           // prefetches the next tile's residual into the other buffer as soon
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (has_res) mbar_wait(&res_full[ob], use & 1);
         uint8_t* srow = sbuf + row * (BN * 2);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = eh * 32; c < BN; c += 64) {
           float v[32];
           tmem_ld32(tbase + c, v);
           epi_columns(p, v, n0 + c, o);
@@ -648,7 +654,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         // staging tile complete -> one thread stores it with TMA (OOB rows/cols are clipped)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         if (store_leader) {
           if (p.mode == SF_GEMM_CONV3X3)
             tma_store_4d(mt.tail ? &mapOT : &mapO, sbuf, n0, mt.x0, mt.y0, mt.f);
@@ -658,7 +664,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // the other buffer's store (tile t-1) must drain before it is refilled
           if (EPI == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         }
-        if (EPI == 2) asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (EPI == 2) asm volatile("bar.sync 1, 256;" ::: "memory");
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -668,7 +674,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = eh * 32; c < BN; c += 64) {
         float v[32];
         tmem_ld32(tbase + c, v);
         const int nb = n0 + c;
@@ -1116,17 +1122,17 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   if (f32_tma) {
     if (pair) {
       switch (BN) {
-        case 256: return launch_cfg<256, 6, 3, true>(p, M, st);
-        case 160: return launch_cfg<160, 7, 3, true>(p, M, st);
-        case 128: return launch_cfg<128, 8, 3, true>(p, M, st);
-        default: return launch_cfg<64, 9, 3, true>(p, M, st);
+        case 256: return launch_cfg<256, 5, 3, true>(p, M, st);
+        case 160: return launch_cfg<160, 6, 3, true>(p, M, st);
+        case 128: return launch_cfg<128, 6, 3, true>(p, M, st);
+        default: return launch_cfg<64, 8, 3, true>(p, M, st);
       }
     }
     switch (BN) {
-      case 256: return launch_cfg<256, 4, 3>(p, M, st);
-      case 160: return launch_cfg<160, 5, 3>(p, M, st);
-      case 128: return launch_cfg<128, 6, 3>(p, M, st);
-      default: return launch_cfg<64, 8, 3>(p, M, st);
+      case 256: return launch_cfg<256, 3, 3>(p, M, st);
+      case 160: return launch_cfg<160, 4, 3>(p, M, st);
+      case 128: return launch_cfg<128, 5, 3>(p, M, st);
+      default: return launch_cfg<64, 6, 3>(p, M, st);
     }
   }
   if (pair) {
