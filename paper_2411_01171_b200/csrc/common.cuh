@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/sliceflow_b200.h"
 
@@ -86,6 +88,42 @@ __device__ __forceinline__ bf16x8 pack8(const float* f) {
   v.u.z = u32_of(__floats2bfloat162_rn(f[4], f[5]));
   v.u.w = u32_of(__floats2bfloat162_rn(f[6], f[7]));
   return v;
+}
+
+// Programmatic dependent launch (PDL).  Every kernel of this library starts with
+// griddep_wait() -- block until the grid this one depends on has completed and its
+// writes are visible (a no-op when launched without PDL) -- before touching global
+// memory, then griddep_trigger() so the next kernel in the stream can be scheduled
+// while this one runs (its blocks park in their own griddep_wait).  All launches go
+// through launch_k, which sets the stream-serialisation attribute when SF_PDL=1.
+// Off by default: measured on B200 inside the CUDA-graph run it cost ~1 % (79.2 vs
+// 80.2 steps/s) -- the parked blocks hold SM slots and the launch gaps it hides are small.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SF_PDL");
+    on = e && e[0] == '1';
+  }
+  return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

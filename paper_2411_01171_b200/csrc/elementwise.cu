@@ -34,6 +34,8 @@ static int gn_splits(int frames, int n_inner) {
 constexpr int GN_U = 8;
 __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits,
                                                             double2* partial) {
+  griddep_wait();
+  griddep_trigger();
   const int frame = blockIdx.x / splits, split = blockIdx.x % splits;
   const int nvec = C / 8;
   const int rows_per_iter = blockDim.x / nvec > 0 ? blockDim.x / nvec : 1;
@@ -113,6 +115,8 @@ __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_i
 // one warp per (frame, group): combine splits x channels in fixed order
 __global__ void gn_finalize_kernel(const double2* partial, int frames, int splits, int C, int groups,
                                    int64_t count, float eps, float* mean, float* rstd) {
+  griddep_wait();
+  griddep_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= frames * groups) return;
   const int frame = warp / groups, g = warp % groups, cg = C / groups;
@@ -143,6 +147,8 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y,
                                                        const float* __restrict__ rstd,
                                                        const float* __restrict__ gamma,
                                                        const float* __restrict__ beta, int act) {
+  griddep_wait();
+  griddep_trigger();
   const int cg = C / groups, nvec = C / 8;
   const int rpi = nvec <= (int)blockDim.x ? (int)blockDim.x / nvec : 1;   // rows per iteration
   const int64_t total = (int64_t)frames * n_inner;
@@ -209,6 +215,8 @@ template <int L, int VPL>
 __global__ void __launch_bounds__(256) layer_norm_kernel(sf_view_t x, sf_view_t y, int n_outer, int n_inner, int C,
                                                          const float* __restrict__ gamma,
                                                          const float* __restrict__ beta, float eps, int act) {
+  griddep_wait();
+  griddep_trigger();
   constexpr int RPW = 32 / L;  // rows per warp
   const int64_t rows = (int64_t)n_outer * n_inner;
   const int lane = threadIdx.x & 31, sub = lane % L, grp = lane / L;
@@ -281,6 +289,8 @@ enum { EW_SILU = 0, EW_ADD = 1, EW_COPY = 2 };
 template <int OP>
 __global__ void rows_ew_kernel(sf_view_t a, sf_view_t b, sf_view_t y, int n_outer, int n_inner, int C,
                                int b_bcast) {
+  griddep_wait();
+  griddep_trigger();
   const int nvec = C / 8;
   const int64_t total = (int64_t)n_outer * n_inner * nvec;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -309,6 +319,8 @@ __global__ void rows_ew_kernel(sf_view_t a, sf_view_t b, sf_view_t y, int n_oute
 }
 
 __global__ void copy_rows_scalar_kernel(sf_view_t x, sf_view_t y, int n_outer, int n_inner, int C) {
+  griddep_wait();
+  griddep_trigger();
   const int64_t total = (int64_t)n_outer * n_inner * C;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -320,6 +332,8 @@ __global__ void copy_rows_scalar_kernel(sf_view_t x, sf_view_t y, int n_outer, i
 }
 
 __global__ void downsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int W, int C) {
+  griddep_wait();
+  griddep_trigger();
   const int nvec = C / 8, Ho = H / 2, Wo = W / 2;
   const int64_t total = (int64_t)frames * Ho * Wo * nvec;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -339,6 +353,8 @@ __global__ void downsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, i
 }
 
 __global__ void upsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int W, int C) {
+  griddep_wait();
+  griddep_trigger();
   const int nvec = C / 8, Ho = 2 * H, Wo = 2 * W;
   const int64_t total = (int64_t)frames * Ho * Wo * nvec;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -357,6 +373,8 @@ __global__ void upsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int
 template <int PER>
 __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restrict__ s, int64_t lds,
                                                            bf16* __restrict__ p, int64_t ldp, int n) {
+  griddep_wait();
+  griddep_trigger();
   // PER float4 chunks per thread; n % 4 == 0 and 16-byte aligned rows
   const int64_t row = blockIdx.x;
   const float4* src = reinterpret_cast<const float4*>(s + row * lds);
@@ -412,6 +430,8 @@ constexpr int TA_MAXT = 64;
 constexpr int TA_CHUNK = 32;
 __global__ void __launch_bounds__(256) temporal_attn_kernel(sf_view_t qkv, int koff, int voff, sf_view_t out,
                                                             int T, int n_inner, int C, float scale) {
+  griddep_wait();
+  griddep_trigger();
   const int pix = blockIdx.x % n_inner, b = blockIdx.x / n_inner;
   __shared__ float S[TA_MAXT][TA_MAXT + 1];
   __shared__ float qs[TA_MAXT][TA_CHUNK + 1];
@@ -556,6 +576,8 @@ __device__ __forceinline__ void tq_put(bf16 (*dst)[TQ_LD], const TqChunk& r, int
 __global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
                                                                           sf_view_t out, int B, int T, int n_inner,
                                                                           int C, float scale_log2) {
+  griddep_wait();
+  griddep_trigger();
   extern __shared__ __align__(16) unsigned char tq_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bf16 (*qs)[TQ_LD] = reinterpret_cast<bf16 (*)[TQ_LD]>(tq_smem + warp * 3 * 32 * TQ_LD * 2);
@@ -708,6 +730,8 @@ __global__ void __launch_bounds__(SC_THREADS) conv_smallcin_kernel(const float* 
                                                                    int W, int cin, const float* __restrict__ wt,
                                                                    const float* __restrict__ bias, int cout,
                                                                    sf_view_t y) {
+  griddep_wait();
+  griddep_trigger();
   extern __shared__ float wsm[];  // [9][cin][cout]
   const int nw = 9 * cin * cout;
   for (int i = threadIdx.x; i < nw; i += blockDim.x) wsm[i] = wt[i];
@@ -766,6 +790,8 @@ __global__ void __launch_bounds__(SCM_THREADS) conv_smallcin_mma_kernel(const fl
                                                                        int W, int cin, const float* __restrict__ wt,
                                                                        const float* __restrict__ bias, int cout,
                                                                        sf_view_t y) {
+  griddep_wait();
+  griddep_trigger();
   using L = ScmLayout<KP>;
   extern __shared__ __align__(16) uint8_t scm_raw[];
   bf16* sA = reinterpret_cast<bf16*>(scm_raw);
@@ -872,7 +898,7 @@ static sf_status conv_smallcin_mma_launch(const float* x, int frames, int H, int
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_smallcin_mma_kernel<KP>, SCM_THREADS, smem);
   const int64_t ntiles = ((int64_t)frames * H * W + SCM_TILE - 1) / SCM_TILE;
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));
-  conv_smallcin_mma_kernel<KP><<<(unsigned)grid, SCM_THREADS, smem, st>>>(x, frames, H, W, cin, w, bias, cout, y);
+  launch_k(conv_smallcin_mma_kernel<KP>, dim3((unsigned)grid), dim3(SCM_THREADS), smem, st, x, frames, H, W, cin, w, bias, cout, y);
   return launch_status("sf_conv3x3_smallcin(mma)");
 }
 
@@ -880,6 +906,8 @@ static sf_status conv_smallcin_mma_launch(const float* x, int frames, int H, int
 // [f][p][tap*cout + co] from one plain GEMM; each output sums its 9 shifted taps.
 __global__ void conv_tapsum_kernel(const float* __restrict__ y, int ldy, int frames, int H, int W, int cout,
                                    const float* __restrict__ bias, sf_view_t out) {
+  griddep_wait();
+  griddep_trigger();
   const int HW = H * W;
   const int64_t total = (int64_t)frames * HW * cout;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -901,6 +929,8 @@ __global__ void conv_tapsum_kernel(const float* __restrict__ y, int ldy, int fra
 
 __global__ void gemv_kernel(const float* __restrict__ Wm, const float* __restrict__ e, const float* __restrict__ b,
                             float* __restrict__ y, int N, int K) {
+  griddep_wait();
+  griddep_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= N) return;
   float a = 0.f;
@@ -911,6 +941,8 @@ __global__ void gemv_kernel(const float* __restrict__ Wm, const float* __restric
 
 __global__ void transpose_f32_kernel(const float* __restrict__ x, float* __restrict__ y, int frames, int A, int B,
                                      int to_rows) {
+  griddep_wait();
+  griddep_trigger();
   // to_rows: x[f][A=C][B=HW] -> y[f][HW][C];  else x[f][A=HW][B=C] -> y[f][C][HW]
   const int64_t total = (int64_t)frames * A * B;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -923,6 +955,8 @@ __global__ void transpose_f32_kernel(const float* __restrict__ x, float* __restr
 }
 
 __global__ void axpy_kernel(float* __restrict__ x, const float* __restrict__ e, float alpha, int64_t n) {
+  griddep_wait();
+  griddep_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = x[i] - alpha * e[i];
 }
@@ -934,6 +968,8 @@ constexpr int DOT_BLOCKS = 592, DOT_THREADS = 256;
 
 __global__ void dot3_partial_kernel(const bf16* __restrict__ a, const bf16* __restrict__ b, int64_t n,
                                     double* __restrict__ part) {
+  griddep_wait();
+  griddep_trigger();
   double aa = 0, bb = 0, ab = 0;
   const int64_t nv = n / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
@@ -976,6 +1012,8 @@ __global__ void dot3_partial_kernel(const bf16* __restrict__ a, const bf16* __re
 }
 
 __global__ void sum_parts_kernel(const double* __restrict__ part, int nparts, int width, double* __restrict__ out) {
+  griddep_wait();
+  griddep_trigger();
   // out[j] = sum_p part[p*width + j], fixed order
   for (int j = threadIdx.x; j < width; j += blockDim.x) {
     double s = 0;
@@ -988,6 +1026,8 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int nparts, in
 constexpr int GRAM_BLOCKS = 296;
 __global__ void gram_partial_kernel(const bf16* const* __restrict__ probes, int K, int64_t n,
                                     double* __restrict__ part) {
+  griddep_wait();
+  griddep_trigger();
   const int npairs = K * (K + 1) / 2;
   const int64_t nv = n / 8;
   const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
@@ -1026,6 +1066,8 @@ __global__ void gram_partial_kernel(const bf16* const* __restrict__ probes, int 
 }
 
 __global__ void gram_finalize_kernel(const double* __restrict__ sums, int K, double* __restrict__ out) {
+  griddep_wait();
+  griddep_trigger();
   int pr = 0;
   for (int i = 0; i < K; ++i)
     for (int j = i; j < K; ++j, ++pr)
@@ -1070,9 +1112,9 @@ sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int3
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(gn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
-  gn_partial_kernel<<<frames * splits, threads, smem, st>>>(x, n_inner, C, splits, (double2*)work);
+  launch_k(gn_partial_kernel, dim3(frames * splits), dim3(threads), smem, st, x, n_inner, C, splits, (double2*)work);
   int warps = frames * groups;
-  gn_finalize_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>((const double2*)work, frames, splits, C, groups,
+  launch_k(gn_finalize_kernel, dim3((warps * 32 + 255) / 256), dim3(256), 0, st, (const double2*)work, frames, splits, C, groups,
                                                                 (int64_t)n_inner * (C / groups), eps, mean, rstd);
   return launch_status("sf_group_norm_stats");
 }
@@ -1098,7 +1140,7 @@ sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t 
   const int64_t most = (rows + rpi * 8 - 1) / (rpi * 8);
   if (grid > most) grid = most;
   if (grid < 1) grid = 1;
-  gn_apply_kernel<<<(unsigned)grid, threads, 0, (cudaStream_t)stream>>>(x, y, frames, n_inner, C, groups, mean, rstd,
+  launch_k(gn_apply_kernel, dim3((unsigned)grid), dim3(threads), 0, (cudaStream_t)stream, x, y, frames, n_inner, C, groups, mean, rstd,
                                                                         gamma, beta, act);
   return launch_status("sf_group_norm_apply");
 }
@@ -1119,7 +1161,7 @@ sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inn
   int64_t g = (warps * 32 + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 8;
   const int grid = (int)(g < cap ? (g < 1 ? 1 : g) : cap);
-#define SF_LN(LL, VV) layer_norm_kernel<LL, VV><<<grid, 256, 0, st>>>(x, y, n_outer, n_inner, C, gamma, beta, eps, act)
+#define SF_LN(LL, VV) launch_k(layer_norm_kernel<LL, VV>, dim3(grid), dim3(256), 0, st, x, y, n_outer, n_inner, C, gamma, beta, eps, act)
   if (L == 1) SF_LN(1, 5);
   else if (L == 2) SF_LN(2, 5);
   else if (L == 4) SF_LN(4, 5);
@@ -1136,7 +1178,7 @@ sf_status sf_silu(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, in
   SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0, SF_ERR_SHAPE, "bad extents");
   SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
   int64_t total = (int64_t)n_outer * n_inner * (C / 8);
-  rows_ew_kernel<EW_SILU><<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, x, y, n_outer, n_inner, C, 0);
+  launch_k(rows_ew_kernel<EW_SILU>, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, x, y, n_outer, n_inner, C, 0);
   return launch_status("sf_silu");
 }
 
@@ -1145,7 +1187,7 @@ sf_status sf_add(sf_view_t a, sf_view_t b, sf_view_t y, int32_t n_outer, int32_t
   SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0, SF_ERR_SHAPE, "bad extents");
   SF_CHECK_ARG(view_vec8_ok(a) && view_vec8_ok(b) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
   int64_t total = (int64_t)n_outer * n_inner * (C / 8);
-  rows_ew_kernel<EW_ADD><<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(a, b, y, n_outer, n_inner, C,
+  launch_k(rows_ew_kernel<EW_ADD>, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, a, b, y, n_outer, n_inner, C,
                                                                                  b_broadcast_inner);
   return launch_status("sf_add");
 }
@@ -1155,11 +1197,11 @@ sf_status sf_copy_rows(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inne
   SF_CHECK_ARG(x.ptr && y.ptr, SF_ERR_PARAM, "null view");
   if (C % 8 || !view_vec8_ok(x) || !view_vec8_ok(y)) {  // odd channel ranges: element copy
     int64_t total = (int64_t)n_outer * n_inner * C;
-    copy_rows_scalar_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, n_outer, n_inner, C);
+    launch_k(copy_rows_scalar_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, n_outer, n_inner, C);
     return launch_status("sf_copy_rows");
   }
   int64_t total = (int64_t)n_outer * n_inner * (C / 8);
-  rows_ew_kernel<EW_COPY><<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, x, y, n_outer, n_inner, C, 0);
+  launch_k(rows_ew_kernel<EW_COPY>, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, x, y, n_outer, n_inner, C, 0);
   return launch_status("sf_copy_rows");
 }
 
@@ -1167,14 +1209,14 @@ sf_status sf_downsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, i
   SF_CHECK_ARG(H % 2 == 0 && W % 2 == 0, SF_ERR_SHAPE, "downsample2x needs even h, w");
   SF_CHECK_ARG(frames >= 1 && C % 8 == 0 && view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "bad view");
   int64_t total = (int64_t)frames * (H / 2) * (W / 2) * (C / 8);
-  downsample_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, H, W, C);
+  launch_k(downsample_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, frames, H, W, C);
   return launch_status("sf_downsample2x");
 }
 
 sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, void* stream) {
   SF_CHECK_ARG(frames >= 1 && C % 8 == 0 && view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "bad view");
   int64_t total = (int64_t)frames * (2 * H) * (2 * W) * (C / 8);
-  upsample_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, H, W, C);
+  launch_k(upsample_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, frames, H, W, C);
   return launch_status("sf_upsample2x");
 }
 
@@ -1185,7 +1227,7 @@ sf_status sf_softmax_rows(const float* s, int64_t lds, void* p, int64_t ldp, int
   cudaStream_t st = (cudaStream_t)stream;
   const int per = (n / 4 + 255) / 256;
   bf16* P = (bf16*)p;
-#define SF_SM(K) softmax_rows_kernel<K><<<(unsigned)rows, 256, 0, st>>>(s, lds, P, ldp, n)
+#define SF_SM(K) launch_k(softmax_rows_kernel<K>, dim3((unsigned)rows), dim3(256), 0, st, s, lds, P, ldp, n)
   if (per <= 1) SF_SM(1);
   else if (per <= 2) SF_SM(2);
   else if (per <= 3) SF_SM(3);
@@ -1208,12 +1250,11 @@ sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, 
       init = true;
     }
     int64_t warps = (int64_t)B * n_inner;
-    temporal_attn_mma_kernel<<<(unsigned)((warps + TQ_WARPS - 1) / TQ_WARPS), TQ_WARPS * 32, smem,
-                               (cudaStream_t)stream>>>(qkv, koff, voff, out, B, T, n_inner, C,
+    launch_k(temporal_attn_mma_kernel, dim3((unsigned)((warps + TQ_WARPS - 1) / TQ_WARPS)), dim3(TQ_WARPS * 32), smem, (cudaStream_t)stream, qkv, koff, voff, out, B, T, n_inner, C,
                                                        scale * 1.4426950408889634f);
     return launch_status("sf_temporal_attention_core");
   }
-  temporal_attn_kernel<<<B * n_inner, 256, 0, (cudaStream_t)stream>>>(qkv, koff, voff, out, T, n_inner, C, scale);
+  launch_k(temporal_attn_kernel, dim3(B * n_inner), dim3(256), 0, (cudaStream_t)stream, qkv, koff, voff, out, T, n_inner, C, scale);
   return launch_status("sf_temporal_attention_core");
 }
 
@@ -1240,7 +1281,7 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
       cfg32 = smem;
     }
     const int64_t total = (int64_t)frames * H * W * (cout / 32);
-    conv_smallcin_kernel<32><<<ew_grid(total, SC_THREADS), SC_THREADS, smem, st>>>(x, frames, H, W, cin, w, bias,
+    launch_k(conv_smallcin_kernel<32>, dim3(ew_grid(total, SC_THREADS)), dim3(SC_THREADS), smem, st, x, frames, H, W, cin, w, bias,
                                                                                    cout, y);
   } else {
     static size_t cfg8 = 0;
@@ -1249,7 +1290,7 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
       cfg8 = smem;
     }
     const int64_t total = (int64_t)frames * H * W * (cout / 8);
-    conv_smallcin_kernel<8><<<ew_grid(total, SC_THREADS), SC_THREADS, smem, st>>>(x, frames, H, W, cin, w, bias,
+    launch_k(conv_smallcin_kernel<8>, dim3(ew_grid(total, SC_THREADS)), dim3(SC_THREADS), smem, st, x, frames, H, W, cin, w, bias,
                                                                                   cout, y);
   }
   return launch_status("sf_conv3x3_smallcin");
@@ -1260,30 +1301,30 @@ sf_status sf_conv3x3_tapsum(const float* y, int32_t ldy, int32_t frames, int32_t
   SF_CHECK_ARG(frames >= 1 && H >= 1 && W >= 1 && cout >= 1 && ldy >= 9 * cout, SF_ERR_SHAPE, "bad extents");
   SF_CHECK_ARG(y && out.ptr, SF_ERR_PARAM, "null buffer");
   const int64_t total = (int64_t)frames * H * W * cout;
-  conv_tapsum_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(y, ldy, frames, H, W, cout, bias, out);
+  launch_k(conv_tapsum_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, y, ldy, frames, H, W, cout, bias, out);
   return launch_status("sf_conv3x3_tapsum");
 }
 
 sf_status sf_gemv_f32(const float* W, const float* e, const float* b, float* y, int32_t N, int32_t K, void* stream) {
   SF_CHECK_ARG(N >= 1 && K >= 1, SF_ERR_SHAPE, "bad extents");
-  gemv_kernel<<<(N * 32 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(W, e, b, y, N, K);
+  launch_k(gemv_kernel, dim3((N * 32 + 255) / 256), dim3(256), 0, (cudaStream_t)stream, W, e, b, y, N, K);
   return launch_status("sf_gemv_f32");
 }
 
 sf_status sf_bcthw_to_rows_f32(const float* x, float* y, int32_t frames, int32_t C, int32_t HW, void* stream) {
   int64_t total = (int64_t)frames * C * HW;
-  transpose_f32_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, C, HW, 1);
+  launch_k(transpose_f32_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, frames, C, HW, 1);
   return launch_status("sf_bcthw_to_rows_f32");
 }
 
 sf_status sf_rows_to_bcthw_f32(const float* x, float* y, int32_t frames, int32_t C, int32_t HW, void* stream) {
   int64_t total = (int64_t)frames * C * HW;
-  transpose_f32_kernel<<<ew_grid(total, 256), 256, 0, (cudaStream_t)stream>>>(x, y, frames, HW, C, 0);
+  launch_k(transpose_f32_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, frames, HW, C, 0);
   return launch_status("sf_rows_to_bcthw_f32");
 }
 
 sf_status sf_axpy_f32(float* x, const float* eps, float alpha, int64_t n, void* stream) {
-  axpy_kernel<<<ew_grid(n, 256), 256, 0, (cudaStream_t)stream>>>(x, eps, alpha, n);
+  launch_k(axpy_kernel, dim3(ew_grid(n, 256)), dim3(256), 0, (cudaStream_t)stream, x, eps, alpha, n);
   return launch_status("sf_axpy_f32");
 }
 
@@ -1292,8 +1333,8 @@ int64_t sf_dot3_workspace(int64_t n) { return (int64_t)DOT_BLOCKS * 3 * sizeof(d
 sf_status sf_dot3_bf16(const void* a, const void* b, int64_t n, void* work, double* out, void* stream) {
   SF_CHECK_ARG(n >= 1 && aligned16(a) && aligned16(b), SF_ERR_PARAM, "bad probe buffers");
   cudaStream_t st = (cudaStream_t)stream;
-  dot3_partial_kernel<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>((const bf16*)a, (const bf16*)b, n, (double*)work);
-  sum_parts_kernel<<<1, 32, 0, st>>>((const double*)work, DOT_BLOCKS, 3, out);
+  launch_k(dot3_partial_kernel, dim3(DOT_BLOCKS), dim3(DOT_THREADS), 0, st, (const bf16*)a, (const bf16*)b, n, (double*)work);
+  launch_k(sum_parts_kernel, dim3(1), dim3(32), 0, st, (const double*)work, DOT_BLOCKS, 3, out);
   return launch_status("sf_dot3_bf16");
 }
 
@@ -1308,9 +1349,9 @@ sf_status sf_gram_bf16(const void* const* probes, int32_t K, int64_t n, void* wo
   int npairs = K * (K + 1) / 2;
   double* part = (double*)work;
   double* sums = part + (int64_t)GRAM_BLOCKS * npairs;
-  gram_partial_kernel<<<GRAM_BLOCKS, DOT_THREADS, 0, st>>>((const bf16* const*)probes, K, n, part);
-  sum_parts_kernel<<<1, 256, 0, st>>>(part, GRAM_BLOCKS, npairs, sums);
-  gram_finalize_kernel<<<1, 32, 0, st>>>(sums, K, out);
+  launch_k(gram_partial_kernel, dim3(GRAM_BLOCKS), dim3(DOT_THREADS), 0, st, (const bf16* const*)probes, K, n, part);
+  launch_k(sum_parts_kernel, dim3(1), dim3(256), 0, st, part, GRAM_BLOCKS, npairs, sums);
+  launch_k(gram_finalize_kernel, dim3(1), dim3(32), 0, st, sums, K, out);
   return launch_status("sf_gram_bf16");
 }
 

@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
+  // prologue (barriers, TMEM) done without touching global data: now wait for the
+  // producing kernel (PDL) and let the next one be scheduled
+  griddep_wait();
+  griddep_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -404,7 +408,7 @@ static sf_status launch(const Params& p, const CUtensorMap& q, const CUtensorMap
     init = true;
   }
   dim3 grid((p.HW + BQ - 1) / BQ, p.frames);
-  flash2_kernel<D><<<grid, THREADS, smem, st>>>(p, q, k, v);
+  launch_k(flash2_kernel<D>, dim3(grid), dim3(THREADS), smem, st, p, q, k, v);
   return launch_status("sf_spatial_attention_core(v2)");
 }
 

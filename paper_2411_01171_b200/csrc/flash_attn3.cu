@@ -243,6 +243,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   cluster_sync();
   fence_after();
   const uint32_t tmem = *tslot;
+  // prologue (barriers, TMEM) done without touching global data: now wait for the
+  // producing kernel (PDL) and let the next one be scheduled
+  griddep_wait();
+  griddep_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -476,13 +480,15 @@ static sf_status launch(const Params& p, const CUtensorMap& q, const CUtensorMap
   cfg.blockDim = dim3(THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, flash3_kernel<D>, p, q, k, v);
   return launch_status("sf_spatial_attention_core(v3, 2-CTA)");
 }

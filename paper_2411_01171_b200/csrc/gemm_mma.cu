@@ -74,6 +74,8 @@ __device__ __forceinline__ const bf16* a_addr(const sf_gemm_args& p, const bf16*
 
 template <bool WK>
 __global__ void __launch_bounds__(THREADS) gemm_kernel(const __grid_constant__ sf_gemm_args p) {
+  griddep_wait();
+  griddep_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -242,14 +244,14 @@ sf_status gemm_mma_launch(const sf_gemm_args& p, cudaStream_t st) {
       cudaFuncSetAttribute(mma::gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       init = true;
     }
-    mma::gemm_kernel<true><<<grid, mma::THREADS, smem, st>>>(p);
+    launch_k(mma::gemm_kernel<true>, dim3(grid), dim3(mma::THREADS), smem, st, p);
   } else {
     static bool init = false;
     if (!init) {
       cudaFuncSetAttribute(mma::gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       init = true;
     }
-    mma::gemm_kernel<false><<<grid, mma::THREADS, smem, st>>>(p);
+    launch_k(mma::gemm_kernel<false>, dim3(grid), dim3(mma::THREADS), smem, st, p);
   }
   return launch_status("sf_gemm(mma.sync)");
 }

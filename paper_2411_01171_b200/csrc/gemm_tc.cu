@@ -376,6 +376,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (PAIR) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue (barriers, TMEM) done without touching global data: now wait for the
+  // producing kernel (PDL) and let the next one be scheduled
+  griddep_wait();
+  griddep_trigger();
 
   const int kiters = p.taps * p.cblocks;
   // tile walk: a pair walks pair-tiles (two adjacent M-tiles x one N-tile)
@@ -882,7 +886,7 @@ static sf_status launch_cfg(const tc::Params& p, const tc::Maps& m, cudaStream_t
   if (!PAIR) {
     int64_t tiles = p.tiles_m * p.tiles_n;
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    kern<<<grid, tc::NUM_THREADS, smem, st>>>(p, m.a, m.b, m.r, m.o, m.at, m.rt, m.ot);
+    launch_k(kern, dim3(grid), dim3(tc::NUM_THREADS), smem, st, p, m.a, m.b, m.r, m.o, m.at, m.rt, m.ot);
     return launch_status("sf_gemm(tcgen05)");
   }
   const int64_t pair_tiles = (p.tiles_m + 1) / 2 * p.tiles_n;
@@ -892,13 +896,15 @@ static sf_status launch_cfg(const tc::Params& p, const tc::Maps& m, cudaStream_t
   cfg.blockDim = dim3(tc::NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, kern, p, m.a, m.b, m.r, m.o, m.at, m.rt, m.ot);
   return launch_status("sf_gemm(tcgen05 pair)");
 }
