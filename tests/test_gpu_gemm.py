@@ -181,3 +181,18 @@ def test_temporal_core(B, T, P, C):
     q, k, v = x[..., :C], x[..., C:2 * C], x[..., 2 * C:]
     ref = (torch.softmax(q @ k.transpose(-1, -2) * C ** -0.5, dim=-1) @ v).permute(0, 2, 1, 3).reshape(-1, C)
     assert rel(o, ref) <= 1.5e-2
+
+
+@pytest.mark.parametrize("C", [8, 32, 64, 96, 128, 192, 320, 640, 960, 1280, 1920, 2560])
+def test_layer_norm_widths(C):
+    """sf_layer_norm vs torch layer_norm at every lanes-per-row / vectors-per-lane dispatch."""
+    torch.manual_seed(7)
+    rows = 333
+    x = rnd(rows, C, scale=3.0)
+    g = torch.randn(C, device=dev)
+    b = torch.randn(C, device=dev)
+    y = torch.empty_like(x)
+    N.call("sf_layer_norm", Rows(x, 0, rows).view(), Rows(y, 0, rows).view(), 1, rows, C, g.data_ptr(), b.data_ptr(),
+           1e-5, N.ACT_NONE, torch.cuda.current_stream().cuda_stream)
+    ref = F.layer_norm(x.float(), (C,), g, b, 1e-5)
+    assert rel(y, ref) <= 1e-2
