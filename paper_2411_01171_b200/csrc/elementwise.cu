@@ -352,18 +352,22 @@ __global__ void downsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, i
   }
 }
 
+// nearest 2x upsample: one thread per input 16-byte vector, stored to its 2x2 output block
+// (one load, four coalesced stores; 32-bit index math)
 __global__ void upsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int W, int C) {
   griddep_wait();
   griddep_trigger();
-  const int nvec = C / 8, Ho = 2 * H, Wo = 2 * W;
-  const int64_t total = (int64_t)frames * Ho * Wo * nvec;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int v = idx % nvec;
-    int64_t p = idx / nvec;
-    int xo = p % Wo, yo = (p / Wo) % Ho, f = p / ((int64_t)Wo * Ho);
-    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, yo * Wo + xo) + v * 8) =
-        *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (yo / 2) * W + xo / 2) + v * 8);
+  const int nvec = C / 8, Wo = 2 * W;
+  const uint32_t total = (uint32_t)frames * H * W * nvec;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t v = idx % nvec, p = idx / nvec;
+    const uint32_t xi = p % W, t = p / W, yi = t % H, f = t / H;
+    const bf16x8 val = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (int64_t)yi * W + xi) + v * 8);
+    const int64_t o = (int64_t)(2 * yi) * Wo + 2 * xi;
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o) + v * 8) = val;
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 1) + v * 8) = val;
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + Wo) + v * 8) = val;
+    *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + Wo + 1) + v * 8) = val;
   }
 }
 
@@ -1224,7 +1228,8 @@ sf_status sf_downsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, i
 
 sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, void* stream) {
   SF_CHECK_ARG(frames >= 1 && C % 8 == 0 && view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "bad view");
-  int64_t total = (int64_t)frames * (2 * H) * (2 * W) * (C / 8);
+  int64_t total = (int64_t)frames * H * W * (C / 8);   // one thread per input vector
+  SF_CHECK_ARG(total < (1ll << 31), SF_ERR_SHAPE, "upsample input too large for 32-bit indexing");
   launch_k(upsample_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, frames, H, W, C);
   return launch_status("sf_upsample2x");
 }
