@@ -129,22 +129,27 @@ __device__ __forceinline__ void tma3_2sm(const CUtensorMap* m, uint32_t bar_clus
       "l"(m), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// The MMA warp runs converged (all 32 lanes, warp-uniform descriptors) and every tcgen05
+// instruction is issued by one elect.sync-chosen lane inside the asm: with the operands
+// provably uniform ptxas keeps them in uniform registers and emits no per-MMA waterfall
+// loop (issuing from a lane==0 branch cost ~13 SASS instructions per MMA).
 __device__ __forceinline__ void mma2_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 __device__ __forceinline__ void mma2_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
 }
 // arrive on the barrier at this offset in both CTAs once the leader's MMAs complete
 __device__ __forceinline__ void commit2(uint64_t* bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
           smem_u32(bar)),
       "h"((uint16_t)0x3)
       : "memory");
@@ -271,8 +276,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
-      // ---------------- MMA issuer (leader only), M = 256 ----------------
+    if (leader) {
+      // ---------------- MMA issuer (leader only, whole warp converged), M = 256 ----------------
       constexpr uint32_t idS = idesc256(BKV), idO = idesc256(D / 2);
       mbar_wait(q_full, 0);
       fence_after();
