@@ -822,9 +822,9 @@ static int pick_bn(int N) {
 // tile's per-CTA work (128 x BN x K) times a per-width efficiency factor.
 // Pairs and wide tiles win unless they cost whole extra rounds.
 static bool choose_tiling(int N, int64_t tiles_m, bool pair_ok, int* bn) {
-  // per-unit-work cost by tile width, measured on B200 conv/linear shapes:
-  // narrower MMAs pay a fixed issue cost (N=160 ~1.3x the cost of N=256)
-  auto eff = [](int b) { return b >= 256 ? 1.0 : b == 160 ? 1.3 : b == 128 ? 1.35 : 1.6; };
+  // per-unit-work cost by tile width, measured on B200 conv shapes (L0 conv, N = 128..1024):
+  // narrower tiles move more operand bytes per flop (N=160 ~1.15x, N=128 ~1.3x of N=256)
+  auto eff = [](int b) { return b >= 256 ? 1.0 : b == 160 ? 1.15 : b == 128 ? 1.3 : 1.6; };
   const int sms = num_sms();
   int cands[4], nc = 0;
   cands[nc++] = *bn;
