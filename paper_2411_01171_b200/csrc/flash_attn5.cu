@@ -133,6 +133,21 @@ __device__ __forceinline__ void tma3_2sm(const CUtensorMap* m, uint32_t bar_clus
 // instruction is issued by one elect.sync-chosen lane inside the asm: with the operands
 // provably uniform ptxas keeps them in uniform registers and emits no per-MMA waterfall
 // loop (issuing from a lane==0 branch cost ~13 SASS instructions per MMA).
+// converged-warp producer variants (one elect.sync lane issues; whole warp calls)
+__device__ __forceinline__ void mbar_expect_tx_e(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma3_2sm_e(const CUtensorMap* m, uint32_t bar_cluster, void* dst, int c0, int c1,
+                                           int c2) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void mma2_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
@@ -240,11 +255,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   griddep_trigger();
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // whole warp converged, elect.sync issue
       // ---------------- TMA: my halves, completion counted on the leader ----------------
-      if (leader) mbar_expect_tx(q_full, 2 * L::Q_BYTES);
+      if (leader) mbar_expect_tx_e(q_full, 2 * L::Q_BYTES);
       const uint32_t qbar = leader_addr(q_full);
-      for (int c = 0; c < L::NCH; ++c) tma3_2sm(&mQ, qbar, sQ + c * BQ * 128, c * 64, q0, f);
+      for (int c = 0; c < L::NCH; ++c) tma3_2sm_e(&mQ, qbar, sQ + c * BQ * 128, c * 64, q0, f);
       int slot = 0;
       uint32_t ph = 0;
       auto next = [&]() {
@@ -255,13 +270,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       auto item = [&](int bytes_both) {
         mbar_wait(&r_empty[slot], ph ^ 1);
-        if (leader) mbar_expect_tx(&r_full[slot], bytes_both);
+        if (leader) mbar_expect_tx_e(&r_full[slot], bytes_both);
         return leader_addr(&r_full[slot]);
       };
       auto load_k = [&](int j) {
         const uint32_t b = item(2 * L::K_HALF);
         for (int c = 0; c < L::NCH; ++c)
-          tma3_2sm(&mK, b, sRing + slot * L::SLOT + c * L::K_SUB, c * 64, j * BKV + (int)rank * (BKV / 2), f);
+          tma3_2sm_e(&mK, b, sRing + slot * L::SLOT + c * L::K_SUB, c * 64, j * BKV + (int)rank * (BKV / 2), f);
         next();
       };
       load_k(0);
@@ -270,7 +285,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t b = item(2 * L::V_HALF);
         for (int h = 0; h < 2; ++h)
           for (int kc = 0; kc < L::NKC; ++kc)
-            tma3_2sm(&mV, b, sRing + slot * L::SLOT + (h * L::NKC + kc) * L::V_CH, j * BKV + kc * 32,
+            tma3_2sm_e(&mV, b, sRing + slot * L::SLOT + (h * L::NKC + kc) * L::V_CH, j * BKV + kc * 32,
                      h * (D / 2) + (int)rank * (D / 4), f);
         next();
       }

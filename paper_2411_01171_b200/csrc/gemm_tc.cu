@@ -138,6 +138,49 @@ __device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, uint32_t
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// Converged-warp producer variants: every lane executes the call with warp-uniform
+// operands and one elect.sync lane issues the instruction (no per-instruction
+// waterfall loop, see the MMA issuer).  Only for code the whole warp runs.
+__device__ __forceinline__ void mbar_expect_tx_e(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_e(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                              int c3) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_e(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n}\n" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_2sm_e(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1,
+                                                  int c2, int c3) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm_e(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1,
+                                                  int c2) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                               uint32_t accumulate) {
   asm volatile(
@@ -395,8 +438,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   };
 
   if (warp == 0) {
-    // ================= TMA producer =================
-    if (lane == 0) {
+    // ================= TMA producer (whole warp converged, elect.sync issue) =================
+    {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t tcount = 0;
@@ -411,32 +454,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           void* dB = sB + stage * L::B_BYTES;
           if constexpr (PAIR) {
             // my A tile + my half of B, completion bytes counted on the leader's barrier
-            if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+            if (leader) mbar_expect_tx_e(&full[stage], 2 * L::STAGE_BYTES);
             const uint32_t fb = leader_addr(&full[stage]);
             if (p.mode == SF_GEMM_CONV3X3)
-              tma_load_4d_2sm(mt.tail ? &mapAT : &mapA, fb, dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1,
+              tma_load_4d_2sm_e(mt.tail ? &mapAT : &mapA, fb, dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1,
                               mt.f);
             else if (p.mode == SF_GEMM_TCONV3)
-              tma_load_4d_2sm(&mapA, fb, dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
+              tma_load_4d_2sm_e(&mapA, fb, dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
             else
-              tma_load_4d_2sm(&mapA, fb, dA, cb * BK, mt.i0, mt.o0, p.a_batched ? mt.z : 0);
-            tma_load_3d_2sm(&mapB, fb, dB, tap * p.cin + cb * BK, n0 + (int)rank * (BN / 2), p.b_batched ? mt.z : 0);
+              tma_load_4d_2sm_e(&mapA, fb, dA, cb * BK, mt.i0, mt.o0, p.a_batched ? mt.z : 0);
+            tma_load_3d_2sm_e(&mapB, fb, dB, tap * p.cin + cb * BK, n0 + (int)rank * (BN / 2), p.b_batched ? mt.z : 0);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
             continue;
           }
-          mbar_expect_tx(&full[stage], L::STAGE_BYTES);
+          mbar_expect_tx_e(&full[stage], L::STAGE_BYTES);
           if (p.mode == SF_GEMM_CONV3X3) {
-            tma_load_4d(mt.tail ? &mapAT : &mapA, &full[stage], dA, cb * BK, mt.x0 + tap % 3 - 1,
+            tma_load_4d_e(mt.tail ? &mapAT : &mapA, &full[stage], dA, cb * BK, mt.x0 + tap % 3 - 1,
                         mt.y0 + tap / 3 - 1, mt.f);
           } else if (p.mode == SF_GEMM_TCONV3) {
-            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
+            tma_load_4d_e(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0 + tap - 1, mt.z);
           } else {
-            tma_load_4d(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0, p.a_batched ? mt.z : 0);
+            tma_load_4d_e(&mapA, &full[stage], dA, cb * BK, mt.i0, mt.o0, p.a_batched ? mt.z : 0);
           }
-          tma_load_3d(&mapB, &full[stage], dB, tap * p.cin + cb * BK, n0, p.b_batched ? mt.z : 0);
+          tma_load_3d_e(&mapB, &full[stage], dB, tap * p.cin + cb * BK, n0, p.b_batched ? mt.z : 0);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
