@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   using L = Cfg<D>;
   constexpr int BKV = L::BKV, NSLOT = L::NSLOT;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by offsetting the shared array itself (a uintptr_t round trip loses
+  // the shared address space: every C++ staging access became a generic LD/ST.E)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = base;
   uint8_t* sRing = sQ + L::Q_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRing + NSLOT * L::SLOT);

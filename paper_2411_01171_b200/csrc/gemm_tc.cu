@@ -364,7 +364,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   using L = SmemLayout<BN, STAGES, EPI, PAIR>;
   constexpr bool TMA_EPI = EPI == 1 || EPI == 2;   // bf16 staging + TMA store (EPI 3: fp32 chunks)
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by offsetting the shared array itself (a uintptr_t round trip loses
+  // the shared address space: every C++ staging access became a generic LD/ST.E)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * L::A_BYTES;
   uint8_t* sOut = smem + STAGES * L::STAGE_BYTES;
