@@ -22,6 +22,7 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--detail", action="store_true")
 ap.add_argument("--key-only", action="store_true", help="one key step, no tail step")
 ap.add_argument("--tail", action="store_true", help="--detail profiles the tail (rehash) step instead")
+ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays of one key and one tail step")
 a = ap.parse_args()
 cfg = UNetConfig(**CONFIGS[a.config])
 den = Denoiser(cfg, ExecConfig(gemm_backend=a.backend), K=2)
@@ -70,3 +71,25 @@ if a.detail:
             print(f"{ms*1e3:9.1f} us  {-fl / (ms * 1e6):7.1f} GB/s  {name} {info}")
         else:
             print(f"{ms*1e3:9.1f} us  {fl/ (ms*1e9) if fl else 0:7.1f} TF  {name} {info}")
+if a.graph:
+    def graph_time(fn, reps=20):
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                fn(cs.cuda_stream)
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record()
+        for _ in range(reps):
+            g.replay()
+        e_.record()
+        torch.cuda.synchronize()
+        return s_.elapsed_time(e_) / reps
+    key_ms = graph_time(lambda sp: den.plan.run_full(sp, den.emb_table[0].data_ptr()))
+    tail_ms = graph_time(lambda sp: den.plan.run_tail(sp))
+    print(f"graph replay: key step {key_ms:.3f} ms, tail step {tail_ms:.3f} ms")
