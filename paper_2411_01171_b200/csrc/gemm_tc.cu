@@ -262,19 +262,21 @@ __device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// per-column epilogue terms for 32 columns starting at global column nb: alpha, bias, per-row
-// bias, SiLU.  Vector loads when the 32 columns are in range (bias rows are 16-byte aligned).
+// per-column epilogue terms for W (32 or 16) columns starting at global column nb: alpha,
+// bias, per-row bias, SiLU.  Vector loads when all W columns are in range (bias rows are
+// 16-byte aligned).
+template <int W = 32>
 __device__ __forceinline__ void epi_columns(const Params& p, float* v, int nb, int64_t o) {
   if (p.alpha != 1.f) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+    for (int j = 0; j < W; ++j) v[j] *= p.alpha;
   }
-  const bool full = nb + 32 <= p.N;
+  const bool full = nb + W <= p.N;
   if (p.bias) {
     if (full) {
       const float4* b4 = reinterpret_cast<const float4*>(p.bias + nb);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < W / 4; ++j) {
         const float4 b = __ldg(b4 + j);
         v[4 * j] += b.x;
         v[4 * j + 1] += b.y;
@@ -283,14 +285,14 @@ __device__ __forceinline__ void epi_columns(const Params& p, float* v, int nb, i
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(p.bias + nb + j) : 0.f;
+      for (int j = 0; j < W; ++j) v[j] += (nb + j < p.N) ? __ldg(p.bias + nb + j) : 0.f;
     }
   }
   if (p.rowbias) {
     const float* rb = p.rowbias + o * p.rowbias_stride + nb;
     if (full && ((reinterpret_cast<uintptr_t>(rb) & 15) == 0)) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < W / 4; ++j) {
         const float4 b = __ldg(reinterpret_cast<const float4*>(rb) + j);
         v[4 * j] += b.x;
         v[4 * j + 1] += b.y;
@@ -299,13 +301,25 @@ __device__ __forceinline__ void epi_columns(const Params& p, float* v, int nb, i
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += (nb + j < p.N) ? __ldg(rb + j) : 0.f;
+      for (int j = 0; j < W; ++j) v[j] += (nb + j < p.N) ? __ldg(rb + j) : 0.f;
     }
   }
   if (p.act == SF_ACT_SILU) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+    for (int j = 0; j < W; ++j) v[j] = silu_f(v[j]);
   }
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
 // ---------------------------------------------------------------- tiling
@@ -374,8 +388,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
-  uint64_t* res_full = tempty + 2;    // [2] residual tile landed in staging buffer b
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 2);
+  uint64_t* res_full = tempty + 2;    // [2 buffers][2 halves] residual half-tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 4);
   const bool has_res = TMA_EPI && p.res.ptr != nullptr;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], PAIR ? 16 : 8);  // one arrive per epilogue warp (of both CTAs)
     }
-    for (int b = 0; b < 2; ++b) mbar_init(&res_full[b], 1);
+    for (int b = 0; b < 4; ++b) mbar_init(&res_full[b], 1);
     if (TMA_EPI || EPI == 3) {
       prefetch_map(&mapO);
       if (has_res) prefetch_map(&mapR);
@@ -633,56 +647,63 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         continue;
       }
       if constexpr (TMA_EPI) {
-        const bool store_leader = warp == EPI_W0 && lane == 0;
+        // The two column halves (4 warps each, one per TMEM lane quarter) run independently:
+        // each owns a contiguous BN/2-column staging sub-tile, its residual barrier, its
+        // leader (residual prefetch + TMA store) and a 128-thread named barrier, so neither
+        // half waits for the other before its store.
+        constexpr int HC = BN / 2;                    // columns per half
+        constexpr int HALF_BYTES = BM * HC * 2;
+        const bool hleader = warp == EPI_W0 + 4 * eh && lane == 0;
         const int ob = EPI == 2 ? (int)(tcount & 1) : 0;
         const uint32_t use = EPI == 2 ? (tcount >> 1) : tcount;
-        uint8_t* sbuf = sOut + ob * L::OUT_TILE;
+        uint8_t* hbuf = sOut + ob * L::OUT_TILE + eh * HALF_BYTES;
+        const int hn0 = n0 + eh * HC;
+        uint64_t* rf = &res_full[ob * 2 + eh];
+        auto load_res_half = [&](uint64_t* bar, uint8_t* dst, int col, const MTile& m) {
+          if (p.mode == SF_GEMM_CONV3X3)
+            tma_load_4d(m.tail ? &mapRT : &mapR, bar, dst, col, m.x0, m.y0, m.f);
+          else
+            tma_load_4d(&mapR, bar, dst, col, m.i0, m.o0, m.z);
+        };
+        auto half_sync = [&]() {
+          if (eh) asm volatile("bar.sync 3, 128;" ::: "memory");
+          else asm volatile("bar.sync 2, 128;" ::: "memory");
+        };
         if (EPI == 1) {
-          // single staging buffer: the previous store must have drained it; then fetch the residual
-          if (store_leader) {
+          // single staging buffer: my previous store must have drained it; then fetch my residual
+          if (hleader) {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             if (has_res) {
-              mbar_expect_tx(&res_full[0], L::OUT_TILE);
-              if (p.mode == SF_GEMM_CONV3X3)
-                tma_load_4d(mt.tail ? &mapRT : &mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
-              else
-                tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
+              mbar_expect_tx(rf, HALF_BYTES);
+              load_res_half(rf, hbuf, hn0, mt);
             }
           }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-        } else if (has_res && store_leader) {
-          // double staging: the first tile's residual now; every epilogue then
-          // prefetches the next tile's residual into the other buffer as soon
-          // as that buffer's previous store has been read out
+          half_sync();
+        } else if (has_res && hleader) {
+          // double staging: the first tile's residual now; every epilogue then prefetches the
+          // next tile's residual into the other buffer once that buffer's store has been read
           if (tcount == 0) {
-            mbar_expect_tx(&res_full[0], L::OUT_TILE);
-            if (p.mode == SF_GEMM_CONV3X3)
-              tma_load_4d(mt.tail ? &mapRT : &mapR, &res_full[0], sbuf, n0, mt.x0, mt.y0, mt.f);
-            else
-              tma_load_4d(&mapR, &res_full[0], sbuf, n0, mt.i0, mt.o0, mt.z);
+            mbar_expect_tx(rf, HALF_BYTES);
+            load_res_half(rf, hbuf, hn0, mt);
           }
           const int64_t nt = tile + t_step;
           if (nt < n_tiles) {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             const MTile nm = decode_m(p, my_tm(nt));
-            const int nn0 = (int)(nt % p.tiles_n) * BN;
-            uint8_t* nbuf = sOut + (ob ^ 1) * L::OUT_TILE;
-            mbar_expect_tx(&res_full[ob ^ 1], L::OUT_TILE);
-            if (p.mode == SF_GEMM_CONV3X3)
-              tma_load_4d(nm.tail ? &mapRT : &mapR, &res_full[ob ^ 1], nbuf, nn0, nm.x0, nm.y0, nm.f);
-            else
-              tma_load_4d(&mapR, &res_full[ob ^ 1], nbuf, nn0, nm.i0, nm.o0, nm.z);
+            const int nn0 = (int)(nt % p.tiles_n) * BN + eh * HC;
+            uint64_t* rfn = &res_full[(ob ^ 1) * 2 + eh];
+            mbar_expect_tx(rfn, HALF_BYTES);
+            load_res_half(rfn, sOut + (ob ^ 1) * L::OUT_TILE + eh * HALF_BYTES, nn0, nm);
           }
         }
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        if (has_res) mbar_wait(&res_full[ob], use & 1);
-        uint8_t* srow = sbuf + row * (BN * 2);
-#pragma unroll 1
-        for (int c = eh * 32; c < BN; c += 64) {
+        if (has_res) mbar_wait(rf, use & 1);
+        uint8_t* srow = hbuf + row * (HC * 2);
+        auto finish32 = [&](int c) {
           float v[32];
-          tmem_ld32(tbase + c, v);
-          epi_columns(p, v, n0 + c, o);
+          tmem_ld32(tbase + eh * HC + c, v);
+          epi_columns<32>(p, v, hn0 + c, o);
           bf16x8* sp = reinterpret_cast<bf16x8*>(srow + c * 2);
           if (has_res) {
 #pragma unroll
@@ -695,6 +716,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) sp[j] = pack8(v + 8 * j);
+        };
+#pragma unroll 1
+        for (int c = 0; c + 32 <= HC; c += 32) finish32(c);
+        if constexpr (HC % 32 == 16) {
+          const int c = HC - 16;
+          float v[16];
+          tmem_ld16(tbase + eh * HC + c, v);
+          epi_columns<16>(p, v, hn0 + c, o);
+          bf16x8* sp = reinterpret_cast<bf16x8*>(srow + c * 2);
+          if (has_res) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              float f[8];
+              unpack8(sp[j], f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[j * 8 + e] += f[e];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) sp[j] = pack8(v + 8 * j);
         }
         // accumulator free for the tile after next
         tc_fence_before();
@@ -703,19 +744,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (PAIR) arrive_remote(tempty_l + acc * 8);
           else mbar_arrive(&tempty[acc]);
         }
-        // staging tile complete -> one thread stores it with TMA (OOB rows/cols are clipped)
+        // my half-tile complete -> my leader stores it with TMA (OOB rows/cols are clipped)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (store_leader) {
-          if (p.mode == SF_GEMM_CONV3X3)
-            tma_store_4d(mt.tail ? &mapOT : &mapO, sbuf, n0, mt.x0, mt.y0, mt.f);
-          else
-            tma_store_4d(&mapO, sbuf, n0, mt.i0, mt.o0, mt.z);
+        half_sync();
+        if (hleader) {
+          if (hn0 < p.N) {
+            if (p.mode == SF_GEMM_CONV3X3)
+              tma_store_4d(mt.tail ? &mapOT : &mapO, hbuf, hn0, mt.x0, mt.y0, mt.f);
+            else
+              tma_store_4d(&mapO, hbuf, hn0, mt.i0, mt.o0, mt.z);
+          }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           // the other buffer's store (tile t-1) must drain before it is refilled
           if (EPI == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         }
-        if (EPI == 2) asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (EPI == 2) half_sync();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -961,7 +1004,7 @@ static bool encode_rows_map(CUtensorMap* m, const sf_gemm_args& a, const tc::Par
                             int64_t bstride, int BN, bool tail = false, bool fp32 = false) {
   // fp32 (EPI 3): 32-column boxes in the 128-byte swizzle; bf16: one BN-wide unswizzled box
   const uint64_t es = fp32 ? 4 : 2, ld = (uint64_t)v.ld;
-  const uint32_t bw = fp32 ? 32u : (uint32_t)BN;
+  const uint32_t bw = fp32 ? 32u : (uint32_t)(BN / 2);   // bf16: one box per column half
   if (a.mode == SF_GEMM_CONV3X3) {
     uint64_t dims[4] = {(uint64_t)a.N, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.n_outer};
     uint64_t str[3] = {ld * es, (uint64_t)a.W * ld * es,
