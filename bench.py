@@ -273,6 +273,10 @@ def run_ours(args, world, rank, local):
                 "share_of_step": round(g_ms / pf["total_ms"], 4) if pf["total_ms"] else None,
                 "launches_per_key_step": g_calls, "flops_per_key_step": g_fl,
                 "peak_source": f"{peak_src} bf16_tflops_sustained"}
+    mixed = prof_full.mixed_roofline(peak_tf, peaks["hbm_gbs"])
+    roofline_mixed = {"bound": "per launch max(tensor, hbm)", "kernel": "all sf_gemm launches of one key step",
+                      "peak_tflops": peak_tf, "peak_gbps": peaks["hbm_gbs"], **mixed,
+                      "note": "algorithmic bytes: activations read once, weights, output, residual"}
     fa = pf["by_call"].get("sf_spatial_attention_core")
     roofline_attn = None
     if fa and fa["ms"]:
@@ -300,6 +304,7 @@ def run_ours(args, world, rank, local):
                 "h2d_bytes_per_step": int(x0.nbytes), "d2h_bytes_per_step": int(x0.nbytes)},
         "gpu_launches": launches_per_run * args.steps,
         "roofline": roofline,
+        "roofline_gemm_mixed": roofline_mixed,
         "roofline_attention": roofline_attn,
         "profile": {"key_step_ms": round(pf["total_ms"], 3), "tail_step_ms": round(pt["total_ms"], 3),
                     "top": {k: {"ms": round(v["ms"], 3), "calls": v["calls"], "share": round(v["share"], 3),
