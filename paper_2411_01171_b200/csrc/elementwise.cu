@@ -163,13 +163,13 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y,
       const int64_t seg_end = min(r1, (int64_t)(f + 1) * n_inner);
       const int i0 = (int)(seg - (int64_t)f * n_inner), i1 = (int)(seg_end - (int64_t)f * n_inner);
       seg = seg_end;
-      float mm[8], ss[8], bb[8];
+      // y = x * ss + bb with ss = rstd * gamma, bb = beta - mean * ss (one FMA per element)
+      float ss[8], bb[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int c = v * 8 + j, g = c / cg;
-        mm[j] = __ldg(mean + f * groups + g);
         ss[j] = __ldg(rstd + f * groups + g) * __ldg(gamma + c);
-        bb[j] = __ldg(beta + c);
+        bb[j] = fmaf(-__ldg(mean + f * groups + g), ss[j], __ldg(beta + c));
       }
       const bf16* src = row_ptr<const bf16>(x, f, 0) + v * 8;
       bf16* dst = row_ptr<bf16>(y, f, 0) + v * 8;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y,
           unpack8(in[u], fv);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float t = (fv[j] - mm[j]) * ss[j] + bb[j];
+            const float t = fmaf(fv[j], ss[j], bb[j]);
             fv[j] = act ? silu_f(t) : t;
           }
           *reinterpret_cast<bf16x8*>(dst + (int64_t)(i + u * rpi) * yld) = pack8(fv);
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y,
         unpack8(*reinterpret_cast<const bf16x8*>(src + (int64_t)i * xld), fv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float t = (fv[j] - mm[j]) * ss[j] + bb[j];
+          const float t = fmaf(fv[j], ss[j], bb[j]);
           fv[j] = act ? silu_f(t) : t;
         }
         *reinterpret_cast<bf16x8*>(dst + (int64_t)i * yld) = pack8(fv);
