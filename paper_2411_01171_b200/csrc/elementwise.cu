@@ -217,6 +217,16 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(sf_view_t x, sf_view_t 
                                                          const float* __restrict__ beta, float eps, int act) {
   griddep_wait();
   griddep_trigger();
+  // gamma / beta staged in shared memory once per block: the per-row parameter reads were 4
+  // L1 loads per 16-byte data vector, competing with the data stream
+  extern __shared__ float4 ln_par[];   // [2][C/4]
+  for (int i = threadIdx.x; i < C / 4; i += blockDim.x) {
+    ln_par[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
+    ln_par[C / 4 + i] = __ldg(reinterpret_cast<const float4*>(beta) + i);
+  }
+  __syncthreads();
+  const float4* sg = ln_par;
+  const float4* sb = ln_par + C / 4;
   constexpr int RPW = 32 / L;  // rows per warp
   const int64_t rows = (int64_t)n_outer * n_inner;
   const int lane = threadIdx.x & 31, sub = lane % L, grp = lane / L;
@@ -263,10 +273,8 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(sf_view_t x, sf_view_t 
     for (int k = 0; k < VPL; ++k) {
       const int v = sub + L * k;
       if (v < nvec) {
-        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + v * 8));
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + v * 8) + 1);
-        const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + v * 8));
-        const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + v * 8) + 1);
+        const float4 g0 = sg[2 * v], g1 = sg[2 * v + 1];
+        const float4 b0 = sb[2 * v], b1 = sb[2 * v + 1];
         const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
         const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
         float g[8];
@@ -1168,7 +1176,7 @@ sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inn
   int64_t g = (warps * 32 + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 8;
   const int grid = (int)(g < cap ? (g < 1 ? 1 : g) : cap);
-#define SF_LN(LL, VV) launch_k(layer_norm_kernel<LL, VV>, dim3(grid), dim3(256), 0, st, x, y, n_outer, n_inner, C, gamma, beta, eps, act)
+#define SF_LN(LL, VV) launch_k(layer_norm_kernel<LL, VV>, dim3(grid), dim3(256), (size_t)C * 2 * sizeof(float), st, x, y, n_outer, n_inner, C, gamma, beta, eps, act)
   // the template's VPL must cover vpl = ceil(nvec / L)
   if (L == 1 && vpl > 5) SF_LN(1, 10);
   else if (L == 1) SF_LN(1, 5);
