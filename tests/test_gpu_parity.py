@@ -145,6 +145,17 @@ def test_all_key_schedule_is_bit_identical(c1_denoiser):
     assert np.array_equal(a, c)  # deterministic kernels
 
 
+def test_tail_equals_donor_epsilon(c1_denoiser):
+    """The 9-node rehash tail has no step-dependent node, so a skipped step's epsilon computed from
+    the donor's cached probe equals the donor's epsilon bit for bit: skipping the tail
+    (reuse_donor_eps) gives the identical final latent.  (The measured path still runs the tail.)"""
+    x0 = initial_latent(C1)
+    sched = StepSchedule([0, 3, 6, 9], C1.steps)
+    x_tail = c1_denoiser.run(x0, sched)
+    den2 = Denoiser(C1, reuse_donor_eps=True)
+    assert np.array_equal(den2.run(x0, sched), x_tail)
+
+
 def test_wide_config_matches_reference(golden):
     runs = golden["runs"]
     den = Denoiser(WIDE)
