@@ -112,30 +112,78 @@ __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_i
   }
 }
 
-// one warp per (frame, group): combine splits x channels in fixed order
-__global__ void gn_finalize_kernel(const double2* partial, int frames, int splits, int C, int groups,
-                                   int64_t count, float eps, float* mean, float* rstd) {
+// mean / rstd from per-split (sum, sum sq) partials [frame][split][C] (double2 from
+// gn_partial_kernel, float2 from a GEMM epilogue).  Block = (frame, a run of whole groups):
+// one thread per channel sums its splits with independent loads in flight (the old
+// warp-per-group walk was a chain of dependent L2 round trips), then one warp per group
+// adds its channels.  Fixed summation order: bitwise reproducible.
+template <typename T>
+__global__ void __launch_bounds__(256) gn_finalize_kernel(const T* __restrict__ partial, int splits, int C,
+                                                          int groups, int gpb, int64_t count, float eps,
+                                                          float* mean, float* rstd) {
   griddep_wait();
   griddep_trigger();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= frames * groups) return;
-  const int frame = warp / groups, g = warp % groups, cg = C / groups;
-  double s = 0, q = 0;
-  for (int idx = lane; idx < splits * cg; idx += 32) {
-    int sp = idx / cg, c = g * cg + idx % cg;
-    double2 t = partial[((int64_t)frame * splits + sp) * C + c];
-    s += t.x;
-    q += t.y;
+  extern __shared__ double2 tot[];   // [gpb * cg]
+  const int cg = C / groups;
+  const int frame = blockIdx.y, g0 = blockIdx.x * gpb;
+  const int ng = min(gpb, groups - g0), nch = ng * cg;
+  const T* base = partial + (int64_t)frame * splits * C + (int64_t)g0 * cg;
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    double s = 0, q = 0;
+    int sp = 0;
+    for (; sp + 4 <= splits; sp += 4) {
+      T t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = base[(int64_t)(sp + u) * C + c];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s += (double)t[u].x;
+        q += (double)t[u].y;
+      }
+    }
+    for (; sp < splits; ++sp) {
+      const T t = base[(int64_t)sp * C + c];
+      s += (double)t.x;
+      q += (double)t.y;
+    }
+    tot[c] = make_double2(s, q);
   }
-  s = warp_sum_d(s);
-  q = warp_sum_d(q);
-  if (lane == 0) {
-    double mu = s / (double)count;
-    double var = q / (double)count - mu * mu;
-    if (var < 0) var = 0;
-    mean[warp] = (float)mu;
-    rstd[warp] = (float)(1.0 / sqrt(var + (double)eps));
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int gi = warp; gi < ng; gi += blockDim.x >> 5) {
+    double s = 0, q = 0;
+    for (int c = lane; c < cg; c += 32) {
+      s += tot[gi * cg + c].x;
+      q += tot[gi * cg + c].y;
+    }
+    s = warp_sum_d(s);
+    q = warp_sum_d(q);
+    if (lane == 0) {
+      const double mu = s / (double)count;
+      double var = q / (double)count - mu * mu;
+      if (var < 0) var = 0;
+      const int o = frame * groups + g0 + gi;
+      mean[o] = (float)mu;
+      rstd[o] = (float)(1.0 / sqrt(var + (double)eps));
+    }
   }
+}
+
+template <typename T>
+static void launch_gn_finalize(const T* partial, int frames, int splits, int C, int groups, int64_t count, float eps,
+                               float* mean, float* rstd, cudaStream_t st) {
+  const int cg = C / groups;
+  const int gpb = cg >= 256 ? 1 : min(groups, 256 / cg);
+  const size_t smem = (size_t)gpb * cg * sizeof(double2);
+  if (smem > 48 * 1024) {
+    static size_t set = 0;
+    if (smem > set) {
+      cudaFuncSetAttribute(gn_finalize_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set = smem;
+    }
+  }
+  launch_k(gn_finalize_kernel<T>, dim3((groups + gpb - 1) / gpb, frames), dim3(256), smem, st, partial, splits, C,
+           groups, gpb, count, eps, mean, rstd);
 }
 
 // y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]).  Persistent: each
@@ -1125,10 +1173,18 @@ sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int3
     cudaFuncSetAttribute(gn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   launch_k(gn_partial_kernel, dim3(frames * splits), dim3(threads), smem, st, x, n_inner, C, splits, (double2*)work);
-  int warps = frames * groups;
-  launch_k(gn_finalize_kernel, dim3((warps * 32 + 255) / 256), dim3(256), 0, st, (const double2*)work, frames, splits, C, groups,
-                                                                (int64_t)n_inner * (C / groups), eps, mean, rstd);
+  launch_gn_finalize((const double2*)work, frames, splits, C, groups, (int64_t)n_inner * (C / groups), eps, mean,
+                     rstd, st);
   return launch_status("sf_group_norm_stats");
+}
+
+sf_status sf_group_norm_finalize(const float* partial, int32_t frames, int32_t splits, int32_t C, int32_t groups,
+                                 float eps, int64_t count, float* mean, float* rstd, void* stream) {
+  SF_CHECK_ARG(partial && mean && rstd && frames >= 1 && splits >= 1 && groups >= 1 && C % groups == 0 && count > 0,
+               SF_ERR_PARAM, "bad GroupNorm finalize arguments");
+  launch_gn_finalize(reinterpret_cast<const float2*>(partial), frames, splits, C, groups, count, eps, mean, rstd,
+                     (cudaStream_t)stream);
+  return launch_status("sf_group_norm_finalize");
 }
 
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,

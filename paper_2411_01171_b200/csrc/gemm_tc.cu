@@ -59,6 +59,10 @@ struct Params {
   sf_view_t out;
   int64_t out_bstride;
   int out_fp32;
+  // optional GroupNorm partial sums of the bf16 output (conv, whole-frame tiles):
+  // gn_part[((frame * gn_tpf + tile_in_frame) * 4 + lane_quarter) * N + col] = (sum, sum sq)
+  float2* gn_part;
+  int gn_tpf;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -320,6 +324,50 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Column sums over a warp's 32 rows: on entry lane l holds row l's values v[0..W), on exit
+// v[0] of lane l is the sum of column l over the 32 rows (W = 32), or -- for W = 16 -- of
+// column l & 15 (lanes l and l ^ 16 agree).  31 (resp. 16 + 15) shuffles, fixed order.
+template <int W>
+__device__ __forceinline__ void warp_colsum(float* v, int lane) {
+  if constexpr (W == 16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], 16);
+  }
+#pragma unroll
+  for (int off = W / 2; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const float send = upper ? v[j] : v[j + off];
+      const float keep = upper ? v[j + off] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+}
+
+// GroupNorm partials of W output columns starting at col for this warp's 32 rows, from the
+// bf16-rounded values the next GroupNorm will read (rows outside the image count as zero)
+template <int W>
+__device__ __forceinline__ void gn_partial_cols(const Params& p, const bf16x8* packed, bool valid, int64_t slot,
+                                                int col, int lane) {
+  float s[W], q[W];
+#pragma unroll
+  for (int j = 0; j < W / 8; ++j) {
+    float f[8];
+    unpack8(packed[j], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float r = valid ? f[e] : 0.f;
+      s[j * 8 + e] = r;
+      q[j * 8 + e] = r * r;
+    }
+  }
+  warp_colsum<W>(s, lane);
+  warp_colsum<W>(q, lane);
+  const int c = col + (lane & (W - 1));
+  if (lane < W && c < p.N) p.gn_part[slot * p.N + c] = make_float2(s[0], q[0]);
 }
 
 // ---------------------------------------------------------------- tiling
@@ -700,6 +748,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         if (has_res) mbar_wait(rf, use & 1);
         uint8_t* srow = hbuf + row * (HC * 2);
+        // GroupNorm partials: slot (frame, tile in frame, lane quarter); whole-frame conv tiles only
+        const bool gn_on = p.gn_part != nullptr && !phantom;
+        const int64_t gn_slot = gn_on ? (tm * 4 + q) : 0;   // tm = frame * gn_tpf + tile_in_frame
         auto finish32 = [&](int c) {
           float v[32];
           tmem_ld32(tbase + eh * HC + c, v);
@@ -714,8 +765,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int e = 0; e < 8; ++e) v[j * 8 + e] += f[e];
             }
           }
+          bf16x8 pk[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) sp[j] = pack8(v + 8 * j);
+          for (int j = 0; j < 4; ++j) sp[j] = pk[j] = pack8(v + 8 * j);
+          if (gn_on) gn_partial_cols<32>(p, pk, valid, gn_slot, hn0 + c, lane);
         };
 #pragma unroll 1
         for (int c = 0; c + 32 <= HC; c += 32) finish32(c);
@@ -734,8 +787,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int e = 0; e < 8; ++e) v[j * 8 + e] += f[e];
             }
           }
+          bf16x8 pk[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) sp[j] = pack8(v + 8 * j);
+          for (int j = 0; j < 2; ++j) sp[j] = pk[j] = pack8(v + 8 * j);
+          if (gn_on) gn_partial_cols<16>(p, pk, valid, gn_slot, hn0 + c, lane);
         }
         // accumulator free for the tile after next
         tc_fence_before();
@@ -909,16 +964,32 @@ static int pick_bn(int N) {
 // of `slots` CTAs (pairs) runs ceil(tiles / slots) rounds, each as long as one
 // tile's per-CTA work (128 x BN x K) times a per-width efficiency factor.
 // Pairs and wide tiles win unless they cost whole extra rounds.
-static bool choose_tiling(int N, int64_t tiles_m, bool pair_ok, int* bn) {
+// wide_ok: the 192 / 224 column tiles (CTA pairs, bf16 output, long K) may be used; their
+// last N tile may be partial (OOB B rows load as zeros, stores clip)
+static bool choose_tiling(int N, int64_t tiles_m, bool pair_ok, bool wide_ok, int* bn) {
   // per-unit-work cost by tile width, measured on B200 conv shapes (L0 conv, N = 128..1024):
   // narrower tiles move more operand bytes per flop (N=160 ~1.15x, N=128 ~1.3x of N=256)
-  auto eff = [](int b) { return b >= 256 ? 1.0 : b == 160 ? 1.15 : b == 128 ? 1.3 : 1.6; };
+  auto eff = [](int b) {
+    return b >= 256 ? 1.0 : b == 224 ? 1.04 : b == 192 ? 1.08 : b == 160 ? 1.15 : b == 128 ? 1.3 : 1.6;
+  };
   const int sms = num_sms();
-  int cands[4], nc = 0;
+  int cands[6], nc = 0;
   cands[nc++] = *bn;
   if (N % 256 == 0 && N >= 1024 && *bn != 256) cands[nc++] = 256;
   if (N % 160 == 0 && *bn != 160) cands[nc++] = 160;
   if (N % 128 == 0 && *bn != 128) cands[nc++] = 128;
+  if (wide_ok && pair_ok && N > 256) {
+    cands[nc++] = 224;
+    cands[nc++] = 192;
+  }
+  static const char* bn_env = getenv("SF_GEMM_BN");   // tuning override (same-box A/B)
+  if (bn_env) {
+    const int f = atoi(bn_env);
+    if (f == 256 || f == 160 || f == 128 || f == 64 || ((f == 224 || f == 192) && wide_ok && pair_ok)) {
+      *bn = f;
+      return pair_ok;
+    }
+  }
   double best = 1e300;
   bool best_pair = pair_ok;
   int best_bn = *bn;
@@ -927,6 +998,7 @@ static bool choose_tiling(int N, int64_t tiles_m, bool pair_ok, int* bn) {
     if (pr && !pair_ok) continue;
     for (int c = 0; c < nc; ++c) {
       const int b = cands[c];
+      if (!pr && (b == 224 || b == 192)) continue;
       const int64_t tn = (N + b - 1) / b;
       const int64_t tiles = (pr ? (tiles_m + 1) / 2 : tiles_m) * tn;
       const int64_t slots = pr ? sms / 2 : sms;
@@ -948,6 +1020,15 @@ struct Maps {
 };
 
 }  // namespace tc
+
+// Splits per frame of the epilogue GroupNorm partials (0 = unsupported): 3x3 conv with a bf16
+// output whose frames are whole multiples of the M tile (no tail tiles), x 4 lane quarters.
+int32_t gemm_tc_gn_splits(const sf_gemm_args& a) {
+  if (a.mode != SF_GEMM_CONV3X3 || a.out_fp32 || a.batch != 1) return 0;
+  const int w_t = tc::pow2_floor(a.W < 128 ? a.W : 128), h_t = tc::BM / w_t;
+  if (a.H % h_t) return 0;
+  return ((a.W + w_t - 1) / w_t) * (a.H / h_t) * 4;
+}
 
 bool gemm_tc_supported(const sf_gemm_args& a) {
   if (!a.w_kmajor) return false;
@@ -1049,6 +1130,7 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   p.out = a.out;
   p.out_bstride = a.out_bstride;
   p.out_fp32 = a.out_fp32;
+  p.gn_part = reinterpret_cast<float2*>(a.gn_partial);
   CUtensorMap ma, mb, mat;
   const uint64_t es = 2;
   // CTA pairs (cta_group::2, M = 256) whenever there are two M-tiles to pair up;
@@ -1087,6 +1169,9 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
         p.tiles_m = p.n_main + (int64_t)p.tiles_x * ((a.n_outer + fb - 1) / fb);
       }
     }
+    p.gn_tpf = p.tiles_x * p.tiles_y;
+    SF_CHECK_ARG(!p.gn_part || p.tail_rows == 0, SF_ERR_UNSUPPORTED,
+                 "GroupNorm partials need whole-frame conv tiles (see sf_gemm_gn_splits)");
   } else {
     int n_inner = a.n_inner, n_outer = a.n_outer;
     int64_t ostride = a.a.ostride;
@@ -1148,7 +1233,9 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   // pair must not straddle two batches, i.e. each batch needs an even tile count
   if (a.batch > 1 && a.mode == SF_GEMM_PLAIN && ((int64_t)p.tiles_i * p.tiles_o) % 2) pair = false;
   int BN = pick_bn(a.N);
-  pair = choose_tiling(a.N, p.tiles_m, pair, &BN);
+  // 192/224-wide tiles only for long K: compute-bound convs gain (L1 conv K=17280 N=640: 914 -> 846 us),
+  // memory-bound short-K GEMMs lose (K=320 N=640: 118 -> 131 us in the key step)
+  pair = choose_tiling(a.N, p.tiles_m, pair, !a.out_fp32 && p.taps * p.cblocks >= 12, &BN);
   p.BN = BN;
   p.tiles_n = (a.N + BN - 1) / BN;
   {
@@ -1185,6 +1272,8 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
       if (long_k) {
         switch (BN) {
           case 256: return launch_cfg<256, 5, 1, true>(p, M, st);
+          case 224: return launch_cfg<224, 5, 1, true>(p, M, st);
+          case 192: return launch_cfg<192, 6, 1, true>(p, M, st);
           case 160: return launch_cfg<160, 7, 1, true>(p, M, st);
           case 128: return launch_cfg<128, 8, 1, true>(p, M, st);
           default: return launch_cfg<64, 10, 1, true>(p, M, st);
@@ -1192,6 +1281,8 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
       }
       switch (BN) {
         case 256: return launch_cfg<256, 3, 2, true>(p, M, st);
+        case 224: return launch_cfg<224, 3, 2, true>(p, M, st);
+        case 192: return launch_cfg<192, 4, 2, true>(p, M, st);
         case 160: return launch_cfg<160, 5, 2, true>(p, M, st);
         case 128: return launch_cfg<128, 6, 2, true>(p, M, st);
         default: return launch_cfg<64, 9, 2, true>(p, M, st);
