@@ -93,11 +93,14 @@ EXPORTED = tuple(_PROTOS)
 _lib = None
 
 
-def load(path: str = LIB_PATH) -> C.CDLL:
-    """Load (once) and type the library; raises NativeError if absent."""
+def load(path: str | None = None) -> C.CDLL:
+    """Load (once) and type the library; raises NativeError if absent.
+
+    ``SF_LIB`` names another build of the same library (same-box A/B of kernel variants)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("SF_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise NativeError(f"native library {path} not built; run paper_2411_01171_b200.build.build()")
     try:

@@ -5,6 +5,11 @@
     python -m paper_2411_01171_b200 similarity   [config flags] --out DIR            -> similarity.csv + .json
     python -m paper_2411_01171_b200 search-steps --similarity FILE (--gamma G | --target-count N) --out DIR
                                                                                        -> schedule.json
+    python -m paper_2411_01171_b200 export       [config flags] --out DIR            -> graph.json + weights.slfw
+
+run / compare / similarity take ``--graph graph.json --weights weights.slfw`` (as
+written by ``export`` or by the reference's Graph.save / WeightBundle.save) in
+place of rebuilding the network from the config.
 
 Exit codes: 0 success, 1 runtime error, 2 validation error (the
 message names the failing field).  Every flag is validated before any device
@@ -46,6 +51,30 @@ def _unet_flags(p: argparse.ArgumentParser) -> None:
     p.add_argument("--dtype", default="bfloat16", choices=["bfloat16"],
                    help="device storage type (the device path computes bf16 x bf16 -> fp32)")
     p.add_argument("--out", required=True, help="output directory")
+
+
+def _model_flags(p: argparse.ArgumentParser) -> None:
+    p.add_argument("--graph", help="saved graph JSON (Graph.save) to run instead of the built network")
+    p.add_argument("--weights", help="SLFW weight bundle (WeightBundle.save) for --graph")
+
+
+def _model_files(args):
+    """(graph, weights) loaded from --graph / --weights, or (None, None)."""
+    if (args.graph is None) != (args.weights is None):
+        raise _Usage("--graph and --weights are given together")
+    if args.graph is None:
+        return None, None
+    from .graph import Graph
+    from .weights import WeightBundle
+    try:
+        graph = Graph.load(args.graph)
+    except (OSError, ValueError, KeyError, TypeError) as e:
+        raise _Usage(f"graph: {e}") from None
+    try:
+        weights = WeightBundle.load(args.weights)
+    except (OSError, ValueError, KeyError) as e:
+        raise _Usage(f"weights: {e}") from None
+    return graph, weights
 
 
 def _positive(args, name):
@@ -136,9 +165,10 @@ def cmd_run(args) -> int:
     if keys is not None:
         from .rehash import StepSchedule
         sched = StepSchedule(keys, ucfg.steps)
+    graph, weights = _model_files(args)
     y, rep = run_denoise(DenoiseRunConfig(unet=ucfg, mode=mode, schedule=sched, gamma=gamma,
                                           target_keys=args.target_count, exec_cfg=ex,
-                                          naive_chunk=args.naive_chunk))
+                                          naive_chunk=args.naive_chunk, graph=graph, weights=weights))
     rep.save(os.path.join(out, "run_report.json"))
     if args.save_output:
         np.save(os.path.join(out, "output.npy"), y.data)
@@ -154,10 +184,12 @@ def cmd_compare(args) -> int:
     if ExecMode.NAIVE_CLIP in modes and args.naive_chunk is None:
         raise _Usage("naive-chunk is required when comparing naiveclip")
     ucfg, ex = _unet_cfg(args), _exec_cfg(args)
+    graph, weights = _model_files(args)
     out = _outdir(args.out)
     rows, base = [], None
     for m in modes:
-        y, rep = run_denoise(DenoiseRunConfig(unet=ucfg, mode=m, exec_cfg=ex, naive_chunk=args.naive_chunk))
+        y, rep = run_denoise(DenoiseRunConfig(unet=ucfg, mode=m, exec_cfg=ex, naive_chunk=args.naive_chunk,
+                                              graph=graph, weights=weights))
         if base is None:
             base = y.data
         err = float(np.abs(y.data - base).max() / max(float(np.abs(base).max()), 1e-30))
@@ -177,8 +209,12 @@ def cmd_similarity(args) -> int:
     if args.probe_label not in (None, PROBE_LABEL):
         raise _Usage(f"probe-label: the device path caches {PROBE_LABEL!r} (the rehash probe)")
     ucfg, ex = _unet_cfg(args), _exec_cfg(args)
+    graph, weights = _model_files(args)
+    if graph is not None:
+        from .harness import DenoiseRunConfig, _model_inputs
+        graph, weights = _model_inputs(DenoiseRunConfig(unet=ucfg, graph=graph, weights=weights))
     out = _outdir(args.out)
-    den = Denoiser(ucfg, ex)
+    den = Denoiser(ucfg, ex, graph=graph, weights=weights)
     _, S = den.calibrate(initial_latent(ucfg))
     with open(os.path.join(out, "similarity.csv"), "w") as f:
         f.write(S.export_csv())
@@ -213,11 +249,25 @@ def cmd_search_steps(args) -> int:
     return 0
 
 
+def cmd_export(args) -> int:
+    """Write the config's network as graph.json + weights.slfw (host only, no device work)."""
+    from .unet import build_toy_unet
+    ucfg = _unet_cfg(args)
+    graph, weights = build_toy_unet(ucfg)
+    out = _outdir(args.out)
+    graph.save(os.path.join(out, "graph.json"))
+    weights.save(os.path.join(out, "weights.slfw"))
+    print(json.dumps({"nodes": len(graph.nodes), "weight_entries": len(weights.entries),
+                      "params": int(weights.param_count())}))
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     p = _Parser(prog="python -m paper_2411_01171_b200", description=__doc__.split("\n\n")[0])
     sub = p.add_subparsers(dest="cmd", required=True, parser_class=_Parser)
     r = sub.add_parser("run", help="one denoising run -> run_report.json")
     _unet_flags(r)
+    _model_flags(r)
     r.add_argument("--mode", default=ExecMode.SLICED_LOOP.value)
     r.add_argument("--gamma", type=float)
     r.add_argument("--target-count", type=int)
@@ -227,11 +277,13 @@ def build_parser() -> argparse.ArgumentParser:
     r.set_defaults(fn=cmd_run)
     c = sub.add_parser("compare", help="run several modes, diff their outputs -> compare.json")
     _unet_flags(c)
+    _model_flags(c)
     c.add_argument("--modes", default="reference,slicedloop,pipelined")
     c.add_argument("--naive-chunk", type=int)
     c.set_defaults(fn=cmd_compare)
     s = sub.add_parser("similarity", help="calibration run -> similarity.csv + similarity.json")
     _unet_flags(s)
+    _model_flags(s)
     s.add_argument("--probe-label")
     s.set_defaults(fn=cmd_similarity)
     k = sub.add_parser("search-steps", help="Algorithm A1 on a similarity CSV -> schedule.json")
@@ -240,6 +292,9 @@ def build_parser() -> argparse.ArgumentParser:
     k.add_argument("--target-count", type=int)
     k.add_argument("--out", required=True)
     k.set_defaults(fn=cmd_search_steps)
+    e = sub.add_parser("export", help="write the config's network -> graph.json + weights.slfw")
+    _unet_flags(e)
+    e.set_defaults(fn=cmd_export)
     return p
 
 

@@ -32,6 +32,7 @@ from .rehash import (SimilarityMap, StepSchedule, gamma_for_target, gram_partial
                      op_count_report, similarity_from_gram)
 from .tensor import Tensor5D
 from .unet import PROBE_LABEL, UNetConfig, build_toy_unet, sinusoidal_step_embedding
+from .weights import WeightBundle
 
 # kernels launched per C-ABI call (for the gpu_launches count of the bench)
 KERNELS_PER_CALL = {"sf_group_norm_stats": 2, "sf_dot3_bf16": 2, "sf_gram_bf16": 3}
@@ -221,6 +222,10 @@ class DenoiseRunConfig:
     target_keys: int | None = None
     exec_cfg: ExecConfig = field(default_factory=ExecConfig)
     naive_chunk: int | None = None      # NaiveClip(chunk) frames per independent clip
+    # a saved graph / SLFW weight bundle instead of build_toy_unet(unet) (graph.py:127-169,
+    # kernels.py:397-465); both must describe ``unet``'s network
+    graph: Graph | None = None
+    weights: WeightBundle | None = None
 
 
 @dataclass
@@ -252,6 +257,23 @@ class RunReport:
             json.dump(self.to_json_dict(), f, indent=1, sort_keys=True)
 
 
+def _model_inputs(cfg: DenoiseRunConfig):
+    """(graph, weights) of a run: both given, or (None, None) for build_toy_unet(cfg.unet)."""
+    if (cfg.graph is None) != (cfg.weights is None):
+        raise InvalidParam("a saved graph and its weight bundle are given together")
+    if cfg.graph is None:
+        return None, None
+    want = cfg.unet.input_shape()
+    got = cfg.graph.inputs.get("x")
+    if got is None or tuple(got) != tuple(want):
+        raise InvalidParam(f"graph input x {tuple(got) if got is not None else None} does not match the "
+                           f"config's latent {tuple(want)}")
+    for n in cfg.graph.nodes.values():
+        if n.param_ref is not None:
+            cfg.weights.get(n.param_ref)          # InvalidParam names a missing entry
+    return cfg.graph, cfg.weights
+
+
 def run_denoise(cfg: DenoiseRunConfig) -> tuple[Tensor5D, RunReport]:
     """Full or rehash denoising run on the device.
 
@@ -268,7 +290,8 @@ def run_denoise(cfg: DenoiseRunConfig) -> tuple[Tensor5D, RunReport]:
     x0 = initial_latent(ucfg)
     if mode is ExecMode.NAIVE_CLIP:
         return _run_naive_clip(cfg, ucfg, K, ex, x0)
-    den = Denoiser(ucfg, ex, K=K)
+    graph, weights = _model_inputs(cfg)
+    den = Denoiser(ucfg, ex, graph=graph, weights=weights, K=K)
     torch.cuda.reset_peak_memory_stats()
     t0 = time.perf_counter()
     schedule, sim = cfg.schedule, None
@@ -303,7 +326,9 @@ def _run_naive_clip(cfg: DenoiseRunConfig, ucfg: UNetConfig, K: int, ex: ExecCon
     if cfg.naive_chunk is None:
         raise InvalidParam("naiveclip needs naive_chunk")
     chunks = naive_clip_chunks(ucfg.frames, cfg.naive_chunk)
-    graph, w64 = build_toy_unet(ucfg)
+    graph, w64 = _model_inputs(cfg)
+    if graph is None:
+        graph, w64 = build_toy_unet(ucfg)
     torch.cuda.reset_peak_memory_stats()
     t0 = time.perf_counter()
     dens: dict[int, Denoiser] = {}

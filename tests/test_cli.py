@@ -56,3 +56,39 @@ def test_module_entry_point(tmp_path):
     r = subprocess.run([sys.executable, "-m", "paper_2411_01171_b200", "run", "--spatial-k", "0",
                         "--out", str(tmp_path)], cwd=ROOT, capture_output=True, text=True)
     assert r.returncode == 2 and "spatial-k" in r.stderr
+
+
+SMALL = ["--frames", "4", "--height", "16", "--width", "16", "--base-channels", "8", "--norm-groups", "4",
+         "--channels", "4", "--steps", "5"]
+
+
+def test_export_round_trip(tmp_path):
+    """export writes the config's network as graph.json + weights.slfw (graph.py:127-169,
+    kernels.py:397-465); both load back to the built graph and the fp32 weights."""
+    from paper_2411_01171_b200.graph import Graph
+    from paper_2411_01171_b200.unet import UNetConfig, build_toy_unet
+    from paper_2411_01171_b200.weights import WeightBundle
+    assert main(["export", *SMALL, "--out", str(tmp_path)]) == 0
+    g, w = build_toy_unet(UNetConfig(frames=4, height=16, width=16, base_channels=8, norm_groups=4, channels=4,
+                                     steps=5))
+    g2 = Graph.load(tmp_path / "graph.json")
+    assert g2.to_json_dict() == g.to_json_dict()
+    w2 = WeightBundle.load(tmp_path / "weights.slfw")
+    assert sorted(w2.entries) == sorted(w.entries)
+    for k, arrs in w.entries.items():
+        for n, a in arrs.items():
+            assert np.array_equal(w2.get(k)[n], a.astype(np.float32))
+
+
+def test_model_file_flags_validated(tmp_path, capsys):
+    assert main(["export", *SMALL, "--out", str(tmp_path)]) == 0
+    g, wf = str(tmp_path / "graph.json"), str(tmp_path / "weights.slfw")
+    assert main(["run", *SMALL, "--graph", g, "--out", str(tmp_path / "r")]) == 2         # weights missing
+    assert "together" in capsys.readouterr().err
+    assert main(["run", *SMALL, "--graph", str(tmp_path / "nope.json"), "--weights", wf,
+                 "--out", str(tmp_path / "r")]) == 2
+    assert main(["run", *SMALL, "--graph", g, "--weights", g, "--out", str(tmp_path / "r")]) == 2  # bad magic
+    # a graph for another latent shape is rejected before any device work
+    assert main(["run", "--frames", "8", *SMALL[2:], "--graph", g, "--weights", wf,
+                 "--out", str(tmp_path / "r")]) == 2
+    assert "does not match" in capsys.readouterr().err

@@ -47,3 +47,21 @@ def test_similarity_then_search(tmp_path):
     assert main(["search-steps", "--similarity", str(tmp_path / "similarity.csv"), "--target-count", "3",
                  "--out", str(tmp_path)]) == 0
     assert len(json.loads((tmp_path / "schedule.json").read_text())["key_steps"]) == 3
+
+
+def test_run_from_exported_model(tmp_path):
+    """run --graph/--weights (exported files) == run_denoise on the same graph with the fp32 bundle in
+    memory (bit-exact), and matches the fp64-built network within the bf16 storage tolerance."""
+    import numpy as np
+    from paper_2411_01171_b200.harness import DenoiseRunConfig, run_denoise
+    from paper_2411_01171_b200.unet import UNetConfig, build_toy_unet
+    assert main(["export", *SMALL, "--out", str(tmp_path / "m")]) == 0
+    assert main(["run", *SMALL, "--graph", str(tmp_path / "m" / "graph.json"), "--weights",
+                 str(tmp_path / "m" / "weights.slfw"), "--save-output", "--out", str(tmp_path / "f")]) == 0
+    y_file = np.load(tmp_path / "f" / "output.npy")
+    ucfg = UNetConfig(frames=4, height=16, width=16, base_channels=8, norm_groups=4, channels=4, steps=5)
+    g, w = build_toy_unet(ucfg)
+    y32, _ = run_denoise(DenoiseRunConfig(unet=ucfg, graph=g, weights=w.astype(np.float32)))
+    assert np.array_equal(y_file, y32.data)
+    y64, _ = run_denoise(DenoiseRunConfig(unet=ucfg))
+    assert float(np.abs(y_file - y64.data).max() / np.abs(y64.data).max()) <= 5e-3
