@@ -32,6 +32,9 @@ def test_builder_and_grouping_match_reference(golden, name, cfg, sk):
     graph, w = build_toy_unet(cfg)
     assert graph.topo_order() == ref["topo"]
     assert json.loads(json.dumps(graph.to_json_dict())) == ref["graph_json"]
+    # the reference-written JSON loads here (cli --graph) and describes the same graph
+    from paper_2411_01171_b200.graph import Graph
+    assert Graph.from_json_dict(ref["graph_json"]).to_json_dict() == graph.to_json_dict()
     gg = group_operators(graph, sk, default_temporal_config(cfg.height, cfg.width))
     assert [[k, r] for k, r in gg.schedule] == ref["schedule"]
     assert json.loads(json.dumps(grouped_graph_report(gg))) == ref["report"]
