@@ -410,8 +410,36 @@ struct SmemLayout {
   static constexpr int OUT_TILE = BM * BN * 2;
   // EPI staging buffers: 0 = direct stores; 1/2 = bf16 tiles; 3 = two 128 x 32 fp32 chunks (SW128)
   static constexpr int OUT_BYTES = EPI == 3 ? 4 * F32_CHUNK_BYTES : EPI * OUT_TILE;
-  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + OUT_BYTES + 256 /*barriers*/;
+  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + OUT_BYTES + 512 /*barriers*/;
 };
+
+// TMEM accumulator buffers (<= TC_NACC_MAX BN-column tiles in the 512 columns).  3-4 buffers
+// measured neutral (<= 2 % on K = 320 GEMMs): the MMA warp gets its buffer back right after the
+// commit (tools/gemm_trace.py); it waits on operand stages, i.e. the L2 throughput cap
+#ifndef TC_NACC_MAX
+#define TC_NACC_MAX 2
+#endif
+template <int BN>
+constexpr int nacc() {
+  return 512 / BN >= TC_NACC_MAX ? TC_NACC_MAX : (512 / BN < 2 ? 2 : 512 / BN);
+}
+
+// -DTC_TRACE (tuning builds only): SM-clock stamps of CTA 0's pipeline events, per role
+#ifdef TC_TRACE
+__device__ unsigned long long g_tc_trace[4][4096];
+__device__ unsigned int g_tc_trace_n[4];
+#define TC_TR(role, code)                                                                 \
+  do {                                                                                    \
+    if (blockIdx.x == 0) {                                                                \
+      const unsigned i_ = g_tc_trace_n[role]++;                                           \
+      if (i_ < 4096) g_tc_trace[role][i_] = ((unsigned long long)clock64() << 4) | (code); \
+    }                                                                                     \
+  } while (0)
+#else
+#define TC_TR(role, code) \
+  do {                    \
+  } while (0)
+#endif
 
 // PAIR: CTA pairs (cluster of 2) run tcgen05.mma.cta_group::2 with M = 256:
 // CTA rank r owns M-tile 2*pair + r (its A rows, TMEM accumulator and epilogue)
@@ -434,15 +462,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sOut = smem + STAGES * L::STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sOut + L::OUT_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint64_t* res_full = tempty + 2;    // [2 buffers][2 halves] residual half-tile landed
+  constexpr int NACC = nacc<BN>();
+  uint64_t* tfull = empty + STAGES;   // [NACC]
+  uint64_t* tempty = tfull + NACC;    // [NACC]
+  uint64_t* res_full = tempty + NACC; // [2 buffers][2 halves] residual half-tile landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 4);
   const bool has_res = TMA_EPI && p.res.ptr != nullptr;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
-                                 : (2 * BN <= 256) ? 256 : 512;
+  constexpr uint32_t TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
+                                 : (NACC * BN <= 256) ? 256 : 512;
+  static_assert(NACC * BN <= 512, "TMEM accumulators");
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&mapA);
@@ -452,7 +482,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NACC; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], PAIR ? 16 : 8);  // one arrive per epilogue warp (of both CTAs)
     }
@@ -514,6 +544,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int it = 0; it < kiters; ++it) {
           const int tap = it / p.cblocks, cb = it % p.cblocks;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (lane == 0) TC_TR(0, 1);
           void* dA = sA + stage * L::A_BYTES;
           void* dB = sB + stage * L::B_BYTES;
           if constexpr (PAIR) {
@@ -563,10 +594,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t acc_phase = 0;
       for (int64_t tile = t_first; tile < n_tiles; tile += t_step) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (lane == 0) TC_TR(1, 2);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (int it = 0; it < kiters; ++it) {
           mbar_wait(&full[stage], phase);
+          if (lane == 0) TC_TR(1, 3);
           tc_fence_after();
           const uint64_t ad = make_sdesc(smem_u32(sA + stage * L::A_BYTES));
           const uint64_t bd = make_sdesc(smem_u32(sB + stage * L::B_BYTES));
@@ -585,7 +618,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (PAIR) umma_commit_pair(&tfull[acc]);
         else umma_commit(&tfull[acc]);
-        if (++acc == 2) {
+        if (lane == 0) TC_TR(1, 4);
+        if (++acc == NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -688,7 +722,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (PAIR) arrive_remote(tempty_l + acc * 8);
           else mbar_arrive(&tempty[acc]);
         }
-        if (++acc == 2) {
+        if (++acc == NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -745,6 +779,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         mbar_wait(&tfull[acc], acc_phase);
+        if (hleader) TC_TR(2 + eh, 5);
         tc_fence_after();
         if (has_res) mbar_wait(rf, use & 1);
         uint8_t* srow = hbuf + row * (HC * 2);
@@ -799,6 +834,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (PAIR) arrive_remote(tempty_l + acc * 8);
           else mbar_arrive(&tempty[acc]);
         }
+        if (hleader) TC_TR(2 + eh, 6);
         // my half-tile complete -> my leader stores it with TMA (OOB rows/cols are clipped)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         half_sync();
@@ -812,9 +848,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           // the other buffer's store (tile t-1) must drain before it is refilled
           if (EPI == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          TC_TR(2 + eh, 7);
         }
         if (EPI == 2) half_sync();
-        if (++acc == 2) {
+        if (hleader) TC_TR(2 + eh, 8);
+        if (++acc == NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -889,7 +927,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (PAIR) arrive_remote(tempty_l + acc * 8);
         else mbar_arrive(&tempty[acc]);
       }
-      if (++acc == 2) {
+      if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -1020,6 +1058,20 @@ struct Maps {
 };
 
 }  // namespace tc
+
+#ifdef TC_TRACE
+// tuning builds only (not in the public header): copy out and reset CTA 0's event trace
+extern "C" int32_t sf_debug_gemm_trace(unsigned long long* host, int32_t n_per_role, uint32_t* counts) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(counts, tc::g_tc_trace_n, sizeof(unsigned) * 4);
+  for (int r = 0; r < 4; ++r)
+    cudaMemcpyFromSymbol(host + (size_t)r * n_per_role, tc::g_tc_trace, sizeof(unsigned long long) * n_per_role,
+                         sizeof(unsigned long long) * 4096 * r);
+  const unsigned zero[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(tc::g_tc_trace_n, zero, sizeof(zero));
+  return 0;
+}
+#endif
 
 // Splits per frame of the epilogue GroupNorm partials (0 = unsupported): 3x3 conv with a bf16
 // output whose frames are whole multiples of the M tile (no tail tiles), x 4 lane quarters.
@@ -1267,7 +1319,10 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
     // epilogue (residual prefetch + TMA store) overlaps the next tile
     // (>= 12 K blocks measured on B200: K=1280 plain 49.5 -> 42.8 us, K=960 tconv -1.6 %; at
     // 10 blocks (K=640) double staging still wins)
-    const bool long_k = p.taps * p.cblocks >= 12;
+#ifndef TC_LONGK_MIN
+#define TC_LONGK_MIN 12
+#endif
+    const bool long_k = p.taps * p.cblocks >= TC_LONGK_MIN;
     if (pair) {
       if (long_k) {
         switch (BN) {
