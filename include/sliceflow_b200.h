@@ -96,9 +96,6 @@ typedef struct {
   int64_t out_bstride;
   int32_t out_fp32;      /* 1: fp32 output, 0: bf16 */
   int32_t backend;       /* 0 auto, 1 force mma.sync path, 2 force tcgen05 path */
-  float* gn_partial;     /* optional (NULL = off): GroupNorm partial sums of the bf16 output,
-                            fp32 (sum, sum of squares) per [frame][split][N]; only where
-                            sf_gemm_gn_splits() > 0, which is the split count per frame */
 } sf_gemm_args;
 
 /* ---- GEMM core: conv2d / temporal_conv / linear / attention projections ---- */
@@ -107,10 +104,6 @@ typedef struct {
 sf_status sf_gemm(const sf_gemm_args* args, void* stream);
 /* Which backend sf_gemm would pick (1 = mma.sync, 2 = tcgen05/TMA). */
 int32_t sf_gemm_backend(const sf_gemm_args* args);
-/* Splits per frame of the GroupNorm partial sums sf_gemm can write from its epilogue
- * (gn_partial), or 0 when this launch cannot (only 3x3 conv on the tcgen05 path with
- * whole-frame tiles and a bf16 output). */
-int32_t sf_gemm_gn_splits(const sf_gemm_args* args);
 
 /* ---- normalisation (kernels.py:228-253) ---- */
 /* GroupNorm statistics per (frame, group) over (C/groups channels x n_inner rows):
@@ -119,11 +112,6 @@ int32_t sf_gemm_gn_splits(const sf_gemm_args* args);
 int64_t sf_group_norm_workspace(int32_t frames, int32_t n_inner, int32_t C);
 sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
                               float eps, void* work, float* mean, float* rstd, void* stream);
-/* mean / rstd from the fp32 (sum, sum of squares) partials a GEMM epilogue wrote
- * ([frames][splits][C], see sf_gemm_gn_splits); count = elements per (frame, group).
- * Fixed-order fp64 combination. */
-sf_status sf_group_norm_finalize(const float* partial, int32_t frames, int32_t splits, int32_t C, int32_t groups,
-                                 float eps, int64_t count, float* mean, float* rstd, void* stream);
 /* y = act((x - mean) * rstd * gamma + beta), per (frame, group) stats. */
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C,
                               int32_t groups, const float* mean, const float* rstd, const float* gamma,

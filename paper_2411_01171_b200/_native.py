@@ -40,7 +40,6 @@ class GemmArgs(C.Structure):
         ("res", View), ("res_bstride", i64),
         ("out", View), ("out_bstride", i64),
         ("out_fp32", i32), ("backend", i32),
-        ("gn_partial", vp),
     ]
 
 
@@ -51,8 +50,6 @@ ACT_NONE, ACT_SILU = 0, 1
 _PROTOS = {
     "sf_gemm": [C.POINTER(GemmArgs), vp],
     "sf_gemm_backend": [C.POINTER(GemmArgs)],
-    "sf_gemm_gn_splits": [C.POINTER(GemmArgs)],
-    "sf_group_norm_finalize": [vp, i32, i32, i32, i32, f32, i64, vp, vp, vp],
     "sf_group_norm_workspace": [i32, i32, i32],
     "sf_group_norm_stats": [View, i32, i32, i32, i32, f32, vp, vp, vp, vp],
     "sf_group_norm_apply": [View, View, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp],

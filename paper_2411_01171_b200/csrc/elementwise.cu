@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_i
   }
 }
 
-// mean / rstd from per-split (sum, sum sq) partials [frame][split][C] (double2 from
-// gn_partial_kernel, float2 from a GEMM epilogue).  Block = (frame, a run of whole groups):
+// mean / rstd from the per-split (sum, sum sq) fp64 partials [frame][split][C] of
+// gn_partial_kernel.  Block = (frame, a run of whole groups):
 // one thread per channel sums its splits with independent loads in flight (the old
 // warp-per-group walk was a chain of dependent L2 round trips), then one warp per group
 // adds its channels.  Fixed summation order: bitwise reproducible.
@@ -1192,15 +1192,6 @@ sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int3
   launch_gn_finalize((const double2*)work, frames, splits, C, groups, (int64_t)n_inner * (C / groups), eps, mean,
                      rstd, st);
   return launch_status("sf_group_norm_stats");
-}
-
-sf_status sf_group_norm_finalize(const float* partial, int32_t frames, int32_t splits, int32_t C, int32_t groups,
-                                 float eps, int64_t count, float* mean, float* rstd, void* stream) {
-  SF_CHECK_ARG(partial && mean && rstd && frames >= 1 && splits >= 1 && groups >= 1 && C % groups == 0 && count > 0,
-               SF_ERR_PARAM, "bad GroupNorm finalize arguments");
-  launch_gn_finalize(reinterpret_cast<const float2*>(partial), frames, splits, C, groups, count, eps, mean, rstd,
-                     (cudaStream_t)stream);
-  return launch_status("sf_group_norm_finalize");
 }
 
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,

@@ -7,7 +7,6 @@ namespace sf {
 sf_status gemm_mma_launch(const sf_gemm_args& p, cudaStream_t st);
 bool gemm_tc_supported(const sf_gemm_args& p);
 sf_status gemm_tc_launch(const sf_gemm_args& p, cudaStream_t st);
-int32_t gemm_tc_gn_splits(const sf_gemm_args& p);
 }  // namespace sf
 
 using namespace sf;
@@ -38,18 +37,11 @@ extern "C" int32_t sf_gemm_backend(const sf_gemm_args* a) {
   return gemm_tc_supported(*a) ? 2 : 1;
 }
 
-extern "C" int32_t sf_gemm_gn_splits(const sf_gemm_args* a) {
-  if (sf_gemm_backend(a) != 2) return 0;
-  return gemm_tc_gn_splits(*a);
-}
-
 extern "C" sf_status sf_gemm(const sf_gemm_args* a, void* stream) {
   sf_status s = validate(a);
   if (s != SF_OK) return s;
   int be = sf_gemm_backend(a);
   SF_CHECK_ARG(be != 0, SF_ERR_UNSUPPORTED, "forced tcgen05 backend cannot take this shape");
-  SF_CHECK_ARG(!a->gn_partial || (be == 2 && gemm_tc_gn_splits(*a) > 0), SF_ERR_UNSUPPORTED,
-               "GroupNorm partials are only produced where sf_gemm_gn_splits() > 0");
   if (be == 2) return gemm_tc_launch(*a, (cudaStream_t)stream);
   return gemm_mma_launch(*a, (cudaStream_t)stream);
 }

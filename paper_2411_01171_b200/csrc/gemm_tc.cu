@@ -60,9 +60,6 @@ struct Params {
   int64_t out_bstride;
   int out_fp32;
   // optional GroupNorm partial sums of the bf16 output (conv, whole-frame tiles):
-  // gn_part[((frame * gn_tpf + tile_in_frame) * 4 + lane_quarter) * N + col] = (sum, sum sq)
-  float2* gn_part;
-  int gn_tpf;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -324,50 +321,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-}
-
-// Column sums over a warp's 32 rows: on entry lane l holds row l's values v[0..W), on exit
-// v[0] of lane l is the sum of column l over the 32 rows (W = 32), or -- for W = 16 -- of
-// column l & 15 (lanes l and l ^ 16 agree).  31 (resp. 16 + 15) shuffles, fixed order.
-template <int W>
-__device__ __forceinline__ void warp_colsum(float* v, int lane) {
-  if constexpr (W == 16) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], 16);
-  }
-#pragma unroll
-  for (int off = W / 2; off >= 1; off >>= 1) {
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int j = 0; j < off; ++j) {
-      const float send = upper ? v[j] : v[j + off];
-      const float keep = upper ? v[j + off] : v[j];
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-}
-
-// GroupNorm partials of W output columns starting at col for this warp's 32 rows, from the
-// bf16-rounded values the next GroupNorm will read (rows outside the image count as zero)
-template <int W>
-__device__ __forceinline__ void gn_partial_cols(const Params& p, const bf16x8* packed, bool valid, int64_t slot,
-                                                int col, int lane) {
-  float s[W], q[W];
-#pragma unroll
-  for (int j = 0; j < W / 8; ++j) {
-    float f[8];
-    unpack8(packed[j], f);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float r = valid ? f[e] : 0.f;
-      s[j * 8 + e] = r;
-      q[j * 8 + e] = r * r;
-    }
-  }
-  warp_colsum<W>(s, lane);
-  warp_colsum<W>(q, lane);
-  const int c = col + (lane & (W - 1));
-  if (lane < W && c < p.N) p.gn_part[slot * p.N + c] = make_float2(s[0], q[0]);
 }
 
 // ---------------------------------------------------------------- tiling
@@ -783,9 +736,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         if (has_res) mbar_wait(rf, use & 1);
         uint8_t* srow = hbuf + row * (HC * 2);
-        // GroupNorm partials: slot (frame, tile in frame, lane quarter); whole-frame conv tiles only
-        const bool gn_on = p.gn_part != nullptr && !phantom;
-        const int64_t gn_slot = gn_on ? (tm * 4 + q) : 0;   // tm = frame * gn_tpf + tile_in_frame
         auto finish32 = [&](int c) {
           float v[32];
           tmem_ld32(tbase + eh * HC + c, v);
@@ -800,10 +750,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int e = 0; e < 8; ++e) v[j * 8 + e] += f[e];
             }
           }
-          bf16x8 pk[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) sp[j] = pk[j] = pack8(v + 8 * j);
-          if (gn_on) gn_partial_cols<32>(p, pk, valid, gn_slot, hn0 + c, lane);
+          for (int j = 0; j < 4; ++j) sp[j] = pack8(v + 8 * j);
         };
 #pragma unroll 1
         for (int c = 0; c + 32 <= HC; c += 32) finish32(c);
@@ -822,10 +770,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int e = 0; e < 8; ++e) v[j * 8 + e] += f[e];
             }
           }
-          bf16x8 pk[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) sp[j] = pk[j] = pack8(v + 8 * j);
-          if (gn_on) gn_partial_cols<16>(p, pk, valid, gn_slot, hn0 + c, lane);
+          for (int j = 0; j < 2; ++j) sp[j] = pack8(v + 8 * j);
         }
         // accumulator free for the tile after next
         tc_fence_before();
@@ -1073,15 +1019,6 @@ extern "C" int32_t sf_debug_gemm_trace(unsigned long long* host, int32_t n_per_r
 }
 #endif
 
-// Splits per frame of the epilogue GroupNorm partials (0 = unsupported): 3x3 conv with a bf16
-// output whose frames are whole multiples of the M tile (no tail tiles), x 4 lane quarters.
-int32_t gemm_tc_gn_splits(const sf_gemm_args& a) {
-  if (a.mode != SF_GEMM_CONV3X3 || a.out_fp32 || a.batch != 1) return 0;
-  const int w_t = tc::pow2_floor(a.W < 128 ? a.W : 128), h_t = tc::BM / w_t;
-  if (a.H % h_t) return 0;
-  return ((a.W + w_t - 1) / w_t) * (a.H / h_t) * 4;
-}
-
 bool gemm_tc_supported(const sf_gemm_args& a) {
   if (!a.w_kmajor) return false;
   if (a.cin % 64) return false;
@@ -1182,7 +1119,6 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   p.out = a.out;
   p.out_bstride = a.out_bstride;
   p.out_fp32 = a.out_fp32;
-  p.gn_part = reinterpret_cast<float2*>(a.gn_partial);
   CUtensorMap ma, mb, mat;
   const uint64_t es = 2;
   // CTA pairs (cta_group::2, M = 256) whenever there are two M-tiles to pair up;
@@ -1221,9 +1157,6 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
         p.tiles_m = p.n_main + (int64_t)p.tiles_x * ((a.n_outer + fb - 1) / fb);
       }
     }
-    p.gn_tpf = p.tiles_x * p.tiles_y;
-    SF_CHECK_ARG(!p.gn_part || p.tail_rows == 0, SF_ERR_UNSUPPORTED,
-                 "GroupNorm partials need whole-frame conv tiles (see sf_gemm_gn_splits)");
   } else {
     int n_inner = a.n_inner, n_outer = a.n_outer;
     int64_t ostride = a.a.ostride;

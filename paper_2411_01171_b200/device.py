@@ -113,7 +113,7 @@ class DeviceWeights:
 def gemm_args(*, mode, n_outer, n_inner, cin, n, a: Rows, w: torch.Tensor, w_ld=None, w_kmajor=True,
               out: Rows, out_fp32=False, bias=None, rowbias=None, rowbias_stride=0, act=N.ACT_NONE,
               res: Rows | None = None, H=0, W=0, T=0, batch=1, a_bstride=0, w_bstride=0, out_bstride=0,
-              res_bstride=0, alpha=1.0, backend=0, w_ptr=None, gn_partial: torch.Tensor | None = None):
+              res_bstride=0, alpha=1.0, backend=0, w_ptr=None):
     args = N.GemmArgs()
     args.mode, args.n_outer, args.n_inner = mode, n_outer, n_inner
     args.H, args.W, args.T = H, W, T
@@ -133,7 +133,6 @@ def gemm_args(*, mode, n_outer, n_inner, cin, n, a: Rows, w: torch.Tensor, w_ld=
     args.out, args.out_bstride = out.view(), out_bstride
     args.out_fp32 = 1 if out_fp32 else 0
     args.backend = backend
-    args.gn_partial = gn_partial.data_ptr() if gn_partial is not None else None
     return args
 
 
@@ -150,38 +149,13 @@ class Epilogue:
         self.act, self.rowbias, self.res = act, rowbias, res
 
 
-def _conv_args(x, y, frames, H, W, cin, cout, prm, epi, backend, out_fp32, gn_partial=None):
+def conv2d(stream, x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue, backend=0, out_fp32=False):
+    """3x3 conv (kernels.py:181-201) as an implicit GEMM."""
     if "w" not in prm:
         raise ShapeMismatch(f"conv2d with cin={cin} needs the small-channel path")
-    return gemm_args(mode=N.GEMM_CONV3X3, n_outer=frames, n_inner=H * W, H=H, W=W, cin=cin, n=cout, a=x,
-                     w=prm["w"], out=y, out_fp32=out_fp32, bias=prm["bias"], rowbias=epi.rowbias, act=epi.act,
-                     res=epi.res, backend=backend, gn_partial=gn_partial)
-
-
-def conv2d(stream, x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue, backend=0, out_fp32=False,
-           gn_partial: torch.Tensor | None = None):
-    """3x3 conv (kernels.py:181-201).  ``gn_partial``: also write the per-tile GroupNorm partial sums of the
-    output (the next op's statistics, finished by group_norm_finalize); only where conv_gn_splits() > 0."""
-    args = _conv_args(x, y, frames, H, W, cin, cout, prm, epi, backend, out_fp32, gn_partial)
-    N.call("sf_gemm", args, stream)
-    return args
-
-
-def conv_gn_splits(x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue, backend=0) -> int:
-    """Partial-sum slots per frame the conv epilogue writes for the next GroupNorm (0: not available)."""
-    return N.query("sf_gemm_gn_splits", _conv_args(x, y, frames, H, W, cin, cout, prm, epi, backend, False))
-
-
-def conv_gn_splits_bound(H, W) -> int:
-    """Upper bound of conv_gn_splits() for an H x W frame (scratch sizing; mirrors gemm_tc_gn_splits)."""
-    w_t = 1 << (min(W, 128).bit_length() - 1)
-    h_t = 128 // w_t
-    return 0 if H % h_t else -(-W // w_t) * (H // h_t) * 4
-
-
-def group_norm_finalize(stream, partial: torch.Tensor, frames, splits, C, groups, eps, count, mean, rstd):
-    N.call("sf_group_norm_finalize", partial.data_ptr(), frames, splits, C, groups, eps, count, mean.data_ptr(),
-           rstd.data_ptr(), stream)
+    return gemm(stream, mode=N.GEMM_CONV3X3, n_outer=frames, n_inner=H * W, H=H, W=W, cin=cin, n=cout, a=x,
+                w=prm["w"], out=y, out_fp32=out_fp32, bias=prm["bias"], rowbias=epi.rowbias, act=epi.act,
+                res=epi.res, backend=backend)
 
 
 TAPWISE_MAX_COUT = 16

@@ -198,60 +198,6 @@ def test_layer_norm_widths(C):
     assert rel(y, ref) <= 1e-2
 
 
-@pytest.mark.parametrize("F_,H,W,C,Co,G", [(3, 72, 128, 64, 320, 32), (2, 36, 64, 320, 640, 32),
-                                          (2, 16, 16, 64, 64, 4), (2, 8, 72, 64, 128, 8), (3, 4, 32, 64, 256, 32)])
-def test_conv_epilogue_groupnorm_partials(F_, H, W, C, Co, G):
-    """GroupNorm statistics from the conv GEMM epilogue (gn_partial + sf_group_norm_finalize) equal
-    sf_group_norm_stats on the same bf16 output."""
-    torch.manual_seed(8)
-    x = rnd(F_, H, W, C)
-    w = rnd(Co, C, 3, 3, scale=(9 * C) ** -0.5)
-    wk = w.permute(0, 2, 3, 1).reshape(Co, 9 * C).contiguous()
-    bias = torch.randn(Co, device=dev)
-    out = torch.empty(F_ * H * W, Co, dtype=torch.bfloat16, device=dev)
-    st = torch.cuda.current_stream().cuda_stream
-    args = N.GemmArgs()
-    args.mode, args.n_outer, args.n_inner, args.H, args.W, args.T = N.GEMM_CONV3X3, F_, H * W, H, W, 0
-    args.cin, args.N, args.batch = C, Co, 1
-    args.a, args.a_bstride = Rows(x.view(-1, C), 0, H * W).view(), 0
-    args.w, args.w_kmajor, args.w_ld, args.w_bstride = wk.data_ptr(), 1, wk.stride(0), 0
-    args.alpha, args.bias, args.rowbias, args.rowbias_stride, args.act = 1.0, bias.data_ptr(), None, 0, N.ACT_NONE
-    args.res, args.res_bstride = N.NULL_VIEW, 0
-    args.out, args.out_bstride, args.out_fp32, args.backend = Rows(out, 0, H * W).view(), 0, 0, 2
-    splits = N.query("sf_gemm_gn_splits", args)
-    assert splits > 0
-    part = torch.zeros(F_ * splits * Co * 2, dtype=torch.float32, device=dev)
-    args.gn_partial = part.data_ptr()
-    N.call("sf_gemm", args, st)
-    mean = torch.empty(F_ * G, device=dev)
-    rstd = torch.empty_like(mean)
-    N.call("sf_group_norm_finalize", part.data_ptr(), F_, splits, Co, G, 1e-5, H * W * (Co // G), mean.data_ptr(),
-           rstd.data_ptr(), st)
-    work = torch.zeros(N.query("sf_group_norm_workspace", F_, H * W, Co), dtype=torch.uint8, device=dev)
-    m2 = torch.empty_like(mean)
-    r2 = torch.empty_like(mean)
-    N.call("sf_group_norm_stats", Rows(out, 0, H * W).view(), F_, H * W, Co, G, 1e-5, work.data_ptr(),
-           m2.data_ptr(), r2.data_ptr(), st)
-    torch.cuda.synchronize()
-    assert float((mean - m2).abs().max()) <= 1e-4 * float(m2.abs().max()) + 1e-5
-    assert float(((rstd - r2) / r2).abs().max()) <= 1e-4
-
-
-def test_conv_epilogue_groupnorm_unsupported_with_tail_tiles():
-    args = N.GemmArgs()
-    args.mode, args.n_outer, args.n_inner, args.H, args.W = N.GEMM_CONV3X3, 2, 9 * 16, 9, 16
-    args.cin, args.N, args.batch = 64, 64, 1
-    x = rnd(2 * 9 * 16, 64)
-    wk = rnd(64, 9 * 64)
-    out = torch.empty(2 * 9 * 16, 64, dtype=torch.bfloat16, device=dev)
-    args.a = Rows(x, 0, 144).view()
-    args.w, args.w_kmajor, args.w_ld = wk.data_ptr(), 1, wk.stride(0)
-    args.alpha, args.act = 1.0, N.ACT_NONE
-    args.res = N.NULL_VIEW
-    args.out, args.out_fp32, args.backend = Rows(out, 0, 144).view(), 0, 2
-    assert N.query("sf_gemm_gn_splits", args) == 0
-
-
 @pytest.mark.parametrize("case", ["conv640", "conv640_long", "tconv640", "plain960", "plain640"])
 def test_wide_pair_tiles(case):
     """Shapes the tiling model gives 224- or 192-column CTA-pair tiles (N = 640: 224 + 224 + a partial
