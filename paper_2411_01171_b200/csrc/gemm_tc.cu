@@ -330,9 +330,10 @@ struct MTile {
   int tail;        // CONV: a tail tile (rows tail_y0.. of tail_fb frames starting at f)
 };
 
+template <bool CONV>
 __device__ __forceinline__ MTile decode_m(const Params& p, int64_t tm) {
   MTile t{};
-  if (p.mode == SF_GEMM_CONV3X3) {
+  if (CONV) {
     if (p.tail_rows && tm >= p.n_main) {
       const int64_t tt = tm - p.n_main;
       t.x0 = (int)(tt % p.tiles_x) * p.w_t;
@@ -398,7 +399,9 @@ __device__ unsigned int g_tc_trace_n[4];
 // CTA rank r owns M-tile 2*pair + r (its A rows, TMEM accumulator and epilogue)
 // and stages rows [r*BN/2, (r+1)*BN/2) of the B tile; the leader (rank 0)
 // issues every MMA and its commits arrive on both CTAs' barriers.
-template <int BN, int STAGES, int EPI, bool PAIR>
+// CONV: 3x3-conv instance (2-D frame tiles, tail tiles, tap-shifted boxes); the plain / temporal
+// instance carries none of that code (measured: up to 5 % on short-K GEMMs, profiles finding 20)
+template <int BN, int STAGES, int EPI, bool PAIR, bool CONV>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapR,
@@ -493,7 +496,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int64_t tile = t_first; tile < n_tiles; tile += t_step, ++tcount) {
         const int64_t tm = my_tm(tile);
         const int n0 = (int)(tile % p.tiles_n) * BN;
-        const MTile mt = decode_m(p, tm);
+        const MTile mt = decode_m<CONV>(p, tm);
         for (int it = 0; it < kiters; ++it) {
           const int tap = it / p.cblocks, cb = it % p.cblocks;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // my A tile + my half of B, completion bytes counted on the leader's barrier
             if (leader) mbar_expect_tx_e(&full[stage], 2 * L::STAGE_BYTES);
             const uint32_t fb = leader_addr(&full[stage]);
-            if (p.mode == SF_GEMM_CONV3X3)
+            if (CONV)
               tma_load_4d_2sm_e(mt.tail ? &mapAT : &mapA, fb, dA, cb * BK, mt.x0 + tap % 3 - 1, mt.y0 + tap / 3 - 1,
                               mt.f);
             else if (p.mode == SF_GEMM_TCONV3)
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             continue;
           }
           mbar_expect_tx_e(&full[stage], L::STAGE_BYTES);
-          if (p.mode == SF_GEMM_CONV3X3) {
+          if (CONV) {
             tma_load_4d_e(mt.tail ? &mapAT : &mapA, &full[stage], dA, cb * BK, mt.x0 + tap % 3 - 1,
                         mt.y0 + tap / 3 - 1, mt.f);
           } else if (p.mode == SF_GEMM_TCONV3) {
@@ -590,13 +593,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int64_t tile = t_first; tile < n_tiles; tile += t_step, ++tcount) {
       const int64_t tm = my_tm(tile);
       const int n0 = (int)(tile % p.tiles_n) * BN;
-      const MTile mt = decode_m(p, tm);
+      const MTile mt = decode_m<CONV>(p, tm);
       const bool phantom = tm >= p.tiles_m;   // odd tile count: the pair's second tile is empty
       // output row of this thread
       bool valid;
       int64_t o, i;
       int z = 0;
-      if (p.mode == SF_GEMM_CONV3X3) {
+      if (CONV) {
         // main tile: rows (y, x) of one frame; tail tile: (frame, y, x) over tail_fb frames
         const int per = mt.tail ? p.tail_rows * p.w_t : BM;
         const int fr = mt.f + row / per, rr = row % per;
@@ -662,7 +665,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (eh) asm volatile("bar.sync 3, 128;" ::: "memory");
           else asm volatile("bar.sync 2, 128;" ::: "memory");
           if (store_leader && nb < p.N) {
-            if (p.mode == SF_GEMM_CONV3X3)
+            if (CONV)
               tma_store_4d(mt.tail ? &mapOT : &mapO, buf, nb, mt.x0, mt.y0, mt.f);
             else
               tma_store_4d(&mapO, buf, nb, mt.i0, mt.o0, mt.z);
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int hn0 = n0 + eh * HC;
         uint64_t* rf = &res_full[ob * 2 + eh];
         auto load_res_half = [&](uint64_t* bar, uint8_t* dst, int col, const MTile& m) {
-          if (p.mode == SF_GEMM_CONV3X3)
+          if (CONV)
             tma_load_4d(m.tail ? &mapRT : &mapR, bar, dst, col, m.x0, m.y0, m.f);
           else
             tma_load_4d(&mapR, bar, dst, col, m.i0, m.o0, m.z);
@@ -724,7 +727,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int64_t nt = tile + t_step;
           if (nt < n_tiles) {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            const MTile nm = decode_m(p, my_tm(nt));
+            const MTile nm = decode_m<CONV>(p, my_tm(nt));
             const int nn0 = (int)(nt % p.tiles_n) * BN + eh * HC;
             uint64_t* rfn = &res_full[(ob ^ 1) * 2 + eh];
             mbar_expect_tx(rfn, HALF_BYTES);
@@ -786,7 +789,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         half_sync();
         if (hleader) {
           if (hn0 < p.N) {
-            if (p.mode == SF_GEMM_CONV3X3)
+            if (CONV)
               tma_store_4d(mt.tail ? &mapOT : &mapO, hbuf, hn0, mt.x0, mt.y0, mt.f);
             else
               tma_store_4d(&mapO, hbuf, hn0, mt.i0, mt.o0, mt.z);
@@ -1033,12 +1036,12 @@ bool gemm_tc_supported(const sf_gemm_args& a) {
   return tc::encode_fn() != nullptr;
 }
 
-template <int BN, int STAGES, int EPI, bool PAIR = false>
-static sf_status launch_cfg(const tc::Params& p, const tc::Maps& m, cudaStream_t st) {
+template <int BN, int STAGES, int EPI, bool PAIR, bool CONV>
+static sf_status launch_one(const tc::Params& p, const tc::Maps& m, cudaStream_t st) {
   constexpr int smem = tc::SmemLayout<BN, STAGES, EPI, PAIR>::TOTAL;
   static_assert(smem <= 232448, "shared memory budget");
   static bool init = false;
-  auto kern = tc::tc_gemm_kernel<BN, STAGES, EPI, PAIR>;
+  auto kern = tc::tc_gemm_kernel<BN, STAGES, EPI, PAIR, CONV>;
   if (!init) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     init = true;
@@ -1067,6 +1070,12 @@ static sf_status launch_cfg(const tc::Params& p, const tc::Maps& m, cudaStream_t
   cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, kern, p, m.a, m.b, m.r, m.o, m.at, m.rt, m.ot);
   return launch_status("sf_gemm(tcgen05 pair)");
+}
+
+template <int BN, int STAGES, int EPI, bool PAIR = false>
+static sf_status launch_cfg(const tc::Params& p, const tc::Maps& m, cudaStream_t st) {
+  return p.mode == SF_GEMM_CONV3X3 ? launch_one<BN, STAGES, EPI, PAIR, true>(p, m, st)
+                                   : launch_one<BN, STAGES, EPI, PAIR, false>(p, m, st);
 }
 
 // Output / residual maps share the M tiling of A: box {BN cols, tile rows}.
