@@ -272,7 +272,8 @@ def run_ours(args, world, rank, local):
                                 "launch list (profiles/)" if traffic else None,
                 "share_of_step": round(g_ms / pf["total_ms"], 4) if pf["total_ms"] else None,
                 "launches_per_key_step": g_calls, "flops_per_key_step": g_fl,
-                "peak_source": f"{peak_src} bf16_tflops_sustained"}
+                "peak_source": f"{peak_src} bf16_tflops_sustained",
+                "peak_burst": peaks["bf16_tflops"], "frac_burst": round(achieved / peaks["bf16_tflops"], 4)}
     mixed = prof_full.mixed_roofline(peak_tf, peaks["hbm_gbs"])
     roofline_mixed = {"bound": "per launch max(tensor, hbm)", "kernel": "all sf_gemm launches of one key step",
                       "peak_tflops": peak_tf, "peak_gbps": peaks["hbm_gbs"], **mixed,
@@ -281,9 +282,15 @@ def run_ours(args, world, rank, local):
     roofline_attn = None
     if fa and fa["ms"]:
         fa_tf = fa["flops"] / (fa["ms"] * 1e9)
+        # Each attention launch is ~1.8 ms timed alone between CUDA events, and it runs above the
+        # sustained matmul figure (measured at a lower power-capped clock), so the burst peak is
+        # the honest denominator here; the sustained fraction is kept beside it.
+        peak_b = peaks["bf16_tflops"]
         roofline_attn = {"bound": "tensor", "kernel": "flash5_kernel (fused spatial attention, CTA pairs, 96-key blocks)",
-                         "achieved": round(fa_tf, 2), "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": round(fa_tf / peak_tf, 4), "share_of_step": round(fa["ms"] / pf["total_ms"], 4),
+                         "achieved": round(fa_tf, 2), "peak": peak_b, "unit": "TFLOP/s",
+                         "frac": round(fa_tf / peak_b, 4), "peak_source": f"{peak_src} bf16_tflops (burst)",
+                         "frac_sustained": round(fa_tf / peak_tf, 4),
+                         "share_of_step": round(fa["ms"] / pf["total_ms"], 4),
                          "flops_per_key_step": fa["flops"]}
 
     line = {
