@@ -163,3 +163,27 @@ def test_wide_config_matches_reference(golden):
     r = rel(x, runs["wide_float64_final"])
     print("wide final rel", r)
     assert r <= 2e-2
+
+
+def test_spec_default_toy_matches_reference(golden):
+    """Second parity point (SURVEY.md §8 config note): the SPEC default toy
+    UNetConfig() = c=8, 8 frames, 32x32, K=25 (unet.py:41-55),
+    against the reference's own fp32 run (tests/golden/make_golden.py).
+    Tolerances: final latent max_rel <= 2e-2, similarity map max abs err <= 5e-3,
+    identical key steps G wherever A1's decision margin exceeds 2x that error."""
+    runs = golden["runs"]
+    cfg = UNetConfig()
+    x, S = Denoiser(cfg).calibrate(initial_latent(cfg))
+    r = rel(x, runs["default_float32_final"])
+    s_ref = runs["default_float32_S"]
+    s_err = float(np.abs(S.values - s_ref).max())
+    print("default final rel", r, "S err", s_err)
+    assert r <= 2e-2
+    assert s_err <= 5e-3
+    checked = 0
+    for g in np.linspace(max(float(s_ref.min()), 0.05), 0.999, 24):
+        sch = key_step_search(s_ref, float(g))
+        if sch.margin is not None and sch.margin > 2 * s_err:
+            assert key_step_search(S, float(g)).key_steps == sch.key_steps, g
+            checked += 1
+    assert checked >= 3, checked
