@@ -3,6 +3,7 @@
     python tools/gemm_bench.py plain 230400 320 320 [--res] [--reps 20]
     python tools/gemm_bench.py conv 25x72x128 320 320          # frames x H x W, cin, cout
     python tools/gemm_bench.py tconv 25x9216 320 320           # T x pixels, cin, cout
+    python tools/gemm_bench.py vt 25x9216 320 320              # frames x pixels: v^T = wv^T x^T per frame
 
 Prints time, TFLOP/s and the algorithmic HBM bytes/s (A read once, out (+res) once).
 """
@@ -21,7 +22,7 @@ from paper_2411_01171_b200.device import Rows  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["plain", "conv", "tconv"])
+    ap.add_argument("mode", choices=["plain", "conv", "tconv", "vt"])
     ap.add_argument("m")
     ap.add_argument("cin", type=int)
     ap.add_argument("n", type=int)
@@ -35,7 +36,7 @@ def main():
     rows = 1
     for d in dims:
         rows *= d
-    taps = {"plain": 1, "conv": 9, "tconv": 3}[a.mode]
+    taps = {"plain": 1, "conv": 9, "tconv": 3, "vt": 1}[a.mode]
     x = (torch.randn(rows, a.cin, device=dev)).to(torch.bfloat16)
     w = (torch.randn(a.n, taps * a.cin, device=dev) * (taps * a.cin) ** -0.5).to(torch.bfloat16)
     bias = torch.randn(a.n, device=dev)
@@ -52,6 +53,13 @@ def main():
             D.gemm(st, mode=N.GEMM_CONV3X3, n_outer=F_, n_inner=H * W, H=H, W=W, cin=a.cin, n=a.n,
                    a=Rows(x, 0, H * W), w=w, out=Rows(out, 0, H * W), bias=bias, act=act,
                    res=Rows(res, 0, H * W) if res is not None else None)
+        elif a.mode == "vt":
+            # the spatial-attention v^T projection (device.spatial_attention): A = wv (M = C),
+            # B = the frame's tokens (K-major), batched over frames
+            F_, P = dims
+            D.gemm(st, mode=N.GEMM_PLAIN, n_outer=1, n_inner=a.n, cin=a.cin, n=P, a=Rows(w), w=out,
+                   w_ptr=x.data_ptr(), w_ld=a.cin, out=Rows(out, 0, 0), batch=F_, a_bstride=0,
+                   w_bstride=P * a.cin, out_bstride=a.n * P)
         else:
             T, P = dims
             D.gemm(st, mode=N.GEMM_TCONV3, n_outer=T, n_inner=P, T=T, cin=a.cin, n=a.n, a=Rows(x, 0, P), w=w,
