@@ -649,7 +649,10 @@ __device__ __forceinline__ void tq_put(bf16 (*dst)[TQ_LD], const TqChunk& r, int
   }
 }
 
-__global__ void __launch_bounds__(TQ_WARPS * 32) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
+#ifndef TQ_MINB
+#define TQ_MINB 1   // resident blocks per SM the register allocation must allow (tuning: -DTQ_MINB=n)
+#endif
+__global__ void __launch_bounds__(TQ_WARPS * 32, TQ_MINB) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
                                                                           sf_view_t out, int B, int T, int n_inner,
                                                                           int C, float scale_log2) {
   griddep_wait();
