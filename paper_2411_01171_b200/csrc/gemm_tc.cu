@@ -1229,7 +1229,17 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   int BN = pick_bn(a.N);
   // 192/224-wide tiles only for long K: compute-bound convs gain (L1 conv K=17280 N=640: 914 -> 846 us),
   // memory-bound short-K GEMMs lose (K=320 N=640: 118 -> 131 us in the key step)
+  const bool pair_in = pair;
   pair = choose_tiling(a.N, p.tiles_m, pair, !a.out_fp32 && p.taps * p.cblocks >= 12, &BN);
+  // v^T projections (the weights as a shared A, M = C, batched over frames, many N tiles, short K,
+  // no epilogue operands): memory bound on B with few M tiles, where 160-column tiles (the last one
+  // partial: OOB B rows load as zeros, stores clip) measured faster than the model's pick:
+  // L0 81.9 -> 73.1 us, L1 65.6 -> 57.6 us (profiles/README.md finding 21)
+  if (!getenv("SF_GEMM_BN") && a.mode == SF_GEMM_PLAIN && a.batch > 1 && a.a_bstride == 0 && !a.bias &&
+      !a.rowbias && !a.res.ptr && !a.out_fp32 && a.cin <= 640 && a.N >= 2048) {
+    BN = 160;
+    pair = pair_in;
+  }
   p.BN = BN;
   p.tiles_n = (a.N + BN - 1) / BN;
   {

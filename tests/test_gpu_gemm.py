@@ -239,3 +239,18 @@ def test_wide_pair_tiles(case):
                res=Rows(res), backend=2)
         ref = a.float() @ w.float().T + bias + res.float()
     assert rel(out, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("frames,P,C", [(3, 9216, 320), (2, 2304, 640), (2, 576, 1280), (2, 2056, 320)])
+def test_vt_projection(frames, P, C):
+    """The spatial-attention v^T projection (device.spatial_attention): v^T[f] = wv^T x[f]^T with the
+    weights as a shared A (a_bstride = 0) and each frame's tokens as a K-major B, batched over frames.
+    Covers the 160-column tiles picked for it, including a partial last N tile (P = 2056, 9216)."""
+    torch.manual_seed(0)
+    x, w = rnd(frames * P, C), rnd(C, C, scale=C ** -0.5)
+    out = torch.empty(frames * C, P, dtype=torch.bfloat16, device=dev)
+    D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=C, cin=C, n=P,
+           a=Rows(w), w=out, w_ptr=x.data_ptr(), w_ld=C, out=Rows(out, 0, 0), batch=frames, a_bstride=0,
+           w_bstride=P * C, out_bstride=C * P)
+    ref = torch.einsum("ck,fpk->fcp", w.float(), x.float().view(frames, P, C)).reshape(frames * C, P)
+    assert rel(out, ref) <= 1e-2
