@@ -652,6 +652,11 @@ __device__ __forceinline__ void tq_put(bf16 (*dst)[TQ_LD], const TqChunk& r, int
 #ifndef TQ_MINB
 #define TQ_MINB 1   // resident blocks per SM the register allocation must allow (tuning: -DTQ_MINB=n)
 #endif
+// SPLIT = 1: one warp per pixel.  SPLIT = TQ_WARPS: the block's warps share one pixel (few-pixel deep
+// levels, e.g. 576 / 144 pixels, where one warp per pixel leaves most SMs idle): warp w takes the
+// channel chunks w, w + SPLIT, ...; the partial scores are summed across warps in shared memory in a
+// fixed order (deterministic), every warp runs the (cheap) softmax, and each writes its own chunks of O.
+template <int SPLIT>
 __global__ void __launch_bounds__(TQ_WARPS * 32, TQ_MINB) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
                                                                           sf_view_t out, int B, int T, int n_inner,
                                                                           int C, float scale_log2) {
@@ -662,8 +667,10 @@ __global__ void __launch_bounds__(TQ_WARPS * 32, TQ_MINB) temporal_attn_mma_kern
   bf16 (*qs)[TQ_LD] = reinterpret_cast<bf16 (*)[TQ_LD]>(tq_smem + warp * 3 * 32 * TQ_LD * 2);
   bf16 (*ks)[TQ_LD] = qs + 32;
   bf16 (*vs)[TQ_LD] = qs + 64;
-  const int64_t gp = (int64_t)blockIdx.x * TQ_WARPS + warp;   // global pixel (b, pix)
+  const int64_t gp = SPLIT == 1 ? (int64_t)blockIdx.x * TQ_WARPS + warp : (int64_t)blockIdx.x;  // (b, pix)
   if (gp >= (int64_t)B * n_inner) return;
+  const int cs = SPLIT == 1 ? 0 : warp * TQ_CH;   // this warp's first channel chunk
+  constexpr int CSTEP = SPLIT * TQ_CH;
   const int b = gp / n_inner, pix = gp % n_inner;
   float sacc[2][4][4];
 #pragma unroll
@@ -673,16 +680,18 @@ __global__ void __launch_bounds__(TQ_WARPS * 32, TQ_MINB) temporal_attn_mma_kern
 #pragma unroll
       for (int e = 0; e < 4; ++e) sacc[i][j][e] = 0.f;
   TqChunk rq, rk;
-  tq_fetch(rq, qkv, b, T, pix, 0, min(TQ_CH, C), lane);
-  tq_fetch(rk, qkv, b, T, pix, koff, min(TQ_CH, C), lane);
-  for (int c0 = 0; c0 < C; c0 += TQ_CH) {
+  if (SPLIT == 1 || cs < C) {
+    tq_fetch(rq, qkv, b, T, pix, cs, min(TQ_CH, C - cs), lane);
+    tq_fetch(rk, qkv, b, T, pix, koff + cs, min(TQ_CH, C - cs), lane);
+  }
+  for (int c0 = cs; c0 < C; c0 += CSTEP) {
     tq_put(qs, rq, lane);
     tq_put(ks, rk, lane);
     __syncwarp();
-    if (c0 + TQ_CH < C) {
-      const int nv = min(TQ_CH, C - c0 - TQ_CH);
-      tq_fetch(rq, qkv, b, T, pix, c0 + TQ_CH, nv, lane);
-      tq_fetch(rk, qkv, b, T, pix, koff + c0 + TQ_CH, nv, lane);
+    if (c0 + CSTEP < C) {
+      const int nv = min(TQ_CH, C - c0 - CSTEP);
+      tq_fetch(rq, qkv, b, T, pix, c0 + CSTEP, nv, lane);
+      tq_fetch(rk, qkv, b, T, pix, koff + c0 + CSTEP, nv, lane);
     }
 #pragma unroll
     for (int kk = 0; kk < TQ_CH; kk += 16) {
@@ -701,6 +710,31 @@ __global__ void __launch_bounds__(TQ_WARPS * 32, TQ_MINB) temporal_attn_mma_kern
       }
     }
     __syncwarp();
+  }
+  if constexpr (SPLIT > 1) {
+    // sum the warps' partial scores (fragment layout, fixed warp order) through shared memory
+    float* red = reinterpret_cast<float*>(tq_smem);
+    constexpr int PER = 2 * 4 * 4 * 32;   // floats per warp
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) red[warp * PER + ((i * 4 + j) * 4 + e) * 32 + lane] = sacc[i][j][e];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float v = 0.f;
+#pragma unroll
+          for (int w = 0; w < SPLIT; ++w) v += red[w * PER + ((i * 4 + j) * 4 + e) * 32 + lane];
+          sacc[i][j][e] = v;
+        }
+    __syncthreads();
   }
   // softmax over columns (keys) per row; lane holds rows lane/4 (+8) of each m-tile
   float rsum[2][2];
@@ -747,12 +781,12 @@ __global__ void __launch_bounds__(TQ_WARPS * 32, TQ_MINB) temporal_attn_mma_kern
       pa[mi][kk][3] = pack_bf2(sacc[mi][2 * kk + 1][2], sacc[mi][2 * kk + 1][3]);
     }
   TqChunk rv;
-  tq_fetch(rv, qkv, b, T, pix, voff, min(TQ_CH, C), lane);
-  for (int c0 = 0; c0 < C; c0 += TQ_CH) {
+  if (SPLIT == 1 || cs < C) tq_fetch(rv, qkv, b, T, pix, voff + cs, min(TQ_CH, C - cs), lane);
+  for (int c0 = cs; c0 < C; c0 += CSTEP) {
     const int cv = min(TQ_CH, C - c0);
     tq_put(vs, rv, lane);
     __syncwarp();
-    if (c0 + TQ_CH < C) tq_fetch(rv, qkv, b, T, pix, voff + c0 + TQ_CH, min(TQ_CH, C - c0 - TQ_CH), lane);
+    if (c0 + CSTEP < C) tq_fetch(rv, qkv, b, T, pix, voff + c0 + CSTEP, min(TQ_CH, C - c0 - CSTEP), lane);
     float oacc[2][8][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -1339,12 +1373,19 @@ sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, 
     const int smem = TQ_WARPS * 3 * 32 * TQ_LD * 2;
     static bool init = false;
     if (!init) {
-      cudaFuncSetAttribute(temporal_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(temporal_attn_mma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(temporal_attn_mma_kernel<TQ_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       init = true;
     }
-    int64_t warps = (int64_t)B * n_inner;
-    launch_k(temporal_attn_mma_kernel, dim3((unsigned)((warps + TQ_WARPS - 1) / TQ_WARPS)), dim3(TQ_WARPS * 32), smem, (cudaStream_t)stream, qkv, koff, voff, out, B, T, n_inner, C,
-                                                       scale * 1.4426950408889634f);
+    const int64_t pixels = (int64_t)B * n_inner;
+    const float sl2 = scale * 1.4426950408889634f;
+    // fewer pixels than ~8 warps per SM (C3 L2 / L3: 576 / 144): one block per pixel, channels split
+    if (pixels < (int64_t)num_sms() * 8 && C >= 2 * TQ_CH)
+      launch_k(temporal_attn_mma_kernel<TQ_WARPS>, dim3((unsigned)pixels), dim3(TQ_WARPS * 32), smem,
+               (cudaStream_t)stream, qkv, koff, voff, out, B, T, n_inner, C, sl2);
+    else
+      launch_k(temporal_attn_mma_kernel<1>, dim3((unsigned)((pixels + TQ_WARPS - 1) / TQ_WARPS)),
+               dim3(TQ_WARPS * 32), smem, (cudaStream_t)stream, qkv, koff, voff, out, B, T, n_inner, C, sl2);
     return launch_status("sf_temporal_attention_core");
   }
   launch_k(temporal_attn_kernel, dim3(B * n_inner), dim3(256), 0, (cudaStream_t)stream, qkv, koff, voff, out, T, n_inner, C, scale);

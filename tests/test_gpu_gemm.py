@@ -169,7 +169,11 @@ def test_flash_core(Fr, HW, C):
 
 
 @pytest.mark.parametrize("B,T,P,C", [(1, 25, 300, 320), (2, 8, 64, 32), (1, 32, 50, 640), (1, 64, 20, 64),
-                                     (1, 16, 40, 1280), (1, 3, 10, 24)])
+                                     (1, 16, 40, 1280), (1, 3, 10, 24),
+                                     # one warp per pixel (many pixels) and the channel-split block per
+                                     # pixel (few pixels: C3 L2 / L3, uneven chunk counts, B = 2)
+                                     (1, 25, 2400, 320), (1, 25, 576, 1280), (1, 25, 144, 1280),
+                                     (1, 25, 200, 192), (2, 25, 300, 320)])
 def test_temporal_core(B, T, P, C):
     """Per-pixel attention over T frames vs torch (rows o = b*T+t, i = pixel)."""
     torch.manual_seed(5)
