@@ -1024,7 +1024,7 @@ extern "C" int32_t sf_debug_gemm_trace(unsigned long long* host, int32_t n_per_r
 
 bool gemm_tc_supported(const sf_gemm_args& a) {
   if (!a.w_kmajor) return false;
-  if (a.cin % 64) return false;
+  if (a.cin % 64 && !(a.mode == SF_GEMM_PLAIN && a.cin > 64 && a.cin % 8 == 0)) return false;
   if (a.out_fp32 == 0 && (a.out.ld % 8 || !aligned16(a.out.ptr))) return false;
   if (a.out_fp32 == 0 && ((a.out.ostride * a.out.ld * 2) % 16 || (a.out_bstride * 2) % 16)) return false;
   if (a.res.ptr && ((a.res.ostride * a.res.ld * 2) % 16 || (a.res_bstride * 2) % 16)) return false;
@@ -1116,7 +1116,9 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   p.mode = a.mode;
   p.N = a.N;
   p.cin = a.cin;
-  p.cblocks = a.cin / BK;
+  // plain GEMMs may end in a partial K block (e.g. P.V over 144 tokens): the A / B tensor maps
+  // stop at cin, so the block's tail loads as zeros (TMA OOB fill) and adds nothing
+  p.cblocks = (a.cin + BK - 1) / BK;
   p.taps = a.mode == SF_GEMM_PLAIN ? 1 : (a.mode == SF_GEMM_CONV3X3 ? 9 : 3);
   p.alpha = a.alpha;
   p.bias = a.bias;

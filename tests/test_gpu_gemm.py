@@ -258,3 +258,34 @@ def test_vt_projection(frames, P, C):
            w_bstride=P * C, out_bstride=C * P)
     ref = torch.einsum("ck,fpk->fcp", w.float(), x.float().view(frames, P, C)).reshape(frames * C, P)
     assert rel(out, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("frames,P,C", [(3, 144, 1280), (2, 200, 320), (2, 72, 640)])
+def test_partial_k_block_batched_pv(frames, P, C):
+    """P.V with a token count that is not a multiple of 64 (C3 L3: 144 tokens) on the tcgen05 backend:
+    the last 64-wide K block is partial and loads as zeros past K (TMA OOB fill)."""
+    torch.manual_seed(3)
+    p = torch.softmax(torch.randn(frames, P, P, device=dev), dim=-1).to(torch.bfloat16)
+    vt = rnd(frames, C, P)
+    o = torch.empty(frames * P, C, dtype=torch.bfloat16, device=dev)
+    args = D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=P, cin=P, n=C,
+                  a=Rows(p.view(frames * P, P), 0, 0), w=vt, w_ld=P, out=Rows(o, 0, 0), batch=frames,
+                  a_bstride=P * P, w_bstride=C * P, out_bstride=P * C, backend=2)
+    assert N.query("sf_gemm_backend", args) == 2
+    ref = torch.bmm(p.float(), vt.float().transpose(1, 2)).reshape(frames * P, C)
+    assert rel(o, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("M,K,Nn", [(1000, 200, 320), (4096, 72, 256)])
+def test_plain_partial_k_block(M, K, Nn):
+    """Plain GEMM + fused epilogue with K % 64 != 0 on tcgen05 (partial last K block)."""
+    torch.manual_seed(4)
+    a, w = rnd(M, K), rnd(Nn, K, scale=K ** -0.5)
+    bias = torch.randn(Nn, device=dev)
+    res = rnd(M, Nn)
+    out = torch.empty(M, Nn, dtype=torch.bfloat16, device=dev)
+    args = D.gemm(torch.cuda.current_stream().cuda_stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=M, cin=K, n=Nn,
+                  a=Rows(a), w=w, out=Rows(out), bias=bias, res=Rows(res), act=N.ACT_SILU, backend=2)
+    assert N.query("sf_gemm_backend", args) == 2
+    ref = F.silu(a.float() @ w.float().T + bias) + res.float()
+    assert rel(out, ref) <= 1e-2
