@@ -652,12 +652,15 @@ __device__ __forceinline__ void tq_put(bf16 (*dst)[TQ_LD], const TqChunk& r, int
 #ifndef TQ_MINB
 #define TQ_MINB 1   // resident blocks per SM the register allocation must allow (tuning: -DTQ_MINB=n)
 #endif
+#ifndef TQ_SPLIT_MINB
+#define TQ_SPLIT_MINB 1   // the same for the channel-split variant (tuning: -DTQ_SPLIT_MINB=n)
+#endif
 // SPLIT = 1: one warp per pixel.  SPLIT = TQ_WARPS: the block's warps share one pixel (few-pixel deep
 // levels, e.g. 576 / 144 pixels, where one warp per pixel leaves most SMs idle): warp w takes the
 // channel chunks w, w + SPLIT, ...; the partial scores are summed across warps in shared memory in a
 // fixed order (deterministic), every warp runs the (cheap) softmax, and each writes its own chunks of O.
 template <int SPLIT>
-__global__ void __launch_bounds__(TQ_WARPS * 32, TQ_MINB) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
+__global__ void __launch_bounds__(TQ_WARPS * 32, SPLIT > 1 ? TQ_SPLIT_MINB : TQ_MINB) temporal_attn_mma_kernel(sf_view_t qkv, int koff, int voff,
                                                                           sf_view_t out, int B, int T, int n_inner,
                                                                           int C, float scale_log2) {
   griddep_wait();
