@@ -1,0 +1,270 @@
+"""torch fp64 restatement of the reference path (TEST INFRASTRUCTURE ONLY).
+
+Used only by ``tests/`` (and ``tools/parity_run.py``, which writes the
+committed parity record) as the checker at BASELINE configs 2-5, where the
+numpy oracle (``oracle/kernels.py``) and the reference itself need minutes per
+evaluation (309 s per C3 step on 8 cores).  It runs the same
+arithmetic as the reference kernels through torch fp64 ops on whatever device
+it is given (the B200 in the GPU tests):
+
+=====================  =================================================  ==========================
+reference kernel       torch fp64 equivalent                              reference file:line
+=====================  =================================================  ==========================
+``_conv2d``            ``F.conv2d(padding=1)`` per frame                  ``kernels.py:181-201``
+``_temporal_conv``     ``F.conv3d`` kernel (3,1,1), padding (1,0,0)       ``kernels.py:204-225``
+``_group_norm``        ``F.group_norm`` (biased variance)                 ``kernels.py:228-237``
+``_layer_norm``        ``F.layer_norm`` over channels                     ``kernels.py:240-244``
+``_silu``              ``F.silu``                                         ``kernels.py:247-253``
+``_linear``            ``F.linear`` per token                             ``kernels.py:256-266``
+``_attention``         q,k,v = x@W (no transpose), softmax(qk^T/sqrt(C))  ``kernels.py:269-292``
+spatial / temporal     per frame over h*w / per pixel over t              ``kernels.py:295-308``
+``_downsample2x``      (x00+x01+x10+x11)*0.25                              ``kernels.py:311-316``
+``_upsample2x``        nearest repeat                                     ``kernels.py:319-320``
+Add / Concat           ``a + b`` (h=w=1 operand broadcasts) / ``cat``      ``kernels.py:354-360``
+``cosine_similarity``  fp64 dot products, clipped to [-1, 1]               ``kernels.py:375-390``
+=====================  =================================================  ==========================
+
+The walk is the reference-mode evaluation (every node of ``topo_order()``,
+``SPEC.md:333-341``): in fp64 the reference's SlicedLoop output equals its
+Reference output to ~1e-15 (survey [probe] 1.1e-15), so the
+unsliced walk is the oracle for every slice plan.  Denoise loop, rehash tail
+and Algorithm A1 follow ``SPEC.md:413-487`` exactly like ``oracle/harness.py``.
+
+Pinning: ``tests/test_oracle_golden.py::test_torch_ref_pinned_to_goldens``
+checks this module against the reference's own fp64 runs frozen in
+``tests/golden`` (C1 10-step run, its similarity map, the rehash run, the
+base-64 WIDE run) at <= 1e-12.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from paper_2411_01171_b200.kinds import OpKind
+from paper_2411_01171_b200.unet import PROBE_LABEL, build_toy_unet, sinusoidal_step_embedding
+
+DT = torch.float64
+
+
+def _t(a, dev):
+    return torch.as_tensor(np.asarray(a, dtype=np.float64), device=dev)
+
+
+def conv2d(x, w, b):
+    B, T, C, H, W = x.shape
+    y = F.conv2d(x.reshape(B * T, C, H, W), w, b, padding=1)
+    return y.reshape(B, T, -1, H, W)
+
+
+def temporal_conv(x, w, b):
+    y = F.conv3d(x.permute(0, 2, 1, 3, 4), w[:, :, :, None, None], b, padding=(1, 0, 0))
+    return y.permute(0, 2, 1, 3, 4).contiguous()
+
+
+def group_norm(x, gamma, beta, groups, eps):
+    B, T, C, H, W = x.shape
+    y = F.group_norm(x.reshape(B * T, C, H, W), groups, gamma, beta, eps)
+    return y.reshape(B, T, C, H, W)
+
+
+def layer_norm(x, gamma, beta, eps):
+    y = F.layer_norm(x.permute(0, 1, 3, 4, 2), (x.shape[2],), gamma, beta, eps)
+    return y.permute(0, 1, 4, 2, 3).contiguous()
+
+
+def linear(x, w, b):
+    y = F.linear(x.permute(0, 1, 3, 4, 2), w, b)
+    return y.permute(0, 1, 4, 2, 3).contiguous()
+
+
+def attention_tokens(tok, wq, wk, wv, wo, chunk_elems=1 << 28):
+    """(n, N, C) tokens; chunked over sequences so S stays within ``chunk_elems``."""
+    n, L, C = tok.shape
+    out = torch.empty_like(tok)
+    per = max(1, chunk_elems // max(1, L * L))
+    for s0 in range(0, n, per):
+        t = tok[s0:s0 + per]
+        q, k, v = t @ wq, t @ wk, t @ wv
+        s = (q @ k.transpose(1, 2)) * (1.0 / math.sqrt(C))
+        p = torch.softmax(s, dim=-1)
+        out[s0:s0 + per] = (p @ v) @ wo
+    return out
+
+
+def spatial_attention(x, p):
+    B, T, C, H, W = x.shape
+    tok = x.reshape(B * T, C, H * W).transpose(1, 2)
+    o = attention_tokens(tok, p["wq"], p["wk"], p["wv"], p["wo"])
+    return o.transpose(1, 2).reshape(B, T, C, H, W)
+
+
+def temporal_attention(x, p):
+    B, T, C, H, W = x.shape
+    tok = x.permute(0, 3, 4, 1, 2).reshape(B * H * W, T, C)
+    o = attention_tokens(tok, p["wq"], p["wk"], p["wv"], p["wo"])
+    return o.reshape(B, H, W, T, C).permute(0, 3, 4, 1, 2).contiguous()
+
+
+def downsample2x(x):
+    return (x[..., 0::2, 0::2] + x[..., 0::2, 1::2] + x[..., 1::2, 0::2] + x[..., 1::2, 1::2]) * 0.25
+
+
+def upsample2x(x):
+    return x.repeat_interleave(2, dim=3).repeat_interleave(2, dim=4)
+
+
+def apply(kind, xs, p, attrs):
+    x = xs[0]
+    if kind is OpKind.CONV2D:
+        return conv2d(x, p["weight"], p["bias"])
+    if kind is OpKind.TEMPORAL_CONV:
+        return temporal_conv(x, p["weight"], p["bias"])
+    if kind is OpKind.GROUP_NORM:
+        return group_norm(x, p["gamma"], p["beta"], int(attrs.get("groups", 1)), float(attrs.get("eps", 1e-5)))
+    if kind is OpKind.LAYER_NORM:
+        return layer_norm(x, p["gamma"], p["beta"], float(attrs.get("eps", 1e-5)))
+    if kind is OpKind.SILU:
+        return F.silu(x)
+    if kind is OpKind.LINEAR:
+        return linear(x, p["weight"], p["bias"])
+    if kind is OpKind.SPATIAL_ATTENTION:
+        return spatial_attention(x, p)
+    if kind is OpKind.TEMPORAL_ATTENTION:
+        return temporal_attention(x, p)
+    if kind is OpKind.DOWNSAMPLE2X:
+        return downsample2x(x)
+    if kind is OpKind.UPSAMPLE2X:
+        return upsample2x(x)
+    if kind is OpKind.ADD:
+        return xs[0] + xs[1]          # an h=w=1 operand broadcasts (kernels.py:354-358)
+    if kind is OpKind.CONCAT:
+        return torch.cat(xs, dim=2)
+    if kind is OpKind.SPLIT:
+        sizes = [int(s) for s in attrs["sizes"]]
+        off = sum(sizes[:int(attrs["index"])])
+        return x[:, :, off:off + sizes[int(attrs["index"])]]
+    raise ValueError(f"unknown kind {kind}")
+
+
+class TorchRef:
+    """Graph + fp64 device weights; reference-mode evaluations with value freeing."""
+
+    def __init__(self, cfg, device="cpu", graph=None, weights=None):
+        self.cfg = cfg
+        self.dev = torch.device(device)
+        if graph is None:
+            graph, weights = build_toy_unet(cfg)
+        self.graph = graph
+        self.topo = graph.topo_order()
+        self.W = {}
+        for n in graph.nodes.values():
+            if n.param_ref:
+                self.W[n.id] = {k: _t(v, self.dev) for k, v in weights.get(n.param_ref).items()}
+        last = {}
+        for i, nid in enumerate(self.topo):
+            for r in graph.nodes[nid].inputs:
+                last[r] = i
+        self.last_use = last
+        self.probe_id = graph.node_by_label(PROBE_LABEL).id
+
+    def step_emb(self, s):
+        c = self.cfg
+        v = _t(sinusoidal_step_embedding(s, c.emb_channels, c.emb_scale), self.dev)
+        return v[None, None, :, None, None].expand(c.effective_batch, c.frames, c.emb_channels, 1, 1)
+
+    @torch.no_grad()
+    def evaluate(self, feeds, start_after=None, capture=()):
+        """One evaluation; ``start_after`` = walk only nodes strictly after it (the rehash tail)."""
+        g = self.graph
+        vals = dict(feeds)
+        cut = -1 if start_after is None else self.topo.index(start_after)
+        cap = {}
+        out_id = g.outputs[0]
+        for i, nid in enumerate(self.topo):
+            if i <= cut:
+                continue
+            n = g.nodes[nid]
+            vals[nid] = apply(n.kind, [vals[r] for r in n.inputs], self.W.get(nid), n.attrs)
+            if n.label in capture:
+                cap[n.label] = vals[nid]
+            for r in n.inputs:
+                if self.last_use.get(r) == i and r != out_id and r in vals:
+                    del vals[r]
+        return vals[out_id], cap
+
+    def eps(self, x, s, capture=()):
+        return self.evaluate({"x": x, "step_emb": self.step_emb(s)}, capture=capture)
+
+    def tail(self, cache):
+        return self.evaluate({self.probe_id: cache}, start_after=self.probe_id)[0]
+
+    def initial_latent(self):
+        """x0 = default_rng(seed+1).standard_normal(input_shape) kept in fp64 (the reference's fp64 run)."""
+        c = self.cfg
+        return _t(np.random.default_rng(c.seed + 1).standard_normal(tuple(c.input_shape())), self.dev)
+
+    @staticmethod
+    def alpha(s, K):
+        """alpha_s = 0.08 (1 - s/K) in the run's dtype, fp64 here."""
+        return 0.08 * (1.0 - s / K)
+
+
+def gram(probes):
+    """fp64 K x K Gram of device probes."""
+    K = len(probes)
+    G = torch.empty(K, K, dtype=DT, device=probes[0].device)
+    flat = [p.reshape(-1) for p in probes]
+    for i in range(K):
+        for j in range(i, K):
+            G[i, j] = G[j, i] = torch.dot(flat[i], flat[j])
+    return G.cpu().numpy()
+
+
+def similarity_from_gram(G):
+    d = np.sqrt(np.diag(G))
+    S = np.clip(G / np.outer(d, d), -1.0, 1.0)
+    np.fill_diagonal(S, 1.0)
+    return S
+
+
+@torch.no_grad()
+def run_full(ref: TorchRef, K=None, keep_probes=True, eps_steps=()):
+    """All-key K-step loop: (final x, S map, {s: eps_s} for s in eps_steps)."""
+    K = K or ref.cfg.steps
+    x = ref.initial_latent()
+    probes, epss = [], {}
+    for s in range(K):
+        e, cap = ref.eps(x, s, capture=(PROBE_LABEL,))
+        if keep_probes:
+            probes.append(cap[PROBE_LABEL])
+        if s in eps_steps:
+            epss[s] = e.clone()
+        x = x - ref.alpha(s, K) * e
+        del e, cap
+    S = similarity_from_gram(gram(probes)) if keep_probes else None
+    return x, S, epss
+
+
+@torch.no_grad()
+def run_rehash(ref: TorchRef, G, K=None):
+    """Key steps: full evaluation, cache the probe; skipped: the tail on the donor's cache."""
+    K = K or ref.cfg.steps
+    keys = set(G)
+    x = ref.initial_latent()
+    cache = None
+    for s in range(K):
+        if s in keys:
+            e, cap = ref.eps(x, s, capture=(PROBE_LABEL,))
+            cache = cap[PROBE_LABEL]
+        else:
+            e = ref.tail(cache)
+        x = x - ref.alpha(s, K) * e
+    return x
+
+
+def to_bcthw_numpy(x):
+    return x.detach().cpu().numpy()

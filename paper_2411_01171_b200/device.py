@@ -10,8 +10,9 @@ Weights are uploaded once, in the layouts the kernels consume:
 * attention ``wq, wk, wv, wo`` ``(c, c)``, applied as ``x @ W`` (no transpose,
   kernels.py:285-291) -> one fused bf16 ``[3c][c]`` = [wq^T; wk^T; wv^T] and
   ``wo^T``.
-* norm gamma/beta and every bias stay fp32; the latent-edge convs (in_conv
-  with 4-8 input channels, out_conv with 4-8 output channels) stay fp32.
+* norm gamma/beta and every bias stay fp32; the latent-edge in_conv (4-8
+  input channels) and the step-embedding projections keep fp32 weights only
+  (no bf16 copy), every other weight exists once, in bf16.
 
 Every launcher takes :class:`Rows` views (a two-level row view over a torch
 tensor, see ``sf_view_t``) and the CUDA stream handle, and goes straight to
@@ -84,8 +85,10 @@ class DeviceWeights:
         if k is OpKind.CONV2D:
             w = np.asarray(prm["weight"], dtype=np.float64)
             co, ci = w.shape[:2]
-            out = {"bias": f32(prm["bias"], d), "w32": f32(w, d),
-                   "wt32": f32(w.transpose(2, 3, 1, 0).reshape(9, ci, co), d)}
+            out = {"bias": f32(prm["bias"], d)}
+            if ci % 8 or tuple(getattr(node, "inputs", ()))[:1] == ("x",):
+                # fp32 [tap][ci][co] for sf_conv3x3_smallcin (the latent-edge in_conv)
+                out["wt32"] = f32(w.transpose(2, 3, 1, 0).reshape(9, ci, co), d)
             if ci % 8 == 0:
                 out["w"] = bf16(w.transpose(0, 2, 3, 1).reshape(co, 9 * ci), d)
                 if co < TAPWISE_MAX_COUT:
@@ -97,7 +100,10 @@ class DeviceWeights:
             co, ci = w.shape[:2]
             return {"w": bf16(w.transpose(0, 2, 1).reshape(co, 3 * ci), d), "bias": f32(prm["bias"], d)}
         if k is OpKind.LINEAR:
-            return {"w": bf16(prm["weight"], d), "w32": f32(prm["weight"], d), "bias": f32(prm["bias"], d)}
+            if tuple(getattr(node, "inputs", ())) == ("step_emb",):
+                # step-embedding projection: one fp32 gemv per step (executor.emb_launch)
+                return {"w32": f32(prm["weight"], d), "bias": f32(prm["bias"], d)}
+            return {"w": bf16(prm["weight"], d), "bias": f32(prm["bias"], d)}
         if k in (OpKind.GROUP_NORM, OpKind.LAYER_NORM):
             return {"gamma": f32(prm["gamma"], d), "beta": f32(prm["beta"], d)}
         if k in (OpKind.SPATIAL_ATTENTION, OpKind.TEMPORAL_ATTENTION):

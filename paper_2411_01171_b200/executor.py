@@ -61,14 +61,20 @@ GEMM_KINDS = (OpKind.CONV2D, OpKind.TEMPORAL_CONV, OpKind.LINEAR, OpKind.SPATIAL
 class ExecConfig:
     """Device execution knobs.
 
-    spatial_k / temporal_k: slice counts per group (None = the fewest slices
-    whose scratch fits ``scratch_budget``).  gemm_backend: 0 auto (tcgen05
-    where the shape allows, else mma.sync), 1 mma.sync only, 2 tcgen05 only.
+    slicing: "budget" (default) -- per group the fewest slices whose scratch
+    fits ``scratch_budget`` (``spatial_k`` / ``temporal_k`` override the count);
+    "plan" -- the group's own ``SlicePlan`` (grouping.py:121-127): spatial
+    slices are exactly its frame extents, a temporal plan of k_h x k_w tiles
+    runs as the same number of contiguous pixel bands (a band is one row view
+    of the channels-last layout; the output does not depend on the tiling,
+    slicer.py:263-280).  gemm_backend: 0 auto (tcgen05 where the shape allows,
+    else mma.sync), 1 mma.sync only, 2 tcgen05 only.
     """
 
     spatial_k: int | None = None
     temporal_k: int | None = None
     scratch_budget: int = 2 << 30
+    slicing: str = "budget"
     gemm_backend: int = 0
     device: str = "cuda"
     rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
@@ -117,6 +123,8 @@ class Unit:
 
 class Plan:
     """Compiled launch program for one network evaluation (and its rehash tail)."""
+
+    fp32_out = True      # the graph output (the network's eps) is written as fp32 rows
 
     def __init__(self, graph: Graph, grouped: GroupedGraph, dw: D.DeviceWeights, cfg: ExecConfig,
                  emb_channels: int | None = None):
@@ -363,6 +371,7 @@ class Plan:
         return run
 
     def _compile(self):
+        self.slice_counts: dict[str, int] = {}
         self.scratch_need = 0
         self._scratch_users = []
         for kind, ref in self.grouped.schedule:
@@ -473,14 +482,28 @@ class Plan:
         per_frame = 0
         shape = s
         for o in ops:
+            hw = shape.h * shape.w
             if o.kind is OpKind.SPATIAL_ATTENTION:
                 per_frame += sum(r * c * torch.empty((), dtype=dt).element_size()
-                                 for r, c, dt in D.spatial_attention_scratch(HW, HW, C).values())
-            per_frame += shape.h * shape.w * max(shape.c, 8) * 2 * 2
+                                 for r, c, dt in D.spatial_attention_scratch(hw, hw, shape.c).values())
+            out = self.shapes[o.id]
+            # the op's input and output rows (intermediates are bf16; fp32 at most 2x)
+            per_frame += (hw * max(shape.c, 8) + out.h * out.w * max(out.c, 8)) * 2
+            shape = out
         from .parallel import shard_range
         f0, f1 = shard_range(frames, self.cfg.world, self.cfg.rank)
-        k = self._k_for(per_frame, f1 - f0, self.cfg.spatial_k)
-        slices = [(a + f0, b + f0) for a, b in balanced(f1 - f0, k)]
+        if self.cfg.slicing == "plan" and grp.plan.extents:
+            # the group's own plan (ceil chunks, remainder last), cut to this rank's frames
+            slices, a = [], 0
+            for e in grp.plan.extents:
+                lo, hi = max(a, f0), min(a + e, f1)
+                if lo < hi:
+                    slices.append((lo, hi))
+                a += e
+        else:
+            k = self._k_for(per_frame, f1 - f0, self.cfg.spatial_k)
+            slices = [(a + f0, b + f0) for a, b in balanced(f1 - f0, k)]
+        self.slice_counts[grp.label] = len(slices)
         fmax = max([b - a for a, b in slices] + [1])
         tail = ops[-1].id
         x_id = grp.head_input
@@ -533,7 +556,7 @@ class Plan:
             specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
         scratch = self._scratch(specs)
-        eps_out = tail == self.graph.outputs[0]
+        eps_out = self.fp32_out and tail == self.graph.outputs[0]
 
         def run(st):
             for sl in slices:
@@ -603,8 +626,12 @@ class Plan:
             per_pix += B * T * C * 2 * (4 if o.kind is OpKind.TEMPORAL_ATTENTION else 1)
         from .parallel import shard_range
         p0, p1 = shard_range(HW, self.cfg.world, self.cfg.rank)
-        k = self._k_for(per_pix, p1 - p0, self.cfg.temporal_k)
+        if self.cfg.slicing == "plan" and grp.plan.row_extents:
+            k = max(1, min(grp.plan.n_slices, p1 - p0))
+        else:
+            k = self._k_for(per_pix, p1 - p0, self.cfg.temporal_k)
         bands = [(a + p0, b + p0) for a, b in balanced(p1 - p0, k)]
+        self.slice_counts[grp.label] = len(bands)
         pmax = max([b - a for a, b in bands] + [1])
         tail = ops[-1].id
         x_id = grp.head_input
@@ -723,6 +750,91 @@ class Plan:
         return sum(u.gemm_flops for u in self.tail_units)
 
 
+class _GroupPlan(Plan):
+    """The launch program of one operator group over standalone input/output rows (execute_group)."""
+
+    fp32_out = False
+
+    def __init__(self, group, in_shape: Shape5, weights, cfg: ExecConfig):
+        graph = Graph(list(group.ops), {group.head_input: in_shape}, [group.tail])
+        self.graph, self.cfg = graph, cfg
+        self.grouped = GroupedGraph(graph, (group,), (), (("group", 0),))
+        self.dw = D.DeviceWeights(graph, weights, cfg.device)
+        self.dev = self.dw.dev
+        self.shapes = infer_shapes(graph)
+        self.topo = graph.topo_order()
+        self.pos = {n: i for i, n in enumerate(self.topo)}
+        self.cons = graph.consumers()
+        self.values, self.fused_adds, self.epilogue_of, self.units, self.emb_nodes = {}, {}, {}, [], []
+        self.exchanger = None
+        so = self.shapes[group.tail]
+        self.inp = torch.empty(in_shape.rows, in_shape.c, dtype=torch.bfloat16, device=self.dev)
+        self.out = torch.empty(so.rows, so.c, dtype=torch.bfloat16, device=self.dev)
+        self.values[group.head_input] = Value(group.head_input, in_shape, tensor=self.inp)
+        self.values[group.tail] = Value(group.tail, so, tensor=self.out)
+        self.latent = torch.empty(in_shape.rows, in_shape.c, dtype=torch.float32, device=self.dev) \
+            if group.head_input == "x" else None
+        self.eps = None
+        self._compile()
+
+
+_GROUP_PLANS: dict = {}
+
+
+def execute_group(group, x, weights, ledger=None, cfg: ExecConfig | None = None) -> Tensor5D:
+    """One operator group on the device, slice by slice (grouping.py:223-254).
+
+    Same contract as the reference's ``execute_group(group, x, weights, ledger)``:
+    ``x`` is the group's full input (a Tensor5D of either package), the result a
+    fresh Tensor5D of the group's output in ``x``'s dtype.  The group's own
+    ``SlicePlan`` sets the slices (``ExecConfig(slicing="plan")``; a caller's
+    ``cfg`` may choose the budget planner instead).  The ledger sees the output
+    buffer (kept, like the reference) and the slice scratch of the group
+    (released when the group completes) -- the device analog of the
+    reference's output + per-stage slots.  The compiled launch program is
+    cached per (group, input shape, weights).
+    """
+    from . import ops
+    from .interop import as_array, as_group
+    grp = as_group(group)
+    xa = as_array(x)
+    shape = Shape5(*xa.shape)
+    out_dtype = xa.dtype if xa.dtype in (np.float32, np.float64) else np.float32
+    if len(grp.ops) == 1 and grp.head_input == "step_emb":
+        # the step-embedding projection (a (b,t,c,1,1) input): one per-op launch
+        op = grp.ops[0]
+        y = ops.apply_kernel(op.kind, [Tensor5D(xa)], weights.get(op.param_ref), op.attrs)
+        if ledger is not None:
+            ledger.alloc(y.data.astype(out_dtype).nbytes, op.label)
+        return Tensor5D(y.data.astype(out_dtype))
+    cfg = cfg or ExecConfig(slicing="plan")
+    key = (grp.label, grp.nodes, tuple(shape), id(weights), cfg.slicing, cfg.scratch_budget, cfg.spatial_k,
+           cfg.temporal_k, cfg.gemm_backend)
+    hit = _GROUP_PLANS.get(key)
+    if hit is None or hit[0] is not weights:
+        ops._dev()
+        if len(_GROUP_PLANS) > 64:
+            _GROUP_PLANS.clear()
+        hit = (weights, _GroupPlan(grp, shape, weights, cfg))
+        _GROUP_PLANS[key] = hit
+    plan = hit[1]
+    st = torch.cuda.current_stream().cuda_stream
+    if plan.latent is not None:
+        plan.latent.copy_(ops.to_rows(Tensor5D(xa), torch.float32))
+    else:
+        plan.inp.copy_(ops.to_rows(Tensor5D(xa)))
+    out_shape = plan.shapes[grp.tail]
+    if ledger is not None:
+        ledger.alloc(out_shape.count() * np.dtype(out_dtype).itemsize, grp.ops[-1].label)
+        ledger.alloc(plan.scratch_bytes, f"{grp.label}:slice_scratch")
+    for u in plan.units:
+        u.run(st)
+    y = ops.from_rows(plan.out, out_shape)
+    if ledger is not None:
+        ledger.free(plan.scratch_bytes, f"{grp.label}:slice_scratch")
+    return Tensor5D(y.data.astype(out_dtype))
+
+
 def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = None) -> dict:
     """Arena / scratch bytes the device plan would reserve, computed without a GPU.
 
@@ -772,9 +884,13 @@ class DeviceModel:
         if not torch.cuda.is_available():
             from .errors import NativeError
             raise NativeError("no CUDA device: the sliceflow_b200 path has no CPU fallback")
+        from .interop import as_graph, as_grouped
         self.cfg = cfg or ExecConfig()
+        graph = as_graph(graph)
         self.graph = graph
         self.unet_cfg = unet_cfg
+        if grouped is not None:
+            grouped = as_grouped(grouped)
         if grouped is None:
             xs = graph.inputs["x"]
             grouped = group_operators(graph, xs.b * xs.t, default_temporal_config(xs.h, xs.w))
@@ -849,17 +965,17 @@ def execute(graph_or_grouped, mode, inputs, weights, cfg: ExecConfig | None = No
     frames and stitches them along t -- the divergent
     baseline the slicer avoids.
     """
-    mode = ExecMode(mode)
-    cfg = cfg or ExecConfig()
+    from .interop import as_array, as_graph_or_grouped, as_mode
+    mode = as_mode(mode)
+    graph, grouped = as_graph_or_grouped(graph_or_grouped)
+    if cfg is None:
+        # a caller-built GroupedGraph carries its slice plans: honour them (grouping.py:223-254)
+        cfg = ExecConfig(slicing="plan") if grouped is not None else ExecConfig()
     if mode is ExecMode.REFERENCE or mode is ExecMode.NAIVE_CLIP:
         cfg = ExecConfig(spatial_k=1, temporal_k=1, scratch_budget=cfg.scratch_budget,
                          gemm_backend=cfg.gemm_backend, device=cfg.device)
-    if isinstance(graph_or_grouped, GroupedGraph):
-        graph, grouped = graph_or_grouped.graph, graph_or_grouped
-    else:
-        graph, grouped = graph_or_grouped, None
-    x = inputs["x"].data if isinstance(inputs["x"], Tensor5D) else np.asarray(inputs["x"])
-    se = inputs["step_emb"].data if isinstance(inputs["step_emb"], Tensor5D) else np.asarray(inputs["step_emb"])
+    x = as_array(inputs["x"])
+    se = as_array(inputs["step_emb"])
     vec = np.ascontiguousarray(se.reshape(-1, se.shape[2])[0], dtype=np.float32)
     if not np.all(se.reshape(-1, se.shape[2]) == vec[None]):
         raise ShapeMismatch("device path expects the step embedding broadcast over (b, t) (unet.py:106-113)")

@@ -65,6 +65,8 @@ def make_plan(domain: Domain, in_shape: Shape5, spatial_k: int, temporal_cfg: tu
 
 def group_operators(graph: Graph, spatial_k: int, temporal_cfg: tuple[int, int]) -> GroupedGraph:
     """Greedy maximal chains of same-domain, losslessly sliceable ops (grouping.py:130-200)."""
+    from .interop import as_graph
+    graph = as_graph(graph)
     if spatial_k < 1:
         raise InvalidParam(f"spatial_k must be >= 1, got {spatial_k}")
     if min(temporal_cfg) < 1:
@@ -237,10 +239,10 @@ def _grouped_peak(gg: GroupedGraph, itemsize: int) -> int:
 
 def estimate_peak_memory(g, mode, dtype="float32", naive_chunk: int | None = None) -> int:
     """Static liveness peak of one evaluation (grouping.py:334-364)."""
-    mode = ExecMode(mode)
+    from .interop import as_graph_or_grouped, as_mode
+    mode = as_mode(mode)
     itemsize = np.dtype(resolve_dtype(dtype)).itemsize if dtype not in ("bfloat16", "bf16") else 2
-    grouped = g if isinstance(g, GroupedGraph) else None
-    graph = g.graph if grouped else g
+    graph, grouped = as_graph_or_grouped(g)
     if mode in (ExecMode.SLICED_LOOP, ExecMode.PIPELINED):
         if grouped is None:
             raise ShapeInferenceFailure(f"{mode.value} requires a GroupedGraph")
@@ -267,6 +269,8 @@ def estimate_peak_memory(g, mode, dtype="float32", naive_chunk: int | None = Non
 
 def grouped_graph_report(gg: GroupedGraph, dtype="float32") -> dict:
     """JSON summary per group (grouping.py:457-476)."""
+    from .interop import as_grouped
+    gg = as_grouped(gg)
     itemsize = np.dtype(resolve_dtype(dtype)).itemsize
     shapes = infer_shapes(gg.graph)
     rows = [{"label": g.label, "nodes": list(g.nodes), "node_count": len(g.nodes), "domain": g.domain.value,

@@ -78,6 +78,9 @@ class Denoiser:
         self.cfg = cfg
         self.reuse_donor_eps = reuse_donor_eps
         self.K = K or cfg.steps
+        if graph is not None:
+            from .interop import as_graph
+            graph = as_graph(graph)
         if graph is None:
             graph, w64 = build_toy_unet(cfg)
             weights = w64
@@ -263,15 +266,17 @@ def _model_inputs(cfg: DenoiseRunConfig):
         raise InvalidParam("a saved graph and its weight bundle are given together")
     if cfg.graph is None:
         return None, None
+    from .interop import as_graph
+    graph = as_graph(cfg.graph)
     want = cfg.unet.input_shape()
-    got = cfg.graph.inputs.get("x")
+    got = graph.inputs.get("x")
     if got is None or tuple(got) != tuple(want):
         raise InvalidParam(f"graph input x {tuple(got) if got is not None else None} does not match the "
                            f"config's latent {tuple(want)}")
-    for n in cfg.graph.nodes.values():
+    for n in graph.nodes.values():
         if n.param_ref is not None:
             cfg.weights.get(n.param_ref)          # InvalidParam names a missing entry
-    return cfg.graph, cfg.weights
+    return graph, cfg.weights
 
 
 def run_denoise(cfg: DenoiseRunConfig) -> tuple[Tensor5D, RunReport]:
@@ -360,7 +365,8 @@ def _run_naive_clip(cfg: DenoiseRunConfig, ucfg: UNetConfig, K: int, ex: ExecCon
 def rehash_execute(graph: Graph, weights, schedule: StepSchedule, inputs, cfg: UNetConfig,
                    exec_cfg: ExecConfig | None = None):
     """Run the K-step loop under ``schedule`` -> (output, op_count_report)."""
+    from .interop import as_array
     den = Denoiser(cfg, exec_cfg, graph=graph, weights=weights, K=schedule.K)
-    x0 = inputs["x"].data if isinstance(inputs["x"], Tensor5D) else np.asarray(inputs["x"])
+    x0 = as_array(inputs["x"])
     x = den.run(x0, schedule)
     return Tensor5D(x), op_count_report(graph, schedule, den.tail_node_count())

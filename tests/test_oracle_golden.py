@@ -160,3 +160,24 @@ def test_oracle_c1_denoise_matches_reference(golden, dt, tol):
 def test_slicing_is_lossless_fp64(golden):
     runs = golden["runs"]
     assert _rel(runs["c1_float64_eps0"], runs["c1_float64_eps0_unsliced"]) < 1e-12
+
+
+def test_torch_ref_pinned_to_goldens(golden):
+    """oracle/torch_ref.py (the fp64 checker used at C2/C3 on the GPU) against the reference's own
+    fp64 runs: C1 10-step all-key run, its similarity map, eps at s=0, the gamma=0.93 rehash run,
+    and the base-64 WIDE run.  Bar: <= 1e-12 (measured ~1e-15)."""
+    from oracle import torch_ref as TR
+    runs = golden["runs"]
+    ref = TR.TorchRef(C1)
+    x, S, eps = TR.run_full(ref, eps_steps=(0,))
+    assert _rel(x.numpy(), runs["c1_float64_final"]) <= 1e-12
+    assert float(np.abs(S - runs["c1_float64_S"]).max()) <= 1e-12
+    assert _rel(eps[0].numpy(), runs["c1_float64_eps0"]) <= 1e-12
+    xr = TR.run_rehash(ref, golden["meta"]["c1_G"]["0.93"])
+    assert _rel(xr.numpy(), runs["c1_float64_rehash_g093_final"]) <= 1e-12
+    for g, G in golden["meta"]["c1_G"].items():
+        assert key_step_search(S, float(g)) == G, g
+    wide = UNetConfig(channels=4, frames=4, height=16, width=16, base_channels=64, norm_groups=32, steps=3)
+    xw, _, ew = TR.run_full(TR.TorchRef(wide), eps_steps=(0,))
+    assert _rel(xw.numpy(), runs["wide_float64_final"]) <= 1e-12
+    assert _rel(ew[0].numpy(), runs["wide_float64_eps0"]) <= 1e-12
