@@ -169,10 +169,94 @@ def run_reference(args, world, rank):
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": host_cores(), "kind": "port",
                          "sample": "first slice of every group (scaled by slice count) for one key step and one "
-                                   f"tail step, extrapolated to {nk}/{K}; {np.mean(samples):.1f} s CPU per sample"},
+                                   f"tail step, extrapolated to {nk}/{K}; {np.mean(samples):.1f} s CPU per sample "
+                                   f"= {100 * smp['fraction']:.1f}% of the extrapolated step time actually run"},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def parity_check(config, S, sched) -> dict | None:
+    """Live check of this run's Step Rehash decision against the committed fp64-oracle record.
+
+    ``profiles/r02_parity_<config>.json`` (tests/parity_sd.py, run on a B200) holds the
+    oracle's own 25 x 25 similarity map S_ref and key steps, and the measured
+    eps / latent errors.  Here the calibration map of THIS run is compared with S_ref
+    and A1 is run on S_ref at this run's gamma: identical G means this run's
+    schedule is the reference's.
+    """
+    from paper_2411_01171_b200.rehash import key_step_search
+    path = os.path.join(ROOT, "profiles", f"r02_parity_{config}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        rec = json.load(fh)
+    S_ref = np.asarray(rec["S_ref"])
+    if S_ref.shape != S.values.shape:
+        return None
+    G_ref = key_step_search(S_ref, sched.gamma).key_steps
+    return {"oracle": rec["oracle"], "record": os.path.relpath(path, ROOT),
+            "G_oracle_at_gamma": G_ref, "G_match": list(G_ref) == list(sched.key_steps),
+            "s_err_live": float(np.abs(S.values - S_ref).max()),
+            "margin_oracle": key_step_search(S_ref, sched.gamma).margin,
+            "recorded": {k: rec[k] for k in ("eps0_max_rel", "eps0_rms_rel", "x_allkey_max_rel", "x_rehash_max_rel",
+                                             "update_rehash_max_rel", "s_err") if k in rec},
+            "tolerance": "G identical; S err <= 1e-3; denoised latent max_rel <= 2e-3; one-evaluation eps "
+                         "max_rel <= 2e-2 (bf16-storage floor, tests/test_gpu_parity_sd.py)"}
+
+
+def slice_summary(plan) -> dict:
+    """Realised slices per group of the compiled plan (Feature Slicer + budget)."""
+    counts = plan.slice_counts
+    hist: dict[int, int] = {}
+    for n in counts.values():
+        hist[n] = hist.get(n, 0) + 1
+    return {"policy": f"{plan.cfg.slicing}" + (f" (scratch budget {plan.cfg.scratch_budget >> 20} MiB)"
+                                               if plan.cfg.slicing == "budget" else ""),
+            "groups": len(counts), "sliced_groups": sum(1 for n in counts.values() if n > 1),
+            "max_slices": max(counts.values()) if counts else 0,
+            "groups_by_slice_count": {str(k): v for k, v in sorted(hist.items())}}
+
+
+def north_star_plan(args, cfg, den, sched, x0) -> dict:
+    """The north star's slice plan: one frame per spatial slice and T pixel bands per temporal
+    group (a band of HW/T pixels x all T frames = one frame's worth of rows), same weights and
+    schedule.  Reports its throughput and peak HBM next to the headline plan's."""
+    import torch
+    from paper_2411_01171_b200.executor import ExecConfig
+    from paper_2411_01171_b200.harness import Denoiser
+    dw = den.model.dw
+    bt = cfg.frames * cfg.effective_batch
+    ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=bt, temporal_k=bt)
+    # drop the headline plan's buffers (weights are shared) before measuring this plan's peak
+    import gc
+    den._graphs.clear()
+    den.plan = den.model.plan = None
+    gc.collect()
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats()
+    d2 = Denoiser(cfg, ecfg, device_weights=dw)
+    key = d2.prepare(sched)
+    d2.set_latent(x0)
+    x0_rows = d2.plan.latent.clone()
+    for _ in range(2):
+        d2.plan.latent.copy_(x0_rows)
+        d2.launch(key)
+    torch.cuda.synchronize()
+    n = max(2, min(args.steps, 5))
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(n):
+        d2.plan.latent.copy_(x0_rows)
+        d2.launch(key)
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / n
+    return {"plan": f"spatial k = {bt} (one frame per slice), temporal k = {bt} pixel bands",
+            "value": round(cfg.steps / (ms / 1e3), 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
+            "runs": n, "peak_hbm_bytes": int(torch.cuda.max_memory_allocated()),
+            "arena_bytes": d2.plan.arena_bytes, "scratch_bytes": d2.plan.scratch_bytes,
+            "slices": slice_summary(d2.plan), "gpu_launches_per_run": d2.launches[key]}
 
 
 def run_ours(args, world, rank, local):
@@ -191,8 +275,11 @@ def run_ours(args, world, rank, local):
     if world > 1:
         from paper_2411_01171_b200.parallel import NcclExchanger
         exchanger = NcclExchanger(rank, world)
-    den = Denoiser(cfg, ExecConfig(gemm_backend=args.backend, spatial_k=args.spatial_k, temporal_k=args.temporal_k,
-                                   rank=rank, world=world), exchanger=exchanger)
+    ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=args.spatial_k, temporal_k=args.temporal_k,
+                      rank=rank, world=world)
+    if args.scratch_budget_mb:
+        ecfg.scratch_budget = args.scratch_budget_mb << 20
+    den = Denoiser(cfg, ecfg, exchanger=exchanger)
     x0 = initial_latent(cfg)
     # calibration (setup, untimed): all-key run recording the probe, then A1
     t_cal = time.perf_counter()
@@ -202,6 +289,7 @@ def run_ours(args, world, rank, local):
     nk = n_target_keys(K)
     gamma = args.gamma if args.gamma else gamma_for_target(S, nk)
     sched = key_step_search(S, gamma, K)
+    parity = parity_check(args.config, S, sched)
     den.trace = None
     torch.cuda.empty_cache()
     key = den.prepare(sched)
@@ -318,6 +406,10 @@ def run_ours(args, world, rank, local):
                                 "tflops": round(v["tflops"], 1)} for k, v in list(pf["by_call"].items())[:8]}},
         "setup_s": round(setup_s, 2), "calibration_s": round(t_cal, 2),
     }
+    line["parity"] = parity
+    line["config"]["slices"] = slice_summary(den.plan)
+    if world == 1 and not args.no_north_star_plan:
+        line["north_star_plan"] = north_star_plan(args, cfg, den, sched, x0)
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle.cpu_baseline import CpuBaseline, host_cores
         cb = CpuBaseline(cfg)
@@ -326,9 +418,21 @@ def run_ours(args, world, rank, local):
             "value": round(cb.steps_per_s(len(sched.key_steps), K, smp), 6), "unit": "steps/s",
             "cores": host_cores(), "kind": "port",
             "sample": f"oracle fp32 SlicedLoop: first slice of every group scaled by slice count, one key + one "
-                      f"tail step extrapolated to {len(sched.key_steps)}/{K}; {smp['sample_s']:.1f} s CPU"}
+                      f"tail step extrapolated to {len(sched.key_steps)}/{K}; {smp['sample_s']:.1f} s CPU = "
+                      f"{100 * smp['fraction']:.1f}% of the extrapolated step time actually run"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(n: int):
+    """``--gpus N`` without a torchrun environment: re-exec this script under torch.distributed.run."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execvp(cmd[0], cmd)
 
 
 def main():
@@ -343,7 +447,11 @@ def main():
     ap.add_argument("--spatial-k", type=int, default=None)
     ap.add_argument("--temporal-k", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scratch-budget-mb", type=int, default=None)
+    ap.add_argument("--no-north-star-plan", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     world, rank, local = dist_setup(args.gpus)
     if args.impl == "reference":
         run_reference(args, world, rank)

@@ -54,8 +54,11 @@ class CpuBaseline:
         evaluate(m.graph, m.weights, {self.probe_id: cap[PROBE_LABEL]}, ExecMode.SLICED_LOOP, m.grouped,
                  start_after=self.probe_id, max_slices=self.max_slices, timing=t_tail)
         t2 = time.perf_counter()
+        run = sum(t[1] for t in t_full + t_tail)
+        extrap = sum(t[2] for t in t_full + t_tail)
         return {"full_s": sum(t[2] for t in t_full), "tail_s": sum(t[2] for t in t_tail),
-                "sample_s": t2 - t0, "sample_full_s": t1 - t0}
+                "sample_s": t2 - t0, "sample_full_s": t1 - t0,
+                "fraction": run / extrap if extrap else 1.0}   # share of the extrapolated time actually run
 
     def steps_per_s(self, n_keys: int, K: int, sample: dict) -> float:
         run_s = n_keys * sample["full_s"] + (K - n_keys) * sample["tail_s"]

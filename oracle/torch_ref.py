@@ -232,8 +232,10 @@ def similarity_from_gram(G):
 
 
 @torch.no_grad()
-def run_full(ref: TorchRef, K=None, keep_probes=True, eps_steps=()):
-    """All-key K-step loop: (final x, S map, {s: eps_s} for s in eps_steps)."""
+def run_full(ref: TorchRef, K=None, keep_probes=True, eps_steps=(), probe_sink=None):
+    """All-key K-step loop: (final x, S map, {s: eps_s} for s in eps_steps).
+
+    ``probe_sink`` (a list) receives the K fp64 probe tensors."""
     K = K or ref.cfg.steps
     x = ref.initial_latent()
     probes, epss = [], {}
@@ -246,6 +248,8 @@ def run_full(ref: TorchRef, K=None, keep_probes=True, eps_steps=()):
         x = x - ref.alpha(s, K) * e
         del e, cap
     S = similarity_from_gram(gram(probes)) if keep_probes else None
+    if probe_sink is not None:
+        probe_sink.extend(probes)
     return x, S, epss
 
 

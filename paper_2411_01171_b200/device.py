@@ -256,11 +256,13 @@ def use_flash(HW, C) -> bool:
 
 def spatial_attention_scratch(rows, HW, C) -> dict:
     """Slice scratch the spatial attention lowering needs: {name: (rows, cols, dtype)}."""
-    out = {"qkv": (rows, 3 * C, torch.bfloat16), "o": (rows, C, torch.bfloat16)}
+    flash = HW > SMALL_SEQ and use_flash(HW, C)
+    # the fused core reads q|k from a 2C-wide buffer and V^T from its own (spatial_attention)
+    out = {"qkv": (rows, (2 if flash else 3) * C, torch.bfloat16), "o": (rows, C, torch.bfloat16)}
     frames = rows // HW
     if HW > SMALL_SEQ:
         out["vt"] = (frames * C, HW, torch.bfloat16)
-        if not use_flash(HW, C):
+        if not flash:
             out["s"] = (rows, HW, torch.float32)
             out["p"] = (rows, HW, torch.bfloat16)
     return out

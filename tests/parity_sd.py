@@ -84,7 +84,12 @@ def run(name: str, exec_cfg: ExecConfig | None = None, log=print) -> dict:
 
     t1 = time.perf_counter()
     ref = TR.TorchRef(cfg, "cuda")
-    x_allkey_ref, S_ref, eps = TR.run_full(ref, eps_steps=(0,))
+    probes = []
+    x_allkey_ref, S_ref, eps = TR.run_full(ref, eps_steps=(0,), probe_sink=probes)
+    # how much of the S error bf16 storage of the probe alone would explain: the oracle's own
+    # fp64 probes rounded to bf16, Gram in fp64
+    S_ref_bf16probe = TR.similarity_from_gram(TR.gram([p.to(torch.bfloat16).double() for p in probes]))
+    del probes
     eps0_ref = eps[0].cpu().numpy()
     x_allkey_ref = x_allkey_ref.cpu().numpy()
     G_ref = key_step_search(S_ref, gamma).key_steps
@@ -95,12 +100,23 @@ def run(name: str, exec_cfg: ExecConfig | None = None, log=print) -> dict:
     log(f"[{name}] oracle done in {t_ref:.1f} s")
 
     s_err = float(np.abs(S_dev.values - S_ref).max())
+    fixed = {}
+    for g in (0.90, 0.93, 0.95, 0.97):
+        sr, sd = key_step_search(S_ref, g), key_step_search(S_dev.values, g)
+        fixed[f"{g:.2f}"] = {"G_ref": list(sr.key_steps), "G_dev": list(sd.key_steps),
+                             "match": list(sr.key_steps) == list(sd.key_steps), "margin_ref": sr.margin}
+    x0d = x0.astype(np.float64)
     rec = {
         "config": name, "unet": CONFIGS[name], "K": K, "target_keys": nk,
         "eps0_max_rel": rel(eps0_dev, eps0_ref), "eps0_max_abs": float(np.abs(eps0_dev - eps0_ref).max()),
+        "eps0_rms_rel": float(np.sqrt(np.mean((eps0_dev - eps0_ref) ** 2) / np.mean(eps0_ref ** 2))),
+        "update_allkey_max_rel": rel(x_allkey_dev - x0d, x_allkey_ref - x0d),
+        "update_rehash_max_rel": rel(x_rehash_dev - x0d, x_rehash_ref - x0d),
         "x_allkey_max_rel": rel(x_allkey_dev, x_allkey_ref),
         "x_allkey_max_abs": float(np.abs(x_allkey_dev - x_allkey_ref).max()),
         "s_err": s_err,
+        "s_err_bf16_probe_storage_only": float(np.abs(S_ref_bf16probe - S_ref).max()),
+        "fixed_gamma": fixed,
         "gamma": gamma, "G_dev": list(G_dev), "G_ref": list(G_ref), "G_match": list(G_dev) == list(G_ref),
         "margin_ref": a1_margin(S_ref, gamma), "margin_dev": a1_margin(S_dev.values, gamma),
         "gamma_ref_target": gamma_ref, "G_ref_target": list(G_ref_target),

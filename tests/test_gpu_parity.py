@@ -2,10 +2,14 @@
 
 Tolerances (stated per test) are for bf16 activation storage with fp32
 accumulation against the fp64 reference:
-  * single kernels: max_rel <= 1.5e-2 (one bf16 rounding of inputs+output);
-  * a full 10-step toy denoise: final-latent max_rel <= 2e-2;
-  * Step Rehash schedule: identical key steps G at a gamma whose decision
-    margin exceeds the measured similarity error.
+  * single kernels: max_rel <= 1e-2 (bf16 rounding of inputs + output; measured 2.5e-3..6.4e-3);
+  * a full 10-step toy denoise: final-latent max_rel <= 5e-3 (measured 4.0e-4);
+  * similarity map: max abs err <= 2e-3 (measured 3.3e-4 C1, 1.4e-3 SPEC default toy);
+  * Step Rehash schedule: identical key steps G at every gamma of the reference's
+    C1 goldens (decision margins >= 1.6e-3, 5x the similarity error) and at the
+    target-count gamma; at the SPEC default toy wherever the margin exceeds 2x
+    the measured similarity error.
+SD widths (C2/C3) are in test_gpu_parity_sd.py.
 """
 
 import json
@@ -50,7 +54,7 @@ def test_kernels_match_reference_vectors(golden):
         y = ops.apply_kernel(kind, [Tensor5D(kv[f"{key}/x"])], params, attrs)
         worst[key] = rel(y.data, kv[f"{key}/y"])
     print(worst)
-    assert max(worst.values()) <= 1.5e-2, worst
+    assert max(worst.values()) <= 1e-2, worst
     y = ops.apply_kernel(OpKind.ADD, [Tensor5D(kv["add_bias/a"]), Tensor5D(kv["add_bias/b"])])
     assert rel(y.data, kv["add_bias/y"]) <= 1e-2
     y = ops.apply_kernel(OpKind.CONCAT, [Tensor5D(kv["concat/a"]), Tensor5D(kv["concat/b"])])
@@ -103,7 +107,7 @@ def test_sd_width_kernels_vs_oracle(case, backend):
     y = ops.apply_kernel(kind, [Tensor5D(x)], p, attrs, backend=backend)
     r = rel(y.data, ref)
     print(case, backend, r)
-    assert r <= 1.5e-2
+    assert r <= 1e-2
 
 
 @pytest.fixture(scope="module")
@@ -118,13 +122,14 @@ def test_c1_full_denoise_matches_reference(golden, c1_denoiser):
     r = rel(x, runs["c1_float64_final"])
     s_err = float(np.abs(S.values - runs["c1_float64_S"]).max())
     print("c1 final rel", r, "S err", s_err)
-    assert r <= 2e-2
-    assert s_err <= 5e-3
-    # identical schedule wherever the decision margin exceeds the similarity error
+    assert r <= 5e-3
+    assert s_err <= 2e-3
+    # identical schedule at every golden gamma (unconditional) and at the target-count gamma
     for g, G in golden["meta"]["c1_G"].items():
-        sch = key_step_search(runs["c1_float64_S"], float(g))
-        if sch.margin is not None and sch.margin > 2 * s_err:
-            assert key_step_search(S, float(g)).key_steps == G, g
+        assert key_step_search(S, float(g)).key_steps == G, g
+    from paper_2411_01171_b200.rehash import gamma_for_target
+    gt = gamma_for_target(S, 6)
+    assert key_step_search(S, gt).key_steps == key_step_search(runs["c1_float64_S"], gt).key_steps
 
 
 def test_c1_rehash_matches_reference(golden, c1_denoiser):
@@ -133,7 +138,7 @@ def test_c1_rehash_matches_reference(golden, c1_denoiser):
     x = c1_denoiser.run(initial_latent(C1), StepSchedule(G, 10))
     r = rel(x, runs["c1_float64_rehash_g093_final"])
     print("c1 rehash rel", r)
-    assert r <= 2e-2
+    assert r <= 5e-3
 
 
 def test_all_key_schedule_is_bit_identical(c1_denoiser):
@@ -162,14 +167,14 @@ def test_wide_config_matches_reference(golden):
     x = den.run(initial_latent(WIDE), None)
     r = rel(x, runs["wide_float64_final"])
     print("wide final rel", r)
-    assert r <= 2e-2
+    assert r <= 5e-3
 
 
 def test_spec_default_toy_matches_reference(golden):
     """Second parity point (SURVEY.md §8 config note): the SPEC default toy
     UNetConfig() = c=8, 8 frames, 32x32, K=25 (unet.py:41-55),
     against the reference's own fp32 run (tests/golden/make_golden.py).
-    Tolerances: final latent max_rel <= 2e-2, similarity map max abs err <= 5e-3,
+    Tolerances: final latent max_rel <= 5e-3, similarity map max abs err <= 2e-3,
     identical key steps G wherever A1's decision margin exceeds 2x that error."""
     runs = golden["runs"]
     cfg = UNetConfig()
@@ -178,8 +183,8 @@ def test_spec_default_toy_matches_reference(golden):
     s_ref = runs["default_float32_S"]
     s_err = float(np.abs(S.values - s_ref).max())
     print("default final rel", r, "S err", s_err)
-    assert r <= 2e-2
-    assert s_err <= 5e-3
+    assert r <= 5e-3
+    assert s_err <= 2e-3
     checked = 0
     for g in np.linspace(max(float(s_ref.min()), 0.05), 0.999, 24):
         sch = key_step_search(s_ref, float(g))
