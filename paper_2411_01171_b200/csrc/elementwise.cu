@@ -1138,61 +1138,6 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int nparts, in
   }
 }
 
-// Gram: each block covers a slice of the element range for every (i<=j) pair
-constexpr int GRAM_BLOCKS = 296;
-__global__ void gram_partial_kernel(const bf16* const* __restrict__ probes, int K, int64_t n,
-                                    double* __restrict__ part) {
-  griddep_wait();
-  griddep_trigger();
-  const int npairs = K * (K + 1) / 2;
-  const int64_t nv = n / 8;
-  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
-  const int64_t v0 = blockIdx.x * per, v1 = min(nv, v0 + per);
-  __shared__ double red[DOT_THREADS / 32];
-  for (int pr = 0; pr < npairs; ++pr) {
-    int i = 0, rem = pr;
-    while (rem >= K - i) {
-      rem -= K - i;
-      ++i;
-    }
-    int j = i + rem;
-    double acc = 0;
-    for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-      float fa[8], fb[8];
-      unpack8(reinterpret_cast<const bf16x8*>(probes[i])[v], fa);
-      unpack8(reinterpret_cast<const bf16x8*>(probes[j])[v], fb);
-      float s = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s += fa[k] * fb[k];
-      acc += s;
-    }
-    if (blockIdx.x == 0)
-      for (int64_t e = nv * 8 + threadIdx.x; e < n; e += blockDim.x)
-        acc += (double)__bfloat162float(probes[i][e]) * __bfloat162float(probes[j][e]);
-    acc = warp_sum_d(acc);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0;
-      for (int w = 0; w < DOT_THREADS / 32; ++w) s += red[w];
-      part[(int64_t)blockIdx.x * npairs + pr] = s;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void gram_finalize_kernel(const double* __restrict__ sums, int K, double* __restrict__ out) {
-  griddep_wait();
-  griddep_trigger();
-  int pr = 0;
-  for (int i = 0; i < K; ++i)
-    for (int j = i; j < K; ++j, ++pr)
-      if (threadIdx.x == 0) {
-        out[i * K + j] = sums[pr];
-        out[j * K + i] = sums[pr];
-      }
-}
-
 static int ew_grid(int64_t total, int threads) {
   int64_t g = (total + threads - 1) / threads;
   int64_t cap = (int64_t)num_sms() * 16;
@@ -1475,21 +1420,5 @@ sf_status sf_dot3_bf16(const void* a, const void* b, int64_t n, void* work, doub
   return launch_status("sf_dot3_bf16");
 }
 
-int64_t sf_gram_workspace(int32_t K, int64_t n) {
-  int64_t npairs = (int64_t)K * (K + 1) / 2;
-  return (GRAM_BLOCKS + 1) * npairs * (int64_t)sizeof(double);
-}
-
-sf_status sf_gram_bf16(const void* const* probes, int32_t K, int64_t n, void* work, double* out, void* stream) {
-  SF_CHECK_ARG(K >= 1 && n >= 1, SF_ERR_SHAPE, "bad extents");
-  cudaStream_t st = (cudaStream_t)stream;
-  int npairs = K * (K + 1) / 2;
-  double* part = (double*)work;
-  double* sums = part + (int64_t)GRAM_BLOCKS * npairs;
-  launch_k(gram_partial_kernel, dim3(GRAM_BLOCKS), dim3(DOT_THREADS), 0, st, (const bf16* const*)probes, K, n, part);
-  launch_k(sum_parts_kernel, dim3(1), dim3(256), 0, st, part, GRAM_BLOCKS, npairs, sums);
-  launch_k(gram_finalize_kernel, dim3(1), dim3(32), 0, st, sums, K, out);
-  return launch_status("sf_gram_bf16");
-}
 
 }  // extern "C"

@@ -73,7 +73,7 @@ class ExecConfig:
 
     spatial_k: int | None = None
     temporal_k: int | None = None
-    scratch_budget: int = 2 << 30
+    scratch_budget: int = 1 << 30
     slicing: str = "budget"
     gemm_backend: int = 0
     device: str = "cuda"
@@ -478,18 +478,55 @@ class Plan:
         HW = s.h * s.w
         backend = self.cfg.gemm_backend
         C = s.c
-        # per-frame scratch estimate of the chain
-        per_frame = 0
+        tail = ops[-1].id
+        x_id = grp.head_input
+        latent_in = x_id == "x"
+
+        def vrows(vid, sl):
+            sh = self.shapes[vid]
+            return self.rows(vid, sl[0] * sh.h * sh.w, sh.h * sh.w)
+
+        epi_fn = self._epilogue(tail, vrows)
+        # lower the chain into steps over slice-local buffers; scratch specs per frame first
+        steps = []
+        pf_specs = {}          # name -> (rows per frame, cols, dtype)
         shape = s
-        for o in ops:
-            hw = shape.h * shape.w
+        cur = "IN"
+        i = 0
+        nb = 0
+        flops = 0.0
+        gn_shapes = []
+        max_groups = max([int(o.attrs.get("groups", 1)) for o in ops if o.kind is OpKind.GROUP_NORM] + [1])
+        while i < len(ops):
+            o = ops[i]
+            nxt = ops[i + 1] if i + 1 < len(ops) else None
+            fuse_act = nxt is not None and nxt.kind is OpKind.SILU
+            last = (i + (2 if fuse_act else 1)) >= len(ops)
+            out_shape = self.shapes[ops[i + (1 if fuse_act else 0)].id]
+            dst = "OUT" if last else f"t{nb}"
+            if not last:
+                pf_specs[dst] = (out_shape.h * out_shape.w, out_shape.c, torch.bfloat16)
+                nb += 1
+            act = N.ACT_SILU if fuse_act else N.ACT_NONE
+            steps.append((o, cur, dst, shape, out_shape, act, last))
+            cur = dst
+            if o.kind is OpKind.CONV2D:
+                flops += 2.0 * frames * out_shape.h * out_shape.w * shape.c * out_shape.c * 9
+            elif o.kind is OpKind.LINEAR:
+                flops += 2.0 * frames * HW * shape.c * out_shape.c
+            elif o.kind is OpKind.SPATIAL_ATTENTION:
+                flops += frames * (8.0 * HW * C * C + 4.0 * HW * HW * C)
+            if o.kind is OpKind.GROUP_NORM:
+                gn_shapes.append(shape)
             if o.kind is OpKind.SPATIAL_ATTENTION:
-                per_frame += sum(r * c * torch.empty((), dtype=dt).element_size()
-                                 for r, c, dt in D.spatial_attention_scratch(hw, hw, shape.c).values())
-            out = self.shapes[o.id]
-            # the op's input and output rows (intermediates are bf16; fp32 at most 2x)
-            per_frame += (hw * max(shape.c, 8) + out.h * out.w * max(out.c, 8)) * 2
-            shape = out
+                hw = shape.h * shape.w
+                pf_specs.update(D.spatial_attention_scratch(hw, hw, shape.c))
+            if o.kind is OpKind.CONV2D and "w_taps" in self.dw.p.get(o.id, {}):
+                pf_specs["taps_y"] = (out_shape.h * out_shape.w, 9 * out_shape.c, torch.float32)
+            shape = out_shape
+            i += 2 if fuse_act else 1
+        # exact per-frame slice scratch of this chain -> slice count under the budget
+        per_frame = sum(r * c * torch.empty((), dtype=dt).element_size() for r, c, dt in pf_specs.values())
         from .parallel import shard_range
         f0, f1 = shard_range(frames, self.cfg.world, self.cfg.rank)
         if self.cfg.slicing == "plan" and grp.plan.extents:
@@ -505,53 +542,8 @@ class Plan:
             slices = [(a + f0, b + f0) for a, b in balanced(f1 - f0, k)]
         self.slice_counts[grp.label] = len(slices)
         fmax = max([b - a for a, b in slices] + [1])
-        tail = ops[-1].id
-        x_id = grp.head_input
-        latent_in = x_id == "x"
-
-        def vrows(vid, sl):
-            sh = self.shapes[vid]
-            return self.rows(vid, sl[0] * sh.h * sh.w, sh.h * sh.w)
-
-        epi_fn = self._epilogue(tail, vrows)
-        # lower the chain into steps over slice-local buffers
-        steps = []
-        specs = {}
-        shape = s
-        cur = "IN"
-        i = 0
-        nb = 0
-        flops = 0.0
-        gn_need = None
-        max_groups = max([int(o.attrs.get("groups", 1)) for o in ops if o.kind is OpKind.GROUP_NORM] + [1])
-        while i < len(ops):
-            o = ops[i]
-            nxt = ops[i + 1] if i + 1 < len(ops) else None
-            fuse_act = nxt is not None and nxt.kind is OpKind.SILU
-            last = (i + (2 if fuse_act else 1)) >= len(ops)
-            out_shape = self.shapes[ops[i + (1 if fuse_act else 0)].id]
-            dst = "OUT" if last else f"t{nb}"
-            if not last:
-                specs[dst] = (fmax * out_shape.h * out_shape.w, out_shape.c, torch.bfloat16)
-                nb += 1
-            act = N.ACT_SILU if fuse_act else N.ACT_NONE
-            steps.append((o, cur, dst, shape, out_shape, act, last))
-            cur = dst
-            if o.kind is OpKind.CONV2D:
-                flops += 2.0 * frames * out_shape.h * out_shape.w * shape.c * out_shape.c * 9
-            elif o.kind is OpKind.LINEAR:
-                flops += 2.0 * frames * HW * shape.c * out_shape.c
-            elif o.kind is OpKind.SPATIAL_ATTENTION:
-                flops += frames * (8.0 * HW * C * C + 4.0 * HW * HW * C)
-            if o.kind is OpKind.GROUP_NORM:
-                gn_need = max(gn_need or 0, N.query("sf_group_norm_workspace", fmax, shape.h * shape.w, shape.c))
-            if o.kind is OpKind.SPATIAL_ATTENTION:
-                hw = shape.h * shape.w
-                specs.update(D.spatial_attention_scratch(fmax * hw, hw, shape.c))
-            if o.kind is OpKind.CONV2D and "w_taps" in self.dw.p.get(o.id, {}):
-                specs["taps_y"] = (fmax * out_shape.h * out_shape.w, 9 * out_shape.c, torch.float32)
-            shape = out_shape
-            i += 2 if fuse_act else 1
+        specs = {k: (fmax * r, c, dt) for k, (r, c, dt) in pf_specs.items()}
+        gn_need = max([N.query("sf_group_norm_workspace", fmax, g.h * g.w, g.c) for g in gn_shapes] or [0])
         if gn_need:
             specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
@@ -621,18 +613,6 @@ class Plan:
     def _compile_temporal(self, grp, ops, kinds, s):
         B, T, HW, C = s.b, s.t, s.h * s.w, s.c
         backend = self.cfg.gemm_backend
-        per_pix = 0
-        for o in ops:
-            per_pix += B * T * C * 2 * (4 if o.kind is OpKind.TEMPORAL_ATTENTION else 1)
-        from .parallel import shard_range
-        p0, p1 = shard_range(HW, self.cfg.world, self.cfg.rank)
-        if self.cfg.slicing == "plan" and grp.plan.row_extents:
-            k = max(1, min(grp.plan.n_slices, p1 - p0))
-        else:
-            k = self._k_for(per_pix, p1 - p0, self.cfg.temporal_k)
-        bands = [(a + p0, b + p0) for a, b in balanced(p1 - p0, k)]
-        self.slice_counts[grp.label] = len(bands)
-        pmax = max([b - a for a, b in bands] + [1])
         tail = ops[-1].id
         x_id = grp.head_input
 
@@ -640,7 +620,7 @@ class Plan:
             return self.rows(vid, band[0], HW)
 
         epi_fn = self._epilogue(tail, vrows)
-        steps, specs = [], {}
+        steps, pp_specs = [], {}        # name -> (rows per pixel, cols, dtype)
         i = nb = 0
         flops = 0.0
         while i < len(ops):
@@ -651,7 +631,7 @@ class Plan:
             oc = self.shapes[ops[i + (1 if fuse_act else 0)].id].c
             dst = "OUT" if last else f"t{nb}"
             if not last:
-                specs[dst] = (B * T * pmax, oc, torch.bfloat16)
+                pp_specs[dst] = (B * T, oc, torch.bfloat16)
                 nb += 1
             steps.append((o, None, dst, N.ACT_SILU if fuse_act else N.ACT_NONE, last, oc))
             if o.kind is OpKind.TEMPORAL_CONV:
@@ -660,9 +640,21 @@ class Plan:
                 flops += 2.0 * B * T * HW * C * oc
             elif o.kind is OpKind.TEMPORAL_ATTENTION:
                 flops += B * HW * (8.0 * T * C * C + 4.0 * T * T * C)
-                specs["qkv"] = (B * T * pmax, 3 * C, torch.bfloat16)
-                specs["o"] = (B * T * pmax, C, torch.bfloat16)
+                pp_specs["qkv"] = (B * T, 3 * C, torch.bfloat16)
+                pp_specs["o"] = (B * T, C, torch.bfloat16)
             i += 2 if fuse_act else 1
+        # exact per-pixel slice scratch -> band count under the budget
+        per_pix = sum(r * c * torch.empty((), dtype=dt).element_size() for r, c, dt in pp_specs.values())
+        from .parallel import shard_range
+        p0, p1 = shard_range(HW, self.cfg.world, self.cfg.rank)
+        if self.cfg.slicing == "plan" and grp.plan.row_extents:
+            k = max(1, min(grp.plan.n_slices, p1 - p0))
+        else:
+            k = self._k_for(per_pix, p1 - p0, self.cfg.temporal_k)
+        bands = [(a + p0, b + p0) for a, b in balanced(p1 - p0, k)]
+        self.slice_counts[grp.label] = len(bands)
+        pmax = max([b - a for a, b in bands] + [1])
+        specs = {k: (pmax * r, c, dt) for k, (r, c, dt) in pp_specs.items()}
         # fix up sources: each step reads the previous step's destination
         fixed, prev = [], "IN"
         for (o, _src, dst, act, last, oc) in steps:
