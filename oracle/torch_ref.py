@@ -272,3 +272,25 @@ def run_rehash(ref: TorchRef, G, K=None):
 
 def to_bcthw_numpy(x):
     return x.detach().cpu().numpy()
+
+
+@torch.no_grad()
+def run_naive_clip(cfg, chunk, device="cpu", K=None):
+    """NaiveClip(chunk): every clip of ``chunk``
+    frames is denoised as an independent video (the same weights -- they do not depend on T --
+    and its frames of the seeded latent), the clips stitched along t.  All-key loop."""
+    import dataclasses
+    K = K or cfg.steps
+    graph, w = build_toy_unet(cfg)
+    x_full = np.random.default_rng(cfg.seed + 1).standard_normal(tuple(cfg.input_shape()))
+    outs = []
+    for f0 in range(0, cfg.frames, chunk):
+        n = min(chunk, cfg.frames - f0)
+        sub = dataclasses.replace(cfg, frames=n)
+        ref = TorchRef(sub, device, *build_toy_unet(sub))
+        x = _t(x_full[:, f0:f0 + n], ref.dev)
+        for s in range(K):
+            e, _ = ref.eps(x, s)
+            x = x - ref.alpha(s, K) * e
+        outs.append(x)
+    return torch.cat(outs, dim=1)

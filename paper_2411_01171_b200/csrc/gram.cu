@@ -3,14 +3,16 @@
 //
 // G = P P^T with P the K x n matrix of probes (n = 73.7M elements at SVD-XT shape).  The
 // contraction is HBM-bound (K = 25: 3.7 GB of bf16 probes per map), so the kernel is built to
-// read every probe element exactly once: each warp walks a contiguous element range 16 at a
-// time and feeds the same registers to both operands of bf16 mma.sync m16n8k16 (A = rows of
-// P, B = the same rows as P^T columns).  Products of bf16 values are exact in fp32; the fp32
-// MMA accumulators are flushed into fp64 every 16 k-steps (256 elements), warps are combined
-// in fixed order through shared memory and blocks in fixed order by the finalize kernel --
+// read every probe element exactly once: each warp walks a contiguous element range 32 at a
+// time (16-byte loads, 4 lanes x 16 B per row) and feeds the same registers to both operands of
+// bf16 mma.sync m16n8k16 (A = rows of P, B = the same rows as P^T columns).  Products of bf16
+// values are exact; the MMA's fp32 accumulators are flushed into thread-private fp64 shared-
+// memory accumulators every 16 k-steps (256 elements), warps are combined
+// in fixed order through shared memory and blocks in fixed order by the combine kernel --
 // bit-reproducible, no atomics.
 //
-// K <= 32 runs as one 32 x 32 job; larger K as jobs over pairs of 32-probe blocks (gridDim.y).
+// K <= 32 runs as one 32 x 32 job; larger K as one launch per pair of 32-probe blocks.
+// Every probe must be 16-byte aligned (n % 8 == 0 for probes packed back to back).
 // A row >= K reads as zero.  The n % 16 tail is added in fp64 by block 0.
 #include "common.cuh"
 
@@ -18,19 +20,24 @@ namespace sf {
 namespace gram {
 
 constexpr int WARPS = 8, THREADS = WARPS * 32;
-constexpr int KSTEP = 16, UNROLL = 4, FLUSH = 16;   // flush every FLUSH k-steps
+constexpr int CHUNK = 32;        // elements per row per warp load (4 lanes x 16 B) = 2 mma k-steps
+constexpr int UNROLL = 4;        // 16-byte loads per probe row in flight per thread
+constexpr int FLUSH = 2;         // loop iterations (2*UNROLL k-steps each) between fp64 flushes
 
-__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, const uint32_t* b) {
+__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint32_t ld_u32(const bf16* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+__device__ __forceinline__ uint4 ld16(const bf16* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
   return v;
 }
 
@@ -44,18 +51,41 @@ __device__ __forceinline__ void job_of(int y, int nb, int& bi, int& bj) {
   bj = bi + y;
 }
 
-// part[(blockIdx.y * gridDim.x + blockIdx.x) * 1024 + i * 32 + j]: this block's 32x32 partial
-__global__ void __launch_bounds__(THREADS) gram_mma_kernel(const bf16* const* __restrict__ probes, int K, int64_t n,
-                                                            double* __restrict__ part) {
+// One k-step (half h of a 16-byte load): the Gram is invariant under any permutation of the
+// element index applied to every row alike, so lane (g, q) feeds its 8 loaded elements
+// e0..e7 (offset 8q of a 32-element chunk) as k-slots {2q, 2q+1} <- e[4h], e[4h+1] and
+// {2q+8, 2q+9} <- e[4h+2], e[4h+3]: each chunk is two complete m16n8k16 k-steps.
+template <bool DIAG>
+__device__ __forceinline__ void kstep(float (&c)[2][4][4], const uint4* LA, const uint4* LB, int h) {
+  uint32_t a0[4], a1[4], b0[4], b1[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    a0[r] = h ? LA[r].z : LA[r].x;
+    a1[r] = h ? LA[r].w : LA[r].y;
+    b0[r] = DIAG ? a0[r] : (h ? LB[r].z : LB[r].x);
+    b1[r] = DIAG ? a1[r] : (h ? LB[r].w : LB[r].y);
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) mma16816(c[m][t], a0[2 * m], a0[2 * m + 1], a1[2 * m], a1[2 * m + 1], b0[t], b1[t]);
+}
+
+// part[(job * gridDim.x + blockIdx.x) * 1024 + i * 32 + j]: this block's 32x32 partial of job (bi, bj)
+template <bool DIAG>
+__global__ void __launch_bounds__(THREADS, 2) gram_mma_kernel(const bf16* const* __restrict__ probes, int K, int64_t n,
+                                                               int job, double* __restrict__ part) {
   griddep_wait();
   griddep_trigger();
+  extern __shared__ double sacc[];   // [WARPS][32 entries][32 lanes]: thread-private fp64 accumulators
   const int nb = (K + 31) / 32;
   int bi, bj;
-  job_of(blockIdx.y, nb, bi, bj);
-  const bool diag = bi == bj;
+  job_of(job, nb, bi, bj);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, c0 = (lane & 3) * 2;
-  // the 4 probe rows this thread loads for the A side (block bi) and the B side (block bj)
+  const int g = lane >> 2, q = lane & 3;
+  double* my = sacc + warp * 1024 + lane;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) my[i * 32] = 0.0;
   const bf16* pa[4];
   const bf16* pb[4];
   bool va[4], vb[4];
@@ -64,105 +94,71 @@ __global__ void __launch_bounds__(THREADS) gram_mma_kernel(const bf16* const* __
     const int ia = bi * 32 + g + 8 * r, ib = bj * 32 + g + 8 * r;
     va[r] = ia < K;
     vb[r] = ib < K;
-    pa[r] = probes[va[r] ? ia : 0] + c0;
-    pb[r] = probes[vb[r] ? ib : 0] + c0;
+    pa[r] = probes[va[r] ? ia : 0] + 8 * q;
+    pb[r] = probes[vb[r] ? ib : 0] + 8 * q;
   }
-  const int64_t nsteps = n / KSTEP;
+  const int64_t nchunks = n / CHUNK;
   const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
-  const int64_t per = (nsteps + nw - 1) / nw;
-  const int64_t s0 = gw * per, s1 = s0 + per < nsteps ? s0 + per : nsteps;
-
-  double acc[2][4][4];
+  const int64_t per = (nchunks + nw - 1) / nw;
+  const int64_t s0 = gw * per, s1 = s0 + per < nchunks ? s0 + per : nchunks;
   float c[2][4][4];
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int t = 0; t < 4; ++t)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        acc[m][t][e] = 0.0;
-        c[m][t][e] = 0.f;
-      }
-  int since = 0;
+      for (int e = 0; e < 4; ++e) c[m][t][e] = 0.f;
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  int it = 0;
   for (int64_t s = s0; s < s1; s += UNROLL) {
-    const int nk = (int)(s1 - s < UNROLL ? s1 - s : UNROLL);
-    uint32_t LA[UNROLL][4][2], LB[UNROLL][4][2];
+    uint4 LA[UNROLL][4], LB[UNROLL][4];
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      if (u < nk) {
-        const int64_t e0 = (s + u) * KSTEP;
+      const bool in = s + u < s1;
+      const int64_t e0 = (s + u) * CHUNK;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          LA[u][r][0] = va[r] ? ld_u32(pa[r] + e0) : 0u;
-          LA[u][r][1] = va[r] ? ld_u32(pa[r] + e0 + 8) : 0u;
-          if (!diag) {
-            LB[u][r][0] = vb[r] ? ld_u32(pb[r] + e0) : 0u;
-            LB[u][r][1] = vb[r] ? ld_u32(pb[r] + e0 + 8) : 0u;
-          }
-        }
+      for (int r = 0; r < 4; ++r) {
+        LA[u][r] = in && va[r] ? ld16(pa[r] + e0) : zero;
+        if (!DIAG) LB[u][r] = in && vb[r] ? ld16(pb[r] + e0) : zero;
       }
     }
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      if (u < nk) {
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-          const uint32_t a[4] = {LA[u][2 * m][0], LA[u][2 * m + 1][0], LA[u][2 * m][1], LA[u][2 * m + 1][1]};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const uint32_t b[2] = {diag ? LA[u][t][0] : LB[u][t][0], diag ? LA[u][t][1] : LB[u][t][1]};
-            mma16816(c[m][t], a, b);
-          }
-        }
-      }
+      kstep<DIAG>(c, LA[u], DIAG ? LA[u] : LB[u], 0);
+      kstep<DIAG>(c, LA[u], DIAG ? LA[u] : LB[u], 1);
     }
-    since += nk;
-    if (since >= FLUSH) {
-      since = 0;
+    if (++it == FLUSH || s + UNROLL >= s1) {
+      it = 0;
 #pragma unroll
       for (int m = 0; m < 2; ++m)
 #pragma unroll
         for (int t = 0; t < 4; ++t)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            acc[m][t][e] += (double)c[m][t][e];
+            my[((m * 4 + t) * 4 + e) * 32] += (double)c[m][t][e];
             c[m][t][e] = 0.f;
           }
     }
   }
-#pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[m][t][e] += (double)c[m][t][e];
-
-  // fixed-order combine of the 8 warps into one 32x32 tile (warp 0 first, then 1, ...)
-  __shared__ double tile[32 * 32];
-  for (int w = 0; w < WARPS; ++w) {
-    if (warp == w) {
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int idx = (m * 16 + g + (e >= 2 ? 8 : 0)) * 32 + t * 8 + c0 + (e & 1);
-            tile[idx] = (w == 0 ? 0.0 : tile[idx]) + acc[m][t][e];
-          }
-    }
-    __syncthreads();
+  __syncthreads();
+  // fixed-order combine: entry (m,t,e) of lane L of warp w is Gram element (row, col) below
+  double* out = part + ((int64_t)job * gridDim.x + blockIdx.x) * 1024;
+  for (int idx = threadIdx.x; idx < 1024; idx += THREADS) {
+    const int L = idx & 31, slot = idx >> 5;          // slot = (m*4 + t)*4 + e
+    const int m = slot >> 4, t = (slot >> 2) & 3, e = slot & 3;
+    const int row = m * 16 + (L >> 2) + (e >= 2 ? 8 : 0), col = t * 8 + (L & 3) * 2 + (e & 1);
+    double v = 0.0;
+    for (int w = 0; w < WARPS; ++w) v += sacc[w * 1024 + slot * 32 + L];
+    out[row * 32 + col] = v;
   }
-  double* out = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 1024;
-  for (int i = threadIdx.x; i < 1024; i += THREADS) out[i] = tile[i];
-  // the n % 16 tail elements, block 0 of every job
-  if (blockIdx.x == 0 && nsteps * KSTEP < n) {
+  // the n % 32 tail elements, block 0 of every job
+  if (blockIdx.x == 0 && nchunks * CHUNK < n) {
     __syncthreads();
     for (int i = threadIdx.x; i < 1024; i += THREADS) {
       const int ri = bi * 32 + i / 32, rj = bj * 32 + i % 32;
       if (ri < K && rj < K) {
         double v = 0.0;
-        for (int64_t e = nsteps * KSTEP; e < n; ++e)
+        for (int64_t e = nchunks * CHUNK; e < n; ++e)
           v += (double)__bfloat162float(probes[ri][e]) * (double)__bfloat162float(probes[rj][e]);
         out[i] += v;
       }
@@ -190,7 +186,8 @@ __global__ void gram_combine_kernel(const double* __restrict__ part, int K, int 
   }
 }
 
-inline int blocks_per_job() { return num_sms(); }   // one 8-warp block per SM (232 registers)
+inline int blocks_per_job() { return num_sms() * 2; }   // two 8-warp blocks per SM
+constexpr int SMEM = WARPS * 1024 * (int)sizeof(double);
 
 }  // namespace gram
 }  // namespace sf
@@ -209,8 +206,23 @@ sf_status sf_gram_bf16(const void* const* probes, int32_t K, int64_t n, void* wo
   SF_CHECK_ARG(K >= 1 && n >= 1 && probes && work && out, SF_ERR_SHAPE, "bad extents");
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = (K + 31) / 32, jobs = nb * (nb + 1) / 2, nblk = gram::blocks_per_job();
-  launch_k(gram::gram_mma_kernel, dim3(nblk, jobs), dim3(gram::THREADS), 0, st, (const bf16* const*)probes, (int)K, n,
-           (double*)work);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(gram::gram_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gram::SMEM);
+    cudaFuncSetAttribute(gram::gram_mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gram::SMEM);
+    init = true;
+  }
+  SF_CHECK_ARG(((uintptr_t)probes & 7) == 0, SF_ERR_PARAM, "probe pointer array misaligned");
+  // one launch per job (bi, bj); diagonal jobs feed one register set to both operands
+  for (int y = 0, bi = 0; bi < nb; ++bi)
+    for (int bj = bi; bj < nb; ++bj, ++y) {
+      if (bi == bj)
+        launch_k(gram::gram_mma_kernel<true>, dim3(nblk), dim3(gram::THREADS), gram::SMEM, st,
+                 (const bf16* const*)probes, (int)K, n, y, (double*)work);
+      else
+        launch_k(gram::gram_mma_kernel<false>, dim3(nblk), dim3(gram::THREADS), gram::SMEM, st,
+                 (const bf16* const*)probes, (int)K, n, y, (double*)work);
+    }
   launch_k(gram::gram_combine_kernel, dim3(jobs), dim3(256), 0, st, (const double*)work, (int)K, nblk, out);
   return launch_status("sf_gram_bf16");
 }

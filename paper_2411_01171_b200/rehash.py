@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import BadThreshold, ScheduleMismatch, TargetUnreachable, ZeroNorm
+from .errors import BadThreshold, InvalidParam, ScheduleMismatch, TargetUnreachable, ZeroNorm
 
 
 @dataclass
@@ -78,6 +78,8 @@ def gram_partial(probes: list[torch.Tensor]) -> np.ndarray:
     K = len(probes)
     n = probes[0].numel()
     dev = probes[0].device
+    if any(p.data_ptr() % 16 for p in probes):
+        raise InvalidParam("sf_gram_bf16 needs 16-byte aligned probes")
     ptrs = torch.tensor([p.data_ptr() for p in probes], dtype=torch.int64, device=dev)
     work = torch.empty(N.query("sf_gram_workspace", K, n), dtype=torch.uint8, device=dev)
     out = torch.empty(K * K, dtype=torch.float64, device=dev)

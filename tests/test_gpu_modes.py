@@ -129,3 +129,19 @@ def test_c3_full_size_slicing_properties():
     r = float(np.abs(b.data - a.data).max() / np.abs(a.data).max())
     print("c3 ragged vs default rel", r)
     assert r <= 2e-2
+
+
+def test_naive_clip_run_matches_oracle_naive_clip():
+    """run_denoise(NAIVE_CLIP) against the fp64 oracle's own NaiveClip (oracle/torch_ref.py:
+    independent clips, stitched): <= 5e-3 max_rel; and NaiveClip differs from the full-video
+    run by far more than that (the divergence the Feature Slicer avoids)."""
+    from oracle import torch_ref as TR
+    from paper_2411_01171_b200.harness import DenoiseRunConfig, run_denoise
+    x_nc, _ = run_denoise(DenoiseRunConfig(C1, mode=ExecMode.NAIVE_CLIP, naive_chunk=3))
+    ref_nc = TR.run_naive_clip(C1, 3, "cuda").cpu().numpy()
+    r = float(np.abs(x_nc.data - ref_nc).max() / np.abs(ref_nc).max())
+    ref_full, _, _ = TR.run_full(TR.TorchRef(C1, "cuda"), keep_probes=False)
+    div = float(np.abs(ref_nc - ref_full.cpu().numpy()).max() / np.abs(ref_full.cpu().numpy()).max())
+    print("naiveclip vs oracle naiveclip", r, "oracle naiveclip vs full", div)
+    assert r <= 5e-3
+    assert div > 4 * r
