@@ -274,7 +274,7 @@ def run_ours(args, world, rank, local):
     exchanger = None
     if world > 1:
         from paper_2411_01171_b200.parallel import NcclExchanger
-        exchanger = NcclExchanger(rank, world)
+        exchanger = NcclExchanger(rank, world, comm_stream=True)
     ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=args.spatial_k, temporal_k=args.temporal_k,
                       rank=rank, world=world)
     if args.scratch_budget_mb:

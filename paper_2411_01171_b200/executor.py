@@ -106,6 +106,7 @@ class Value:
     col0: int = 0
     width: int = 0              # storage row width (>= C when aliased into a concat)
     tensor: torch.Tensor | None = None
+    store: dict = field(default_factory=dict)   # layout "F" | "S" | "T" -> (rows tensor, col0)
 
 
 @dataclass
@@ -216,14 +217,15 @@ class Plan:
                         alias[self._storage_id(v)] = (nid, off)
                         off += self.shapes[v].c
         self.alias = alias
-        # buffers: one per storage root
+        # buffers: one per (storage root, layout)
         intervals: dict[str, list[int]] = {}
-        sizes: dict[str, int] = {}
 
         def root(sid):
             while sid in alias:
                 sid = alias[sid][0]
             return sid
+        self._root_fn = root
+        self.root = lambda vid: root(self._storage_id(vid))
 
         special = {"x", "step_emb", *self.emb_nodes}
         # only values that cross a schedule unit live in the arena: group tails and
@@ -240,10 +242,6 @@ class Plan:
             lo, hi = intervals.get(sid, [d, last])
             intervals[sid] = [min(lo, d), max(hi, last)]
         out_id = g.outputs[0]
-        for sid in intervals:
-            s = self.shapes[sid]
-            sizes[sid] = s.b * s.t * s.h * s.w * s.c * 2
-        sizes[out_id] = self.shapes[out_id].count() * 4   # eps is fp32
         # persistent: the rehash probe (its storage doubles as the feature cache)
         probe = None
         for n in g.nodes.values():
@@ -252,35 +250,54 @@ class Plan:
         if probe is not None:
             intervals[probe] = [0, len(sched)]
         self.probe_root = probe
+        # layouts: unsharded, one full buffer ("F") per root; sharded (parallel.py), a frame-
+        # sharded copy "S" (this rank's frames x all pixels) and/or a pixel-sharded copy "T"
+        # (all frames x this rank's pixel band) -- only the layouts the root is read or
+        # written in, each 1/world of the full size
+        self.sharded = self.cfg.world > 1
+        if self.sharded:
+            # each layout copy lives only while that layout is read or written
+            key_iv = self._layout_intervals(root, out_id, len(sched))
+            if probe is not None:
+                for key in key_iv:
+                    if key[0] == probe:
+                        key_iv[key] = [0, len(sched)]
+        else:
+            key_iv = {(sid, "F"): iv for sid, iv in intervals.items()}
+        sizes: dict[tuple, int] = {}
+        for (sid, L) in key_iv:
+            sizes[(sid, L)] = self._layout_rows(self.shapes[sid], L) * self.shapes[sid].c * \
+                (4 if sid == out_id else 2)
         # interval packing: largest first, lowest non-conflicting offset
         placed: list[tuple[int, int, int, int]] = []  # (off, size, lo, hi)
         offsets = {}
         align = 256
-        for sid in sorted(sizes, key=lambda s: (-sizes[s], s)):
-            lo, hi = intervals[sid]
-            size = (sizes[sid] + align - 1) // align * align
+        for key in sorted(sizes, key=lambda k: (-sizes[k], k)):
+            lo, hi = key_iv[key]
+            size = (sizes[key] + align - 1) // align * align
             cands = sorted({0} | {o + sz for o, sz, l2, h2 in placed})
             for off in cands:
                 if all(not (l2 <= hi and lo <= h2 and off < o + sz and o < off + size) for o, sz, l2, h2 in placed):
                     break
             placed.append((off, size, lo, hi))
-            offsets[sid] = off
+            offsets[key] = off
         self.arena_bytes = max([o + s for o, s, _, _ in placed] + [align])
         # kept for the derived memory ledger (ledger.py): live units and payload bytes per buffer
-        self.arena_intervals = {sid: tuple(intervals[sid]) for sid in sizes}
+        self.arena_intervals = {key: tuple(key_iv[key]) for key in sizes}
         self.arena_sizes = dict(sizes)
         self.n_units = len(sched)
         self.arena = torch.empty(self.arena_bytes, dtype=torch.uint8, device=self.dev)
         self.buffers = {}
-        for sid, off in offsets.items():
+        for key, off in offsets.items():
+            sid, L = key
             s = self.shapes[sid]
-            rows = s.b * s.t * s.h * s.w
+            rows = self._layout_rows(s, L)
             if sid == out_id:
                 t = self.arena[off:off + rows * s.c * 4].view(torch.float32).view(rows, s.c)
             else:
                 t = self.arena[off:off + rows * s.c * 2].view(torch.bfloat16).view(rows, s.c)
-            self.buffers[sid] = t
-        # values
+            self.buffers[key] = t
+        # values: each points at its root's buffers (a concat operand at its channel offset)
         for vid, shape in self.shapes.items():
             if vid not in self.materialized:
                 continue
@@ -289,11 +306,20 @@ class Plan:
             while sid in alias:
                 sid, c0 = alias[sid][0], alias[sid][1] + col
                 col = c0
-            self.values[vid] = Value(vid, shape, buf=sid, col0=col, tensor=self.buffers[sid])
+            store = {}
+            for L in ("F", "S", "T"):
+                if (sid, L) in self.buffers:
+                    store[L] = (self.buffers[(sid, L)], col)
+            if "F" in store:
+                store["S"] = store["T"] = store["F"]
+            self.values[vid] = Value(vid, shape, buf=sid, col0=col, tensor=store.get("F", (None,))[0], store=store)
         # inputs: latent rows (fp32) and the emb table
         xs = self.shapes["x"]
         self.latent = torch.zeros(xs.b * xs.t * xs.h * xs.w, xs.c, dtype=torch.float32, device=self.dev)
-        self.eps = self.buffers[out_id]
+        # the network output (eps) is produced frame-sharded: this rank's frames only
+        self.eps = self.values[out_id].store["S"][0]
+        F0, F1 = self._frames()
+        self.latent_local = self.latent[F0 * xs.h * xs.w:F1 * xs.h * xs.w]
         # step-embedding projections of every res block: one gemv per step
         ws = [self.dw.p[n]["w32"] for n in self.emb_nodes]
         bs = [self.dw.p[n]["bias"] for n in self.emb_nodes]
@@ -319,9 +345,11 @@ class Plan:
         led = MemoryLedger(summary)
         g = self.graph
 
-        def tag(sid):
+        def tag(key):
+            sid, L = key
             n = g.nodes.get(sid)
-            return n.label or sid if n is not None else sid
+            base = n.label or sid if n is not None else sid
+            return base if L == "F" else f"{base}:{L}"
         if scratch_bytes:
             led.alloc(scratch_bytes, "slice_scratch")
         by_lo: dict[int, list[str]] = {}
@@ -339,8 +367,101 @@ class Plan:
         return led
 
     def rows(self, vid, row0=0, ostride=0) -> Rows:
+        """Global row view of an unsharded value (row = frame * h*w + pixel)."""
         v = self.values[vid]
         return Rows(v.tensor, row0, ostride, v.col0)
+
+    # -- sharded layouts (parallel.py): S = my frames x all pixels, T = all frames x my pixels
+    def _frames(self):
+        from .parallel import shard_range
+        xs = self.shapes["x"]
+        return shard_range(xs.b * xs.t, self.cfg.world, self.cfg.rank)
+
+    def _pixels(self, shape: Shape5):
+        from .parallel import shard_range
+        return shard_range(shape.h * shape.w, self.cfg.world, self.cfg.rank)
+
+    def _layout_rows(self, shape: Shape5, L: str) -> int:
+        if L == "S":
+            f0, f1 = self._frames()
+            return (f1 - f0) * shape.h * shape.w
+        if L == "T":
+            p0, p1 = self._pixels(shape)
+            return shape.b * shape.t * (p1 - p0)
+        return shape.b * shape.t * shape.h * shape.w
+
+    def srows(self, vid, f0: int) -> Rows:
+        """Rows (frame f0 + o, pixel i) of a value in its frame-sharded layout (ostride h*w)."""
+        v = self.values[vid]
+        t, col = v.store["S"]
+        hw = v.shape.h * v.shape.w
+        base = self._frames()[0] if "F" not in v.store else 0
+        return Rows(t, (f0 - base) * hw, hw, col)
+
+    def trows(self, vid, p0: int) -> Rows:
+        """Rows (frame o, pixel p0 + i) of a value in its pixel-sharded layout."""
+        v = self.values[vid]
+        t, col = v.store["T"]
+        if "F" in v.store:
+            return Rows(t, p0, v.shape.h * v.shape.w, col)
+        q0, q1 = self._pixels(v.shape)
+        return Rows(t, p0 - q0, q1 - q0, col)
+
+    def block_rows(self, vid, L: str, f0: int, p0: int) -> Rows:
+        """Row view starting at (frame f0, pixel p0) in layout L; row (o, i) = (f0 + o, p0 + i)."""
+        if L == "S":
+            return self.srows(vid, f0).shifted(rows=p0)
+        r = self.trows(vid, p0)
+        return r.shifted(rows=f0 * r.ostride)
+
+    def _parts(self, root, vid) -> list[str]:
+        """Values whose storage makes up ``vid`` (a zero-copy concat is its operands)."""
+        n = self.graph.nodes.get(vid)
+        if n is not None and n.kind is OpKind.CONCAT and all(
+                root(self._storage_id(v)) == root(self._storage_id(vid)) for v in n.inputs):
+            return [p for v in n.inputs for p in self._parts(root, v)]
+        return [vid]
+
+    def _layout_intervals(self, root, out_id, n_units) -> dict:
+        """(storage root, layout) -> [first, last] schedule unit touching that layout copy.
+
+        A group of domain d reads its input (and fused residual) and writes its output in
+        layout d; the exchanges of ``parallel.exchange_schedule`` move values between layouts.
+        """
+        iv: dict[tuple, list[int]] = {}
+
+        def touch(v, L, ui):
+            key = (root(self._storage_id(v)), L)
+            lo, hi = iv.get(key, [ui, ui])
+            iv[key] = [min(lo, ui), max(hi, ui)]
+        for ui, (kind, ref) in enumerate(self.grouped.schedule):
+            if kind != "group":
+                continue
+            grp = self.grouped.groups[ref]
+            if grp.ops[0].id in self.emb_nodes:
+                continue
+            d = "S" if grp.domain is Domain.SPATIAL else "T"
+            touched = [grp.head_input, grp.tail]
+            if grp.tail in self.epilogue_of:
+                add_id, other, is_emb = self.epilogue_of[grp.tail]
+                touched.append(add_id)
+                if not is_emb:
+                    touched.append(other)
+            for v in touched:
+                if v in ("x", "step_emb"):
+                    continue
+                for part in self._parts(root, v):
+                    touch(part, d, ui)
+        # an exchange reads its source copy and writes its destination copy anywhere from
+        # right after the producer (``at``) until its first reader (``need``): both stay live
+        from .parallel import exchange_schedule
+        for op in exchange_schedule(self, root):
+            for L in (op.src, op.dst):
+                touch(op.value, L, op.at)
+                touch(op.value, L, op.need)
+        key = (root(self._storage_id(out_id)), "S")
+        iv[key] = [iv.get(key, [0, 0])[0], n_units]
+        return iv
 
     # ------------------------------------------------------------------ compile
     def _k_for(self, per_unit_bytes: int, extent: int, override: int | None) -> int:
@@ -350,18 +471,39 @@ class Plan:
         return max(1, math.ceil(extent / units))
 
     def _insert_exchanges(self):
-        from .parallel import plan_exchanges
-        ins = plan_exchanges(self)
-        out, j = [], 0
-        for ui, u in enumerate(self.units):
-            while j < len(ins) and ins[j][0] == ui:
-                op = ins[j][1]
+        """Place every frame<->pixel exchange right after its value's producer; its first reader
+        waits on the exchange's completion event (used when the exchanger runs on a comm stream)."""
+        from .parallel import exchange_schedule
+        ops = exchange_schedule(self)
+        sched_idx = {ref: i for i, ref in enumerate(self.grouped.schedule)}
+        pos = [sched_idx[u.ref] for u in self.units]
+        out = []
+        j = 0
+        ops = sorted(ops, key=lambda o: (o.at, o.need))
+        waits: dict[int, list] = {}
+        for op in ops:
+            op.done = torch.cuda.Event() if torch.cuda.is_available() and self.dev.type == "cuda" else None
+            waits.setdefault(op.need, []).append(op)
+        for u, si in zip(self.units, pos):
+            while j < len(ops) and ops[j].at <= si:
+                op = ops[j]
                 out.append(Unit(f"exchange[{op.value} {op.src}->{op.dst}]", self._exchange_runner(op), ref=u.ref,
                                 exchange=op))
                 j += 1
+            if si in waits:
+                u.run = self._waiting(u.run, waits[si])
             out.append(u)
         self.units = out
-        self.n_exchanges = len(ins)
+        self.n_exchanges = len(ops)
+
+    def _waiting(self, run, ops):
+        def wrapped(st):
+            if getattr(self.exchanger, "comm", None) is not None:
+                cur = torch.cuda.ExternalStream(st)
+                for op in ops:
+                    cur.wait_event(op.done)
+            run(st)
+        return wrapped
 
     def _exchange_runner(self, op):
         def run(st):
@@ -483,8 +625,7 @@ class Plan:
         latent_in = x_id == "x"
 
         def vrows(vid, sl):
-            sh = self.shapes[vid]
-            return self.rows(vid, sl[0] * sh.h * sh.w, sh.h * sh.w)
+            return self.srows(vid, sl[0])
 
         epi_fn = self._epilogue(tail, vrows)
         # lower the chain into steps over slice-local buffers; scratch specs per frame first
@@ -588,7 +729,7 @@ class Plan:
                                    prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), st)
                         elif last and eps_out:
                             # out_conv: fp32 network output (per-tap projection + shifted sum for tiny cout)
-                            out = Rows(self.eps, sl[0] * ohw, ohw)
+                            out = self.srows(tail, sl[0])
                             if "w_taps" in prm and epi.res is None and epi.rowbias is None and not act:
                                 D.conv2d_tapwise(st, X, out, nf, ish.h, ish.w, ish.c, osh.c, prm, scratch["taps_y"],
                                                  backend)
@@ -617,7 +758,7 @@ class Plan:
         x_id = grp.head_input
 
         def vrows(vid, band):
-            return self.rows(vid, band[0], HW)
+            return self.trows(vid, band[0])
 
         epi_fn = self._epilogue(tail, vrows)
         steps, pp_specs = [], {}        # name -> (rows per pixel, cols, dtype)
@@ -732,8 +873,13 @@ class Plan:
     def probe(self) -> torch.Tensor:
         return self.values[self.graph.node_by_label(PROBE_LABEL).id].tensor
 
-    def probe_rows(self) -> Rows:
-        return self.rows(self.graph.node_by_label(PROBE_LABEL).id)
+    def probe_band_rows(self) -> tuple[Rows, int, int]:
+        """(rows, n_outer, n_inner) of this rank's part of the probe: all frames x its pixel band
+        (the probe is a temporal-group output; unsharded: every pixel)."""
+        pid = self.graph.node_by_label(PROBE_LABEL).id
+        sh = self.shapes[pid]
+        p0, p1 = self._pixels(sh) if self.sharded else (0, sh.h * sh.w)
+        return self.trows(pid, p0), sh.b * sh.t, p1 - p0
 
     def flops_full(self) -> float:
         return sum(u.gemm_flops for u in self.units)
@@ -762,8 +908,9 @@ class _GroupPlan(Plan):
         so = self.shapes[group.tail]
         self.inp = torch.empty(in_shape.rows, in_shape.c, dtype=torch.bfloat16, device=self.dev)
         self.out = torch.empty(so.rows, so.c, dtype=torch.bfloat16, device=self.dev)
-        self.values[group.head_input] = Value(group.head_input, in_shape, tensor=self.inp)
-        self.values[group.tail] = Value(group.tail, so, tensor=self.out)
+        self.sharded = False
+        for vid, t in ((group.head_input, self.inp), (group.tail, self.out)):
+            self.values[vid] = Value(vid, self.shapes[vid], tensor=t, store={L: (t, 0) for L in ("F", "S", "T")})
         self.latent = torch.empty(in_shape.rows, in_shape.c, dtype=torch.float32, device=self.dev) \
             if group.head_input == "x" else None
         self.eps = None
@@ -848,7 +995,7 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     plan = Plan.__new__(Plan)
     plan.graph, plan.grouped, plan.dw = graph, grouped, dw
     plan.cfg = ExecConfig(spatial_k=cfg.spatial_k, temporal_k=cfg.temporal_k, scratch_budget=cfg.scratch_budget,
-                          device="meta")
+                          device="meta", rank=cfg.rank, world=cfg.world)
     plan.dev = dw.dev
     plan.shapes = infer_shapes(graph)
     plan.topo = graph.topo_order()

@@ -101,21 +101,19 @@ class Denoiser:
         st = torch.cuda.current_stream().cuda_stream
         p = self.plan
         keys = set(range(self.K)) if schedule is None else set(schedule.key_steps)
-        n_lat = p.latent.numel()
+        n_lat = p.latent_local.numel()
         for s in range(self.K):
             if s in keys:
                 p.run_full(st, self.emb_table[s].data_ptr())
                 if record_trace:
                     # this rank's rows of the probe (all of them unsharded; the pixel band
                     # across all frames when sharded -- the probe is a temporal-group output)
-                    pr = p.probe_rows()
-                    sh = p.shapes[self.graph.node_by_label(PROBE_LABEL).id]
-                    b0, b1 = self._probe_band()
-                    N.call("sf_copy_rows", pr.shifted(rows=b0, ostride=sh.h * sh.w).view(),
-                           N.View(self.trace[s].data_ptr(), sh.c, b1 - b0), sh.b * sh.t, b1 - b0, sh.c, st)
+                    pr, n_out, n_in = p.probe_band_rows()
+                    c = self.trace.shape[1] // (n_out * n_in)
+                    N.call("sf_copy_rows", pr.view(), N.View(self.trace[s].data_ptr(), c, n_in), n_out, n_in, c, st)
             elif not self.reuse_donor_eps:
                 p.run_tail(st)
-            N.call("sf_axpy_f32", p.latent.data_ptr(), p.eps.data_ptr(), alpha(s, self.K), n_lat, st)
+            N.call("sf_axpy_f32", p.latent_local.data_ptr(), p.eps.data_ptr(), alpha(s, self.K), n_lat, st)
 
     def _probe_band(self):
         from .parallel import shard_range
