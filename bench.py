@@ -259,6 +259,33 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
             "slices": slice_summary(d2.plan), "gpu_launches_per_run": d2.launches[key]}
 
 
+def run_plan_only(args, world, rank):
+    """Per-rank arena of the sharded plan (shapes only, ``meta`` device): runs on CPU ranks (gloo)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2411_01171_b200.executor import ExecConfig, plan_memory
+    from paper_2411_01171_b200.grouping import group_operators
+    from paper_2411_01171_b200.slicer import default_temporal_config
+    from paper_2411_01171_b200.unet import UNetConfig, build_toy_unet
+    cfg = UNetConfig(**CONFIGS[args.config])
+    g, _ = build_toy_unet(cfg)
+    gg = group_operators(g, cfg.frames * cfg.effective_batch, default_temporal_config(cfg.height, cfg.width))
+    mine = plan_memory(g, gg, ExecConfig(rank=rank, world=world))
+    arenas = [mine["arena_bytes"]]
+    if world > 1:
+        t = torch.tensor([mine["arena_bytes"]], dtype=torch.int64)
+        out = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        arenas = [int(x.item()) for x in out]
+    if rank == 0:
+        one = plan_memory(g, gg)["arena_bytes"]
+        print(json.dumps({"plan_only": True, "config": {"workload": WORKLOAD[args.config]}, "n_gpus": world,
+                          "per_rank_arena_bytes": arenas, "world1_arena_bytes": one,
+                          "max_rank_fraction": max(arenas) / one,
+                          "exchanges_per_eval": mine.get("exchanges_per_eval", 0),
+                          "hoisted_exchanges": mine.get("hoisted_exchanges", 0)}), flush=True)
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_2411_01171_b200.executor import ExecConfig
@@ -449,11 +476,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--scratch-budget-mb", type=int, default=None)
     ap.add_argument("--no-north-star-plan", action="store_true")
+    ap.add_argument("--plan-only", action="store_true", help="per-rank device memory plan, no GPU needed")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args.gpus)
     world, rank, local = dist_setup(args.gpus)
-    if args.impl == "reference":
+    if args.plan_only:
+        run_plan_only(args, world, rank)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)

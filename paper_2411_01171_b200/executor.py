@@ -499,7 +499,8 @@ class Plan:
     def _waiting(self, run, ops):
         def wrapped(st):
             if getattr(self.exchanger, "comm", None) is not None:
-                cur = torch.cuda.ExternalStream(st)
+                from .parallel import stream_of
+                cur = stream_of(st)
                 for op in ops:
                     cur.wait_event(op.done)
             run(st)
@@ -1006,8 +1007,14 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     plan._analyse()
     plan._layout()
     led = plan.memory_ledger()
-    return {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers), "ledger": led,
-            "ledger_peak_bytes": led.peak_bytes}
+    out = {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers), "ledger": led,
+           "ledger_peak_bytes": led.peak_bytes}
+    if plan.cfg.world > 1:
+        from .parallel import exchange_schedule
+        ex = exchange_schedule(plan)
+        out["exchanges_per_eval"] = len(ex)
+        out["hoisted_exchanges"] = sum(1 for op in ex if op.at < op.need)
+    return out
 
 
 def stream_handle() -> int:

@@ -42,6 +42,13 @@ from .kinds import Domain, OpKind
 S, T = "S", "T"
 
 
+def stream_of(handle: int):
+    """torch stream object of a raw cudaStream_t handle (the current stream when it matches: a
+    handle of 0 is the default stream, which ExternalStream does not map back to)."""
+    cur = torch.cuda.current_stream()
+    return cur if cur.cuda_stream == handle else torch.cuda.ExternalStream(handle)
+
+
 def shard_range(extent: int, world: int, rank: int) -> tuple[int, int]:
     """Balanced contiguous chunk of ``extent`` owned by ``rank``."""
     base, rem = divmod(extent, world)
@@ -244,7 +251,7 @@ class NcclExchanger:
             go(stream)
             return
         start = torch.cuda.Event()
-        start.record(torch.cuda.ExternalStream(stream))
+        start.record(stream_of(stream))
         self.comm.wait_event(start)
         with torch.cuda.stream(self.comm):
             go(self.comm.cuda_stream)
@@ -265,7 +272,7 @@ class LocalExchanger:
     def exchange_all(self, op: ExchangeOp, stream, index: int | None = None):
         if self.comm is not None:
             start = torch.cuda.Event()
-            start.record(torch.cuda.ExternalStream(stream))
+            start.record(stream_of(stream))
             self.comm.wait_event(start)
             self._copies(op, self.comm.cuda_stream)
             for p in self.plans:          # every rank's copy of this exchange is now complete

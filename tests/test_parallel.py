@@ -144,3 +144,22 @@ def test_virtual_sharded_denoise_matches_unsharded(world):
             assert n_ex >= 34
             # per-rank shards run the same per-row arithmetic as the single-GPU plan: bit-identical
             assert np.array_equal(got, ref)
+
+
+def test_bench_gpus2_plan_only_spawns_two_ranks():
+    """``bench.py --gpus 2 --plan-only`` re-execs itself under torch.distributed.run (2 ranks, gloo
+    here) and reports each rank's arena of the sharded C3 plan: <= 0.7x the single-GPU arena."""
+    import json as _json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--plan-only"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    rec = _json.loads(line)
+    assert rec["n_gpus"] == 2 and len(rec["per_rank_arena_bytes"]) == 2
+    assert rec["max_rank_fraction"] <= 0.7
+    assert rec["exchanges_per_eval"] == 34
