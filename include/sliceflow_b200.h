@@ -116,14 +116,6 @@ sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int3
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C,
                               int32_t groups, const float* mean, const float* rstd, const float* gamma,
                               const float* beta, int32_t act, void* stream);
-/* GroupNorm + optional SiLU in one cooperative launch (statistics, finalize and apply
- * separated by grid barriers; replaces stats + apply above on the device path).
- * work: sf_group_norm_fused_workspace() bytes, 16-byte aligned; barrier: 8 bytes,
- * zero-initialised once, owned by one stream. */
-int64_t sf_group_norm_fused_workspace(int32_t frames, int32_t n_inner, int32_t C, int32_t groups);
-sf_status sf_group_norm(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
-                        float eps, const float* gamma, const float* beta, int32_t act, void* work, void* barrier,
-                        void* stream);
 /* LayerNorm over the C channels of every row (kernels.py:240-244), optional SiLU. */
 sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C,
                         const float* gamma, const float* beta, float eps, int32_t act, void* stream);

@@ -53,8 +53,6 @@ _PROTOS = {
     "sf_group_norm_workspace": [i32, i32, i32],
     "sf_group_norm_stats": [View, i32, i32, i32, i32, f32, vp, vp, vp, vp],
     "sf_group_norm_apply": [View, View, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp],
-    "sf_group_norm_fused_workspace": [i32, i32, i32, i32],
-    "sf_group_norm": [View, View, i32, i32, i32, i32, f32, vp, vp, i32, vp, vp, vp],
     "sf_layer_norm": [View, View, i32, i32, i32, vp, vp, f32, i32, vp],
     "sf_silu": [View, View, i32, i32, i32, vp],
     "sf_add": [View, View, View, i32, i32, i32, i32, vp],
@@ -80,7 +78,6 @@ _PROTOS = {
 }
 _RESTYPE = {
     "sf_group_norm_workspace": i64,
-    "sf_group_norm_fused_workspace": i64,
     "sf_dot3_workspace": i64,
     "sf_gram_workspace": i64,
     "sf_gemm_backend": i32,

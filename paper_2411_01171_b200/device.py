@@ -22,7 +22,6 @@ the C ABI.  Nothing here computes on the host.
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -202,16 +201,6 @@ def group_norm_stats(stream, x: Rows, frames, n_inner, C, groups, eps, work, mea
 def group_norm_apply(stream, x: Rows, y: Rows, frames, n_inner, C, groups, mean, rstd, prm, act):
     N.call("sf_group_norm_apply", x.view(), y.view(), frames, n_inner, C, groups, mean.data_ptr(), rstd.data_ptr(),
            prm["gamma"].data_ptr(), prm["beta"].data_ptr(), act, stream)
-
-
-# one-launch GroupNorm (csrc/gn_fused.cu); SF_GN_SPLIT=1 selects the stats + apply pair (A/B runs)
-GN_FUSED = os.environ.get("SF_GN_SPLIT", "0") != "1"
-
-
-def group_norm(stream, x: Rows, y: Rows, frames, n_inner, C, groups, eps, prm, act, work, barrier):
-    """GroupNorm (+ SiLU) in one cooperative launch (csrc/gn_fused.cu; kernels.py:228-253)."""
-    N.call("sf_group_norm", x.view(), y.view(), frames, n_inner, C, groups, eps, prm["gamma"].data_ptr(),
-           prm["beta"].data_ptr(), act, work.data_ptr(), barrier.data_ptr(), stream)
 
 
 def layer_norm(stream, x: Rows, y: Rows, n_outer, n_inner, C, prm, eps, act=N.ACT_NONE):

@@ -526,7 +526,6 @@ class Plan:
                 u.ref = (kind, ref)
                 self.units.append(u)
         self.scratch = torch.empty(max(self.scratch_need, 256), dtype=torch.uint8, device=self.dev)
-        self.gn_barrier = torch.zeros(4, dtype=torch.int32, device=self.dev)   # sf_group_norm grid barrier
         for fn in self._scratch_users:
             fn(self.scratch)
         self.scratch_bytes = self.scratch.numel()
@@ -686,11 +685,7 @@ class Plan:
         self.slice_counts[grp.label] = len(slices)
         fmax = max([b - a for a, b in slices] + [1])
         specs = {k: (fmax * r, c, dt) for k, (r, c, dt) in pf_specs.items()}
-        if D.GN_FUSED:
-            gn_need = max([N.query("sf_group_norm_fused_workspace", b - a, g.h * g.w, g.c, max_groups)
-                           for g in gn_shapes for a, b in slices] or [0])
-        else:
-            gn_need = max([N.query("sf_group_norm_workspace", fmax, g.h * g.w, g.c) for g in gn_shapes] or [0])
+        gn_need = max([N.query("sf_group_norm_workspace", fmax, g.h * g.w, g.c) for g in gn_shapes] or [0])
         if gn_need:
             specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
@@ -716,10 +711,7 @@ class Plan:
                         epi.act = act
                     k = o.kind
                     ihw, ohw = ish.h * ish.w, osh.h * osh.w
-                    if k is OpKind.GROUP_NORM and D.GN_FUSED:
-                        D.group_norm(st, X, Y, nf, ihw, ish.c, int(o.attrs.get("groups", 1)),
-                                     float(o.attrs.get("eps", 1e-5)), prm, act, scratch["gn_work"], self.gn_barrier)
-                    elif k is OpKind.GROUP_NORM:
+                    if k is OpKind.GROUP_NORM:
                         groups = int(o.attrs.get("groups", 1))
                         stats = scratch["gn_stats"]
                         mean = stats[:nf * groups, 0]

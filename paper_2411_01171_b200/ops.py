@@ -99,19 +99,11 @@ def apply_kernel(kind: OpKind, inputs: Sequence[Tensor5D], params: Mapping | Non
         groups = int(attrs.get("groups", 1))
         p = _convert(kind, attrs, params, dev)
         eps = float(attrs.get("eps", 1e-5))
-        if D.GN_FUSED:
-            work = torch.empty(N.query("sf_group_norm_fused_workspace", frames, hw, s.c, groups), dtype=torch.uint8,
-                               device=dev)
-            barrier = torch.zeros(4, dtype=torch.int32, device=dev)
-            D.group_norm(st, Rows(x, 0, hw), Rows(y, 0, hw), frames, hw, s.c, groups, eps, p, N.ACT_NONE, work,
-                         barrier)
-        else:
-            work = torch.empty(N.query("sf_group_norm_workspace", frames, hw, s.c), dtype=torch.uint8, device=dev)
-            mean = torch.empty(frames * groups, dtype=torch.float32, device=dev)
-            rstd = torch.empty_like(mean)
-            D.group_norm_stats(st, Rows(x, 0, hw), frames, hw, s.c, groups, eps, work, mean, rstd)
-            D.group_norm_apply(st, Rows(x, 0, hw), Rows(y, 0, hw), frames, hw, s.c, groups, mean, rstd, p,
-                               N.ACT_NONE)
+        work = torch.empty(N.query("sf_group_norm_workspace", frames, hw, s.c), dtype=torch.uint8, device=dev)
+        mean = torch.empty(frames * groups, dtype=torch.float32, device=dev)
+        rstd = torch.empty_like(mean)
+        D.group_norm_stats(st, Rows(x, 0, hw), frames, hw, s.c, groups, eps, work, mean, rstd)
+        D.group_norm_apply(st, Rows(x, 0, hw), Rows(y, 0, hw), frames, hw, s.c, groups, mean, rstd, p, N.ACT_NONE)
     elif kind is OpKind.LAYER_NORM:
         p = _convert(kind, attrs, params, dev)
         D.layer_norm(st, Rows(x), Rows(y), 1, rows, s.c, p, float(attrs.get("eps", 1e-5)))
