@@ -1,7 +1,6 @@
 // C ABI of the fused spatial attention core (kernels.py:269-300).
 // Kernels: flash_attn5.cu (CTA pairs, 96/128-key blocks, P over S in TMEM: the
-// default), flash_attn3.cu (CTA pairs, 64-key blocks) and flash_attn2.cu
-// (single CTA; head dim 192 and single-query-tile frames).
+// default) and flash_attn2.cu (single CTA; head dim 192 and single-query-tile frames).
 #include "common.cuh"
 
 #include <cstdlib>
@@ -10,9 +9,6 @@
 namespace sf {
 sf_status flash2_launch(sf_view_t q, sf_view_t k, const void* vt, sf_view_t out, int frames, int HW, int C,
                         float scale, cudaStream_t st);
-sf_status flash3_launch(sf_view_t q, sf_view_t k, const void* vt, sf_view_t out, int frames, int HW, int C,
-                        float scale, cudaStream_t st);
-bool flash3_supported(int C);
 sf_status flash5_launch(sf_view_t q, sf_view_t k, const void* vt, sf_view_t out, int frames, int HW, int C,
                         float scale, cudaStream_t st);
 bool flash5_supported(int C);
@@ -43,10 +39,9 @@ extern "C" sf_status sf_spatial_attention_core(sf_view_t q, sf_view_t k, const v
                SF_ERR_PARAM, "operands must be 16-byte aligned, HW % 8 == 0");
   SF_CHECK_ARG(q.ld == k.ld, SF_ERR_PARAM, "q and k must share a row stride");
   cudaStream_t st = (cudaStream_t)stream;
-  // SF_FLASH=2 / 3 force the older kernels (A/B runs); default: v5 CTA pairs where possible
+  // SF_FLASH=2 forces the single-CTA kernel (A/B runs); default: v5 CTA pairs where possible
   static const char* ver = getenv("SF_FLASH");
   const int v = ver ? atoi(ver) : 5;
   if (v >= 5 && flash5_supported(C) && (HW + 127) / 128 >= 2) return flash5_launch(q, k, vt, out, frames, HW, C, scale, st);
-  if (v >= 3 && flash3_supported(C) && (HW + 127) / 128 >= 2) return flash3_launch(q, k, vt, out, frames, HW, C, scale, st);
   return flash2_launch(q, k, vt, out, frames, HW, C, scale, st);
 }
