@@ -62,4 +62,4 @@ def test_gram_bandwidth_c3_shape():
     ms = s.elapsed_time(e) / 5
     gbs = 25 * n * 2 / (ms * 1e6)
     print(f"gram 25 x {n}: {ms:.3f} ms, {gbs:.0f} GB/s")
-    assert gbs > 1500
+    assert gbs > 4000
