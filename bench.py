@@ -19,8 +19,10 @@ fixed ("scaling": "strong"); time = max over ranks.
 
 ``--impl reference`` times the reference algorithm (oracle port of the numpy
 ``sliceflow`` path, fp32, SlicedLoop, capped16) on the host cores with a
-bounded sample per step (first slice of every group, scaled by the slice
-count; one key step + one tail step, extrapolated to the 13/25 schedule).
+bounded sample per step (the first 4 slices of every group, the others charged
+at the median warm slice; one key step + one tail step, extrapolated to the
+13/25 schedule; anchored once against a complete C3 evaluation,
+profiles/r02_cpu_full_eval_c3.json).
 """
 
 from __future__ import annotations
@@ -168,8 +170,9 @@ def run_reference(args, world, rank):
         "config": {"workload": WORKLOAD[args.config], "schedule": f"{nk} key + {K - nk} tail steps",
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": host_cores(), "kind": "port",
-                         "sample": "first slice of every group (scaled by slice count) for one key step and one "
-                                   f"tail step, extrapolated to {nk}/{K}; {np.mean(samples):.1f} s CPU per sample "
+                         "sample": "first 4 slices of every group (the rest charged at the median warm slice) for "
+                                   f"one key step and one tail step, extrapolated to {nk}/{K}; "
+                                   f"{np.mean(samples):.1f} s CPU per sample "
                                    f"= {100 * smp['fraction']:.1f}% of the extrapolated step time actually run"},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -444,8 +447,9 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = {
             "value": round(cb.steps_per_s(len(sched.key_steps), K, smp), 6), "unit": "steps/s",
             "cores": host_cores(), "kind": "port",
-            "sample": f"oracle fp32 SlicedLoop: first slice of every group scaled by slice count, one key + one "
-                      f"tail step extrapolated to {len(sched.key_steps)}/{K}; {smp['sample_s']:.1f} s CPU = "
+            "sample": f"oracle fp32 SlicedLoop: first 4 slices of every group (the rest at the median warm "
+                      f"slice), one key + one tail step extrapolated to {len(sched.key_steps)}/{K}; "
+                      f"{smp['sample_s']:.1f} s CPU = "
                       f"{100 * smp['fraction']:.1f}% of the extrapolated step time actually run"}
     if rank == 0:
         print(json.dumps(line), flush=True)

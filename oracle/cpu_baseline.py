@@ -4,10 +4,13 @@ Used only by ``bench.py`` (the ``cpu_baseline`` object of our line and the
 ``--impl reference`` arm).  Follows BASELINE.md §2: fp32, SlicedLoop,
 spatial_k = B*T, temporal preset capped16, OpenBLAS on all host cores.
 
-Bounded sample: every group runs only its FIRST slice (one frame for spatial
-groups, one capped16 tile for temporal groups) and its time is scaled by the
-group's slice count -- exact for the for-loop executor, whose slices are
-independent and identically shaped up to the remainder (grouping.py:241-254).
+Bounded sample: every group runs only its first ``max_slices`` slices (one frame
+for spatial groups, one capped16 tile for temporal groups); the unsampled slices
+are charged at the median time of the sampled ones after the first (the first
+slice pays cold caches) -- the for-loop executor's slices are independent and
+identically shaped up to the remainder (grouping.py:241-254).  Checked once
+against a complete C3 evaluation on the GPU box's 16 host cores
+(tests/cpu_full_eval.py, profiles/r02_cpu_full_eval_c3.json).
 Ungrouped Add/Concat nodes run in full.  One full (key) step and one tail
 (skipped) step are sampled; a K-step rehash run is extrapolated as
 |G| * full + (K - |G|) * tail.
@@ -35,7 +38,7 @@ def host_cores() -> int:
 
 
 class CpuBaseline:
-    def __init__(self, cfg, max_slices: int = 1):
+    def __init__(self, cfg, max_slices: int | None = 4):
         self.cfg = cfg
         self.max_slices = max_slices
         self.model = Model(cfg, np.float32)

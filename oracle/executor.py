@@ -39,8 +39,10 @@ def run_chain(ops, x, weights):
     return x
 
 
-def run_group_sliced(group, x, weights, max_slices=None):
-    """Slice, run the chain per slice, reassemble (grouping.py:223-254)."""
+def run_group_sliced(group, x, weights, max_slices=None, slice_times=None):
+    """Slice, run the chain per slice, reassemble (grouping.py:223-254).
+
+    ``slice_times`` (a list) receives the wall time of every slice that ran."""
     shape = Shape5(*x.shape)
     out_shape = group_output_shape(group, shape)
     # zeros, not empty: a sampled run (max_slices) leaves the other slices unwritten
@@ -49,6 +51,7 @@ def run_group_sliced(group, x, weights, max_slices=None):
     if max_slices is not None:
         regions = regions[:max_slices]
     for reg in regions:
+        t0 = time.perf_counter()
         if reg.mode is SliceMode.SPATIAL_BT:
             a, b = reg.bt
             part = x.reshape(shape.b * shape.t, *x.shape[2:])[a:b].copy()[None]
@@ -58,6 +61,8 @@ def run_group_sliced(group, x, weights, max_slices=None):
             (r0, r1), (c0, c1) = reg.rows, reg.cols
             part = np.ascontiguousarray(x[:, :, :, r0:r1, c0:c1])
             out[:, :, :, r0:r1, c0:c1] = run_chain(group.ops, part, weights)
+        if slice_times is not None:
+            slice_times.append(time.perf_counter() - t0)
     return out
 
 
@@ -93,15 +98,20 @@ def evaluate(graph, weights, feeds, mode=ExecMode.REFERENCE, grouped=None, start
             done = [ref]
         else:
             g = grouped.groups[ref]
-            vals[g.tail] = run_group_sliced(g, vals[g.head_input], weights, max_slices)
+            st = []
+            vals[g.tail] = run_group_sliced(g, vals[g.head_input], weights, max_slices, st)
             done = [g.tail]
         if timings is not None:
             dt = time.perf_counter() - t0
-            scale = 1.0
+            est = dt
             if kind == "group" and max_slices is not None:
+                # unsampled slices at the median of the sampled ones after the first (the first
+                # slice of a group pays cold caches: extrapolating it alone overstated a full C3
+                # evaluation by 55 %, profiles/r02_cpu_full_eval_c3.json)
                 n = grouped.groups[ref].plan.n_slices
-                scale = n / min(n, max_slices)
-            timings.append((ref if kind == "node" else grouped.groups[ref].label, dt, dt * scale))
+                warm = sorted(st[1:] or st)
+                est = dt + (n - len(st)) * warm[len(warm) // 2]
+            timings.append((ref if kind == "node" else grouped.groups[ref].label, dt, est))
         for d in done:
             lbl = graph.nodes[d].label
             if lbl in capture:

@@ -35,7 +35,6 @@ constexpr int GN_U = 8;
 __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits,
                                                             double2* partial) {
   griddep_wait();
-  griddep_trigger();
   const int frame = blockIdx.x / splits, split = blockIdx.x % splits;
   const int nvec = C / 8;
   const int rows_per_iter = blockDim.x / nvec > 0 ? blockDim.x / nvec : 1;
@@ -122,7 +121,6 @@ __global__ void __launch_bounds__(256) gn_finalize_kernel(const T* __restrict__ 
                                                           int groups, int gpb, int64_t count, float eps,
                                                           float* mean, float* rstd) {
   griddep_wait();
-  griddep_trigger();
   extern __shared__ double2 tot[];   // [gpb * cg]
   const int cg = C / groups;
   const int frame = blockIdx.y, g0 = blockIdx.x * gpb;
@@ -196,7 +194,6 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(sf_view_t x, sf_view_t y,
                                                        const float* __restrict__ gamma,
                                                        const float* __restrict__ beta, int act) {
   griddep_wait();
-  griddep_trigger();
   const int cg = C / groups, nvec = C / 8;
   const int rpi = nvec <= (int)blockDim.x ? (int)blockDim.x / nvec : 1;   // rows per iteration
   const int64_t total = (int64_t)frames * n_inner;
@@ -266,7 +263,6 @@ __global__ void __launch_bounds__(256, VPL <= 5 ? 4 : 3) layer_norm_kernel(sf_vi
                                                                          const float* __restrict__ beta, float eps,
                                                                          int act) {
   griddep_wait();
-  griddep_trigger();
   // gamma / beta staged in shared memory once per block: the per-row parameter reads were 4
   // L1 loads per 16-byte data vector, competing with the data stream
   extern __shared__ float4 ln_par[];   // [2][C/4]
@@ -362,7 +358,6 @@ template <int OP>
 __global__ void rows_ew_kernel(sf_view_t a, sf_view_t b, sf_view_t y, int n_outer, int n_inner, int C,
                                int b_bcast) {
   griddep_wait();
-  griddep_trigger();
   const int nvec = C / 8;
   const int64_t total = (int64_t)n_outer * n_inner * nvec;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -392,7 +387,6 @@ __global__ void rows_ew_kernel(sf_view_t a, sf_view_t b, sf_view_t y, int n_oute
 
 __global__ void copy_rows_scalar_kernel(sf_view_t x, sf_view_t y, int n_outer, int n_inner, int C) {
   griddep_wait();
-  griddep_trigger();
   const int64_t total = (int64_t)n_outer * n_inner * C;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -405,7 +399,6 @@ __global__ void copy_rows_scalar_kernel(sf_view_t x, sf_view_t y, int n_outer, i
 
 __global__ void downsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int W, int C) {
   griddep_wait();
-  griddep_trigger();
   const int nvec = C / 8, Ho = H / 2, Wo = W / 2;
   const int64_t total = (int64_t)frames * Ho * Wo * nvec;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -428,7 +421,6 @@ __global__ void downsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, i
 // (one load, four coalesced stores; 32-bit index math)
 __global__ void upsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int W, int C) {
   griddep_wait();
-  griddep_trigger();
   const int nvec = C / 8, Wo = 2 * W;
   const uint32_t total = (uint32_t)frames * H * W * nvec;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
@@ -450,7 +442,6 @@ template <int PER>
 __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restrict__ s, int64_t lds,
                                                            bf16* __restrict__ p, int64_t ldp, int n) {
   griddep_wait();
-  griddep_trigger();
   // PER float4 chunks per thread; n % 4 == 0 and 16-byte aligned rows
   const int64_t row = blockIdx.x;
   const float4* src = reinterpret_cast<const float4*>(s + row * lds);
@@ -507,7 +498,6 @@ constexpr int TA_CHUNK = 32;
 __global__ void __launch_bounds__(256) temporal_attn_kernel(sf_view_t qkv, int koff, int voff, sf_view_t out,
                                                             int T, int n_inner, int C, float scale) {
   griddep_wait();
-  griddep_trigger();
   const int pix = blockIdx.x % n_inner, b = blockIdx.x / n_inner;
   __shared__ float S[TA_MAXT][TA_MAXT + 1];
   __shared__ float qs[TA_MAXT][TA_CHUNK + 1];
@@ -664,7 +654,6 @@ __global__ void __launch_bounds__(TQ_WARPS * 32, SPLIT > 1 ? TQ_SPLIT_MINB : TQ_
                                                                           sf_view_t out, int B, int T, int n_inner,
                                                                           int C, float scale_log2) {
   griddep_wait();
-  griddep_trigger();
   extern __shared__ __align__(16) unsigned char tq_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bf16 (*qs)[TQ_LD] = reinterpret_cast<bf16 (*)[TQ_LD]>(tq_smem + warp * 3 * 32 * TQ_LD * 2);
@@ -847,7 +836,6 @@ __global__ void __launch_bounds__(SC_THREADS) conv_smallcin_kernel(const float* 
                                                                    const float* __restrict__ bias, int cout,
                                                                    sf_view_t y) {
   griddep_wait();
-  griddep_trigger();
   extern __shared__ float wsm[];  // [9][cin][cout]
   const int nw = 9 * cin * cout;
   for (int i = threadIdx.x; i < nw; i += blockDim.x) wsm[i] = wt[i];
@@ -907,7 +895,6 @@ __global__ void __launch_bounds__(SCM_THREADS) conv_smallcin_mma_kernel(const fl
                                                                        const float* __restrict__ bias, int cout,
                                                                        sf_view_t y) {
   griddep_wait();
-  griddep_trigger();
   using L = ScmLayout<KP>;
   extern __shared__ __align__(16) uint8_t scm_raw[];
   bf16* sA = reinterpret_cast<bf16*>(scm_raw);
@@ -1023,7 +1010,6 @@ static sf_status conv_smallcin_mma_launch(const float* x, int frames, int H, int
 __global__ void conv_tapsum_kernel(const float* __restrict__ y, int ldy, int frames, int H, int W, int cout,
                                    const float* __restrict__ bias, sf_view_t out) {
   griddep_wait();
-  griddep_trigger();
   const int HW = H * W;
   const int64_t total = (int64_t)frames * HW * cout;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -1046,7 +1032,6 @@ __global__ void conv_tapsum_kernel(const float* __restrict__ y, int ldy, int fra
 __global__ void gemv_kernel(const float* __restrict__ Wm, const float* __restrict__ e, const float* __restrict__ b,
                             float* __restrict__ y, int N, int K) {
   griddep_wait();
-  griddep_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= N) return;
   float a = 0.f;
@@ -1058,7 +1043,6 @@ __global__ void gemv_kernel(const float* __restrict__ Wm, const float* __restric
 __global__ void transpose_f32_kernel(const float* __restrict__ x, float* __restrict__ y, int frames, int A, int B,
                                      int to_rows) {
   griddep_wait();
-  griddep_trigger();
   // to_rows: x[f][A=C][B=HW] -> y[f][HW][C];  else x[f][A=HW][B=C] -> y[f][C][HW]
   const int64_t total = (int64_t)frames * A * B;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -1072,7 +1056,6 @@ __global__ void transpose_f32_kernel(const float* __restrict__ x, float* __restr
 
 __global__ void axpy_kernel(float* __restrict__ x, const float* __restrict__ e, float alpha, int64_t n) {
   griddep_wait();
-  griddep_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = x[i] - alpha * e[i];
 }
@@ -1085,7 +1068,6 @@ constexpr int DOT_BLOCKS = 592, DOT_THREADS = 256;
 __global__ void dot3_partial_kernel(const bf16* __restrict__ a, const bf16* __restrict__ b, int64_t n,
                                     double* __restrict__ part) {
   griddep_wait();
-  griddep_trigger();
   double aa = 0, bb = 0, ab = 0;
   const int64_t nv = n / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1129,7 +1111,6 @@ __global__ void dot3_partial_kernel(const bf16* __restrict__ a, const bf16* __re
 
 __global__ void sum_parts_kernel(const double* __restrict__ part, int nparts, int width, double* __restrict__ out) {
   griddep_wait();
-  griddep_trigger();
   // out[j] = sum_p part[p*width + j], fixed order
   for (int j = threadIdx.x; j < width; j += blockDim.x) {
     double s = 0;

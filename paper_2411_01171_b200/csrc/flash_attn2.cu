@@ -175,7 +175,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   // prologue (barriers, TMEM) done without touching global data: now wait for the
   // producing kernel (PDL) and let the next one be scheduled
   griddep_wait();
-  griddep_trigger();
 
   if (warp == 0) {
     if (lane == 0) {

@@ -254,7 +254,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   // prologue (barriers, TMEM) done without touching global data: now wait for the
   // producing kernel (PDL) and let the next one be scheduled
   griddep_wait();
-  griddep_trigger();
 
   if (warp == 0) {
     {   // whole warp converged, elect.sync issue
@@ -292,6 +291,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         next();
       }
     }
+    griddep_trigger();   // all loads issued: let the next kernel's prologue start
   } else if (warp == 1) {
     if (leader) {
       // ---------------- MMA issuer (leader only, whole warp converged), M = 256 ----------------

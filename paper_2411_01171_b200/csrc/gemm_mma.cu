@@ -75,7 +75,6 @@ __device__ __forceinline__ const bf16* a_addr(const sf_gemm_args& p, const bf16*
 template <bool WK>
 __global__ void __launch_bounds__(THREADS) gemm_kernel(const __grid_constant__ sf_gemm_args p) {
   griddep_wait();
-  griddep_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

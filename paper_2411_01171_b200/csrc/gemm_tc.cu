@@ -470,9 +470,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // prologue (barriers, TMEM) done without touching global data: now wait for the
-  // producing kernel (PDL) and let the next one be scheduled
+  // producing kernel (PDL).  The next kernel is released (griddep_trigger) once this CTA's
+  // producer has issued its last load, so its prologue overlaps our last tiles' MMAs/epilogues.
   griddep_wait();
-  griddep_trigger();
 
   const int kiters = p.taps * p.cblocks;
   // tile walk: a pair walks pair-tiles (two adjacent M-tiles x one N-tile)
@@ -538,6 +538,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+    griddep_trigger();
   } else if (warp == 1) {
     // ================= MMA issuer =================
     // whole warp converged; each tcgen05 instruction is issued by one elect.sync lane, so the

@@ -82,7 +82,6 @@ __global__ void __launch_bounds__(Lay<DIAG>::THREADS, 1) gram_mma_kernel(const b
   using L = Lay<DIAG>;
   constexpr int WARPS = L::WARPS, THREADS = L::THREADS;
   griddep_wait();
-  griddep_trigger();
   extern __shared__ __align__(128) uint8_t smem[];
   const int nb = (K + 31) / 32;
   int bi, bj;
@@ -211,7 +210,6 @@ __global__ void __launch_bounds__(Lay<DIAG>::THREADS, 1) gram_mma_kernel(const b
 // out[i*K + j] = sum over blocks (fixed order) of the job's partials, mirrored
 __global__ void gram_combine_kernel(const double* __restrict__ part, int K, int nblk, double* __restrict__ out) {
   griddep_wait();
-  griddep_trigger();
   const int nb = (K + 31) / 32;
   int bi, bj;
   job_of(blockIdx.x, nb, bi, bj);
