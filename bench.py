@@ -378,7 +378,7 @@ def run_ours(args, world, rank, local):
     achieved = g_fl / (g_ms * 1e9) if g_ms else 0.0
     peak_tf = peaks["bf16_tflops_sustained"]
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"r01_{args.config}_keystep_launch_list.txt")
+    tpath = os.path.join(ROOT, "profiles", f"r02_{args.config}_keystep_launch_list.txt")
     if os.path.exists(tpath):
         for l in open(tpath):
             if l.startswith("{") and "gemm_dram_bytes_per_key_step" in l:
