@@ -6,7 +6,11 @@ several similarity thresholds, on one GPU.
 For every gamma: the key-step schedule G from Algorithm A1 on the calibration
 map (measured on the device), its decision margin, device time of the whole
 K-step run (CUDA graph), and the final latent's deviation from the all-key
-(no-skip) run.  Prints one JSON line per setting.
+(no-skip) run.  "Skip schedule matched to the CPU oracle" (BASELINE config 5):
+A1 is also run on the fp64 oracle's own similarity map (committed record
+profiles/r02_parity_<config>.json, tests/parity_sd.py) at the same gamma, and
+``G_oracle_match`` says whether the device's schedule is the oracle's.
+Prints one JSON line per setting.
 """
 
 import argparse
@@ -53,6 +57,9 @@ def main():
     x0 = initial_latent(cfg)
     _, S = den.calibrate(x0)
     den.trace = None
+    rec_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                            f"r02_parity_{a.config}.json")
+    S_ref = np.asarray(json.load(open(rec_path))["S_ref"]) if os.path.exists(rec_path) else None
     adj = [S.values[i, i + 1] for i in range(K - 1)]
     print(json.dumps({"config": a.config, "similarity": {"mean_adjacent": float(np.mean(adj)),
                                                           "min_adjacent": float(np.min(adj))}}))
@@ -65,12 +72,17 @@ def main():
         gamma = g if g is not None else gamma_for_target(S, tgt)
         sched = key_step_search(S, gamma, K)
         ms, x = timed_run(den, x0, sched)
+        oracle = {}
+        if S_ref is not None:
+            so = key_step_search(S_ref, gamma, K)
+            oracle = {"G_oracle": so.key_steps, "G_oracle_match": so.key_steps == sched.key_steps,
+                      "oracle_margin": so.margin, "s_err": float(np.abs(S.values - S_ref).max())}
         print(json.dumps({
             "setting": f"rehash gamma={gamma:.6f}" + (f" (target {tgt})" if tgt else ""),
             "keys": len(sched.key_steps), "key_steps": sched.key_steps,
             "decision_margin": sched.margin, "run_ms": round(ms, 3), "steps_per_s": round(K / ms * 1e3, 3),
             "speedup_vs_all_key": round(full_ms / ms, 3),
-            "final_max_rel_vs_all_key": float(np.abs(x - x_full).max() / scale)}))
+            "final_max_rel_vs_all_key": float(np.abs(x - x_full).max() / scale), **oracle}))
 
 
 if __name__ == "__main__":
