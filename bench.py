@@ -230,7 +230,7 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
     from paper_2411_01171_b200.harness import Denoiser
     dw = den.model.dw
     bt = cfg.frames * cfg.effective_batch
-    ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=bt, temporal_k=bt)
+    ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=bt, temporal_k=bt, slice_streams=args.ns_streams)
     # drop the headline plan's buffers (weights are shared) before measuring this plan's peak
     import gc
     den._graphs.clear()
@@ -255,7 +255,8 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
     en.record()
     torch.cuda.synchronize()
     ms = st.elapsed_time(en) / n
-    return {"plan": f"spatial k = {bt} (one frame per slice), temporal k = {bt} pixel bands",
+    return {"plan": f"spatial k = {bt} (one frame per slice), temporal k = {bt} pixel bands, "
+                    f"{args.ns_streams} slice stream(s)",
             "value": round(cfg.steps / (ms / 1e3), 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
             "runs": n, "peak_hbm_bytes": int(torch.cuda.max_memory_allocated()),
             "arena_bytes": d2.plan.arena_bytes, "scratch_bytes": d2.plan.scratch_bytes,
@@ -306,7 +307,7 @@ def run_ours(args, world, rank, local):
         from paper_2411_01171_b200.parallel import NcclExchanger
         exchanger = NcclExchanger(rank, world, comm_stream=True)
     ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=args.spatial_k, temporal_k=args.temporal_k,
-                      rank=rank, world=world)
+                      rank=rank, world=world, slice_streams=args.slice_streams)
     if args.scratch_budget_mb:
         ecfg.scratch_budget = args.scratch_budget_mb << 20
     den = Denoiser(cfg, ecfg, exchanger=exchanger)
@@ -481,6 +482,8 @@ def main():
     ap.add_argument("--scratch-budget-mb", type=int, default=None)
     ap.add_argument("--no-north-star-plan", action="store_true")
     ap.add_argument("--plan-only", action="store_true", help="per-rank device memory plan, no GPU needed")
+    ap.add_argument("--slice-streams", type=int, default=1, help="headline plan: streams per sliced group")
+    ap.add_argument("--ns-streams", type=int, default=2, help="north-star plan: streams per sliced group")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args.gpus)

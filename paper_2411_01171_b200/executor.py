@@ -61,6 +61,9 @@ GEMM_KINDS = (OpKind.CONV2D, OpKind.TEMPORAL_CONV, OpKind.LINEAR, OpKind.SPATIAL
 class ExecConfig:
     """Device execution knobs.
 
+    slice_streams: 2 runs a sliced group's consecutive slices on two streams with two scratch
+    copies (slices are independent: disjoint rows of the group output), so the launches of small
+    slices overlap instead of leaving the GPU half idle; 1 (default) = one stream, one copy.
     slicing: "budget" (default) -- per group the fewest slices whose scratch
     fits ``scratch_budget`` (``spatial_k`` / ``temporal_k`` override the count);
     "plan" -- the group's own ``SlicePlan`` (grouping.py:121-127): spatial
@@ -75,6 +78,7 @@ class ExecConfig:
     temporal_k: int | None = None
     scratch_budget: int = 1 << 30
     slicing: str = "budget"
+    slice_streams: int = 1      # 2: consecutive slices of a group alternate between two streams
     gemm_backend: int = 0
     device: str = "cuda"
     rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
@@ -531,22 +535,44 @@ class Plan:
         self.scratch_bytes = self.scratch.numel()
         self.gn_work = None
 
-    def _scratch(self, specs):
-        """Reserve named slice-scratch tensors (bound after compile)."""
+    def _scratch(self, specs, copies: int = 1):
+        """Reserve ``copies`` sets of named slice-scratch tensors (bound after compile)."""
         off, layout = 0, {}
         for name, (rows, cols, dtype) in specs.items():
             es = torch.empty((), dtype=dtype).element_size()
             layout[name] = (off, rows, cols, dtype)
             off += (rows * cols * es + 255) // 256 * 256
-        self.scratch_need = max(self.scratch_need, off)
-        holder = {}
+        self.scratch_need = max(self.scratch_need, off * copies)
+        holders = [{} for _ in range(copies)]
 
         def bind(buf):
-            for name, (o, r, c, dt) in layout.items():
-                es = torch.empty((), dtype=dt).element_size()
-                holder[name] = buf[o:o + r * c * es].view(dt).view(r, c)
+            for k, holder in enumerate(holders):
+                for name, (o, r, c, dt) in layout.items():
+                    es = torch.empty((), dtype=dt).element_size()
+                    holder[name] = buf[k * off + o:k * off + o + r * c * es].view(dt).view(r, c)
         self._scratch_users.append(bind)
-        return holder
+        return holders if copies > 1 else holders[0]
+
+    def _fork(self, st, n):
+        """Streams for ``n`` concurrent slice chains: the launch stream and a side stream ordered
+        after everything already issued on it (ExecConfig.slice_streams)."""
+        if n == 1:
+            return [st]
+        from .parallel import stream_of
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.dev)
+        ev = torch.cuda.Event()
+        ev.record(stream_of(st))
+        self._side.wait_event(ev)
+        return [st, self._side.cuda_stream]
+
+    def _join(self, st, streams):
+        if len(streams) == 1:
+            return
+        from .parallel import stream_of
+        ev = torch.cuda.Event()
+        ev.record(self._side)
+        stream_of(st).wait_event(ev)
 
     def _epilogue(self, tail_id, rows_fn):
         """Epilogue for a GEMM-ending group whose output feeds a fused Add."""
@@ -689,11 +715,18 @@ class Plan:
         if gn_need:
             specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
-        scratch = self._scratch(specs)
+        ncopy = 2 if self.cfg.slice_streams > 1 and len(slices) > 1 else 1
+        scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
         eps_out = self.fp32_out and tail == self.graph.outputs[0]
 
-        def run(st):
-            for sl in slices:
+        def run(st0):
+            streams = self._fork(st0, ncopy)
+            for si, sl in enumerate(slices):
+                one_slice(sl, scratches[si % ncopy], streams[si % ncopy])
+            self._join(st0, streams)
+
+        def one_slice(sl, scratch, st):
+            if True:
                 nf = sl[1] - sl[0]
 
                 def loc(name, shp):
@@ -803,10 +836,17 @@ class Plan:
             fixed.append((o, prev, dst, act, last, oc))
             prev = dst
         steps = fixed
-        scratch = self._scratch(specs)
+        ncopy = 2 if self.cfg.slice_streams > 1 and len(bands) > 1 else 1
+        scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
 
-        def run(st):
-            for band in bands:
+        def run(st0):
+            streams = self._fork(st0, ncopy)
+            for bi_, band in enumerate(bands):
+                one_band(band, scratches[bi_ % ncopy], streams[bi_ % ncopy])
+            self._join(st0, streams)
+
+        def one_band(band, scratch, st):
+            if True:
                 npx = band[1] - band[0]
 
                 def loc(name):

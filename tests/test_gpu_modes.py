@@ -145,3 +145,22 @@ def test_naive_clip_run_matches_oracle_naive_clip():
     print("naiveclip vs oracle naiveclip", r, "oracle naiveclip vs full", div)
     assert r <= 5e-3
     assert div > 4 * r
+
+
+def test_two_slice_streams_bit_identical():
+    """ExecConfig(slice_streams=2): consecutive slices of a group on two streams with two scratch
+    copies give the same bits as one stream (slices are independent; every reduction is per slice
+    and fixed-order), at a per-frame / many-band plan."""
+    from paper_2411_01171_b200.executor import ExecConfig
+    from paper_2411_01171_b200.harness import Denoiser, initial_latent
+    from paper_2411_01171_b200.rehash import StepSchedule
+    for cfg in (C1, UNetConfig(channels=4, frames=5, height=16, width=16, base_channels=64, norm_groups=32,
+                               steps=3)):
+        x0 = initial_latent(cfg)
+        sched = StepSchedule([0, cfg.steps - 1], cfg.steps)
+        bt = cfg.frames
+        a = Denoiser(cfg, ExecConfig(spatial_k=bt, temporal_k=bt)).run(x0, sched)
+        d2 = Denoiser(cfg, ExecConfig(spatial_k=bt, temporal_k=bt, slice_streams=2))
+        b = d2.run(x0, sched)          # CUDA-graph replay with the fork/join captured
+        assert np.array_equal(a, b)
+        assert d2.plan.scratch_bytes >= 2 * Denoiser(cfg, ExecConfig(spatial_k=bt, temporal_k=bt)).plan.scratch_bytes - 4096
