@@ -214,7 +214,8 @@ def slice_summary(plan) -> dict:
     hist: dict[int, int] = {}
     for n in counts.values():
         hist[n] = hist.get(n, 0) + 1
-    return {"policy": f"{plan.cfg.slicing}" + (f" (scratch budget {plan.cfg.scratch_budget >> 20} MiB)"
+    return {"policy": f"{plan.cfg.slicing}" + (f" (scratch budget {plan.cfg.scratch_budget >> 20} MiB per copy, "
+                                               f"{plan.cfg.slice_streams} slice stream(s))"
                                                if plan.cfg.slicing == "budget" else ""),
             "groups": len(counts), "sliced_groups": sum(1 for n in counts.values() if n > 1),
             "max_slices": max(counts.values()) if counts else 0,
@@ -482,7 +483,7 @@ def main():
     ap.add_argument("--scratch-budget-mb", type=int, default=None)
     ap.add_argument("--no-north-star-plan", action="store_true")
     ap.add_argument("--plan-only", action="store_true", help="per-rank device memory plan, no GPU needed")
-    ap.add_argument("--slice-streams", type=int, default=1, help="headline plan: streams per sliced group")
+    ap.add_argument("--slice-streams", type=int, default=2, help="headline plan: streams per sliced group")
     ap.add_argument("--ns-streams", type=int, default=2, help="north-star plan: streams per sliced group")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -61,9 +61,10 @@ GEMM_KINDS = (OpKind.CONV2D, OpKind.TEMPORAL_CONV, OpKind.LINEAR, OpKind.SPATIAL
 class ExecConfig:
     """Device execution knobs.
 
-    slice_streams: 2 runs a sliced group's consecutive slices on two streams with two scratch
-    copies (slices are independent: disjoint rows of the group output), so the launches of small
-    slices overlap instead of leaving the GPU half idle; 1 (default) = one stream, one copy.
+    slice_streams: 2 (default) runs a sliced group's consecutive slices on two streams with two
+    scratch copies (slices are independent: disjoint rows of the group output), so the launches of
+    small slices overlap instead of leaving the GPU half idle; 1 = one stream, one copy.  The budget
+    bounds one copy.
     slicing: "budget" (default) -- per group the fewest slices whose scratch
     fits ``scratch_budget`` (``spatial_k`` / ``temporal_k`` override the count);
     "plan" -- the group's own ``SlicePlan`` (grouping.py:121-127): spatial
@@ -76,9 +77,9 @@ class ExecConfig:
 
     spatial_k: int | None = None
     temporal_k: int | None = None
-    scratch_budget: int = 1 << 30
+    scratch_budget: int = 256 << 20
     slicing: str = "budget"
-    slice_streams: int = 1      # 2: consecutive slices of a group alternate between two streams
+    slice_streams: int = 2      # consecutive slices of a sliced group alternate between two streams
     gemm_backend: int = 0
     device: str = "cuda"
     rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
