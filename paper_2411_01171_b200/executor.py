@@ -712,7 +712,11 @@ class Plan:
         self.slice_counts[grp.label] = len(slices)
         fmax = max([b - a for a, b in slices] + [1])
         specs = {k: (fmax * r, c, dt) for k, (r, c, dt) in pf_specs.items()}
-        gn_need = max([N.query("sf_group_norm_workspace", fmax, g.h * g.w, g.c) for g in gn_shapes] or [0])
+        # the split count of the statistics pass grows as a slice's frame count shrinks: size the
+        # workspace for every slice extent, not only the largest (a 3-frame slice of a plan sized
+        # for 4 frames needs 297 split rows against 296)
+        gn_need = max([N.query("sf_group_norm_workspace", n, g.h * g.w, g.c)
+                       for g in gn_shapes for n in {b - a for a, b in slices}] or [0])
         if gn_need:
             specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
