@@ -311,9 +311,6 @@ def run_ours(args, world, rank, local):
                       rank=rank, world=world, slice_streams=args.slice_streams)
     if args.scratch_budget_mb:
         ecfg.scratch_budget = args.scratch_budget_mb << 20
-    if args.min_slices:
-        ecfg.min_slices = args.min_slices
-        ecfg.min_slices_max_rows = args.min_slices_max_rows
     den = Denoiser(cfg, ecfg, exchanger=exchanger)
     x0 = initial_latent(cfg)
     # calibration (setup, untimed): all-key run recording the probe, then A1
@@ -488,8 +485,6 @@ def main():
     ap.add_argument("--plan-only", action="store_true", help="per-rank device memory plan, no GPU needed")
     ap.add_argument("--slice-streams", type=int, default=2, help="headline plan: streams per sliced group")
     ap.add_argument("--ns-streams", type=int, default=2, help="north-star plan: streams per sliced group")
-    ap.add_argument("--min-slices", type=int, default=0)
-    ap.add_argument("--min-slices-max-rows", type=int, default=1 << 62)
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args.gpus)

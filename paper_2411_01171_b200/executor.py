@@ -80,8 +80,6 @@ class ExecConfig:
     scratch_budget: int = 256 << 20
     slicing: str = "budget"
     slice_streams: int = 2      # consecutive slices of a sliced group alternate between two streams
-    min_slices: int = 1         # at least this many slices per group (with 2 streams: overlapping halves)
-    min_slices_max_rows: int = 1 << 62   # ... only for groups with at most this many input rows
     gemm_backend: int = 0
     device: str = "cuda"
     rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
@@ -710,8 +708,6 @@ class Plan:
                 a += e
         else:
             k = self._k_for(per_frame, f1 - f0, self.cfg.spatial_k)
-            if not self.cfg.spatial_k and frames * HW <= self.cfg.min_slices_max_rows:
-                k = max(k, min(self.cfg.min_slices, f1 - f0))
             slices = [(a + f0, b + f0) for a, b in balanced(f1 - f0, k)]
         self.slice_counts[grp.label] = len(slices)
         fmax = max([b - a for a, b in slices] + [1])
@@ -835,8 +831,6 @@ class Plan:
             k = max(1, min(grp.plan.n_slices, p1 - p0))
         else:
             k = self._k_for(per_pix, p1 - p0, self.cfg.temporal_k)
-            if not self.cfg.temporal_k and B * T * HW <= self.cfg.min_slices_max_rows:
-                k = max(k, min(self.cfg.min_slices, p1 - p0))
         bands = [(a + p0, b + p0) for a, b in balanced(p1 - p0, k)]
         self.slice_counts[grp.label] = len(bands)
         pmax = max([b - a for a, b in bands] + [1])
