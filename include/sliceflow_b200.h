@@ -96,6 +96,12 @@ typedef struct {
   int64_t out_bstride;
   int32_t out_fp32;      /* 1: fp32 output, 0: bf16 */
   int32_t backend;       /* 0 auto, 1 force mma.sync path, 2 force tcgen05 path */
+  /* LayerNorm folded into the GEMM (PLAIN, batch 1): rowstats[2m] = rstd_m, rowstats[2m+1] =
+   * -mean_m*rstd_m of A's row m (sf_layer_norm_stats), colvec[n] = sum_k W[n][k]; the accumulator
+   * becomes rstd_m * (acc - mean_m * colvec[n]) = LN(A)_m . W_n before alpha / bias / act / res.
+   * NULL = off. */
+  const float* rowstats;
+  const float* colvec;
 } sf_gemm_args;
 
 /* ---- GEMM core: conv2d / temporal_conv / linear / attention projections ---- */
@@ -116,6 +122,10 @@ sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int3
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C,
                               int32_t groups, const float* mean, const float* rstd, const float* gamma,
                               const float* beta, int32_t act, void* stream);
+/* Per-row LayerNorm statistics for a folded GEMM: stats[2r] = rstd, stats[2r+1] = -mean*rstd
+ * (two-pass, same arithmetic as sf_layer_norm). */
+sf_status sf_layer_norm_stats(sf_view_t x, int32_t n_outer, int32_t n_inner, int32_t C, float eps, float* stats,
+                              void* stream);
 /* LayerNorm over the C channels of every row (kernels.py:240-244), optional SiLU. */
 sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C,
                         const float* gamma, const float* beta, float eps, int32_t act, void* stream);

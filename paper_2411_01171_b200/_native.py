@@ -40,6 +40,7 @@ class GemmArgs(C.Structure):
         ("res", View), ("res_bstride", i64),
         ("out", View), ("out_bstride", i64),
         ("out_fp32", i32), ("backend", i32),
+        ("rowstats", vp), ("colvec", vp),
     ]
 
 
@@ -54,6 +55,7 @@ _PROTOS = {
     "sf_group_norm_stats": [View, i32, i32, i32, i32, f32, vp, vp, vp, vp],
     "sf_group_norm_apply": [View, View, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp],
     "sf_layer_norm": [View, View, i32, i32, i32, vp, vp, f32, i32, vp],
+    "sf_layer_norm_stats": [View, i32, i32, i32, f32, vp, vp],
     "sf_silu": [View, View, i32, i32, i32, vp],
     "sf_add": [View, View, View, i32, i32, i32, i32, vp],
     "sf_copy_rows": [View, View, i32, i32, i32, vp],

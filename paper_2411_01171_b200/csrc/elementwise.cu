@@ -261,12 +261,12 @@ __global__ void __launch_bounds__(256, VPL <= 5 ? 4 : 3) layer_norm_kernel(sf_vi
                                                                          int n_inner, int C,
                                                                          const float* __restrict__ gamma,
                                                                          const float* __restrict__ beta, float eps,
-                                                                         int act) {
+                                                                         int act, float2* __restrict__ stats) {
   griddep_wait();
   // gamma / beta staged in shared memory once per block: the per-row parameter reads were 4
   // L1 loads per 16-byte data vector, competing with the data stream
   extern __shared__ float4 ln_par[];   // [2][C/4]
-  for (int i = threadIdx.x; i < C / 4; i += blockDim.x) {
+  for (int i = threadIdx.x; !stats && i < C / 4; i += blockDim.x) {
     ln_par[i] = __ldg(reinterpret_cast<const float4*>(gamma) + i);
     ln_par[C / 4 + i] = __ldg(reinterpret_cast<const float4*>(beta) + i);
   }
@@ -324,7 +324,10 @@ __global__ void __launch_bounds__(256, VPL <= 5 ? 4 : 3) layer_norm_kernel(sf_vi
 #pragma unroll
     for (int m = L / 2; m > 0; m >>= 1) q += __shfl_xor_sync(0xffffffffu, q, m);
     const float rs = rsqrtf(q / C + eps);
-    if (live) {
+    if (stats) {
+      // statistics only (LayerNorm folded into the next GEMM, sf_gemm_args.rowstats)
+      if (live && sub == 0) stats[row] = make_float2(rs, -mu * rs);
+    } else if (live) {
       bf16* dst = row_ptr<bf16>(y, (int)(row / n_inner), (int)(row % n_inner));
 #pragma unroll
       for (int k = 0; k < VPL; ++k) {
@@ -1186,11 +1189,29 @@ sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t 
   return launch_status("sf_group_norm_apply");
 }
 
+static sf_status layer_norm_launch(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C,
+                                   const float* gamma, const float* beta, float eps, int32_t act, float2* stats,
+                                   void* stream);
+
 sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C, const float* gamma,
                         const float* beta, float eps, int32_t act, void* stream) {
-  SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0 && C <= 32 * 8 * 12, SF_ERR_SHAPE, "bad extents");
-  SF_CHECK_ARG(view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
+  SF_CHECK_ARG(view_vec8_ok(y), SF_ERR_PARAM, "unaligned view");
   SF_CHECK_ARG(aligned16(gamma) && aligned16(beta), SF_ERR_PARAM, "gamma/beta must be 16-byte aligned");
+  return layer_norm_launch(x, y, n_outer, n_inner, C, gamma, beta, eps, act, nullptr, stream);
+}
+
+sf_status sf_layer_norm_stats(sf_view_t x, int32_t n_outer, int32_t n_inner, int32_t C, float eps, float* stats,
+                              void* stream) {
+  SF_CHECK_ARG(stats && ((uintptr_t)stats & 7) == 0, SF_ERR_PARAM, "stats must be 8-byte aligned");
+  return layer_norm_launch(x, sf_view_t{nullptr, 8, 0}, n_outer, n_inner, C, nullptr, nullptr, eps, 0,
+                           reinterpret_cast<float2*>(stats), stream);
+}
+
+static sf_status layer_norm_launch(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inner, int32_t C,
+                                   const float* gamma, const float* beta, float eps, int32_t act, float2* stats,
+                                   void* stream) {
+  SF_CHECK_ARG(n_outer >= 1 && n_inner >= 1 && C % 8 == 0 && C <= 32 * 8 * 12, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(view_vec8_ok(x), SF_ERR_PARAM, "unaligned view");
   const int64_t rows = (int64_t)n_outer * n_inner;
   cudaStream_t st = (cudaStream_t)stream;
   const int nvec = C / 8;
@@ -1208,9 +1229,10 @@ sf_status sf_layer_norm(sf_view_t x, sf_view_t y, int32_t n_outer, int32_t n_inn
   // register prefetch of the next row group (128 registers, 2 blocks per SM) measured slower
   const int64_t cap = (int64_t)num_sms() * (vpl <= 5 ? 4 : 3);
   const int grid = (int)(g < cap ? (g < 1 ? 1 : g) : cap);
-  const size_t smem = (size_t)C * 2 * sizeof(float);
+  const size_t smem = stats ? 16 : (size_t)C * 2 * sizeof(float);
 #define SF_LN(LL, VV) \
-  launch_k(layer_norm_kernel<LL, VV>, dim3(grid), dim3(256), smem, st, x, y, n_outer, n_inner, C, gamma, beta, eps, act)
+  launch_k(layer_norm_kernel<LL, VV>, dim3(grid), dim3(256), smem, st, x, y, n_outer, n_inner, C, gamma, beta, eps, act, \
+           stats)
   // the template's VPL must cover vpl = ceil(nvec / L)
   if (L == 1 && vpl > 5) SF_LN(1, 10);
   else if (L == 1) SF_LN(1, 5);

@@ -27,6 +27,9 @@ static sf_status validate(const sf_gemm_args* a) {
   if (a->mode == SF_GEMM_TCONV3)
     SF_CHECK_ARG(a->T >= 1 && a->n_outer % a->T == 0, SF_ERR_SHAPE, "tconv: n_outer must be a multiple of T");
   SF_CHECK_ARG(a->act == SF_ACT_NONE || a->act == SF_ACT_SILU, SF_ERR_PARAM, "unknown activation");
+  if (a->rowstats)
+    SF_CHECK_ARG(a->colvec && a->mode == SF_GEMM_PLAIN && a->batch == 1 && ((uintptr_t)a->rowstats & 7) == 0,
+                 SF_ERR_PARAM, "folded LayerNorm needs colvec, PLAIN mode, batch 1, 8-byte aligned stats");
   return SF_OK;
 }
 

@@ -188,8 +188,15 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(const __grid_constant__ s
       for (int ni = 0; ni < 4; ++ni) {
         int n = n0 + wn * 32 + ni * 8 + (lane & 3) * 2;
         if (n >= p.N) continue;
-        float v0 = acc[mi][ni][h * 2 + 0] * p.alpha, v1 = acc[mi][ni][h * 2 + 1] * p.alpha;
+        float v0 = acc[mi][ni][h * 2 + 0], v1 = acc[mi][ni][h * 2 + 1];
         bool two = n + 1 < p.N;
+        if (p.rowstats) {   // folded LayerNorm: rstd * (acc - mean * colsum)
+          const float2 s = reinterpret_cast<const float2*>(p.rowstats)[m];
+          v0 = fmaf(s.x, v0, s.y * p.colvec[n]);
+          if (two) v1 = fmaf(s.x, v1, s.y * p.colvec[n + 1]);
+        }
+        v0 *= p.alpha;
+        v1 *= p.alpha;
         if (p.bias) {
           v0 += p.bias[n];
           if (two) v1 += p.bias[n + 1];

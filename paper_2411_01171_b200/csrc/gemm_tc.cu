@@ -53,6 +53,8 @@ struct Params {
   const float* bias;
   const float* rowbias;
   int64_t rowbias_stride;
+  const float2* rowstats;    // folded LayerNorm (PLAIN): per row (rstd, -mean*rstd)
+  const float* colvec;       // ... and per column sum_k W[n][k]
   int act;
   sf_view_t res;
   int64_t res_bstride;
@@ -267,7 +269,13 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // bias, per-row bias, SiLU.  Vector loads when all W columns are in range (bias rows are
 // 16-byte aligned).
 template <int W = 32>
-__device__ __forceinline__ void epi_columns(const Params& p, float* v, int nb, int64_t o) {
+__device__ __forceinline__ void epi_columns(const Params& p, float* v, int nb, int64_t o, int64_t m = -1) {
+  if (p.rowstats && m >= 0) {   // folded LayerNorm: rstd_m * (acc - mean_m * colsum_n)
+    const float2 s = p.rowstats[m];
+    const bool full = nb + W <= p.N;
+#pragma unroll
+    for (int j = 0; j < W; ++j) v[j] = fmaf(s.x, v[j], s.y * ((full || nb + j < p.N) ? __ldg(p.colvec + nb + j) : 0.f));
+  }
   if (p.alpha != 1.f) {
 #pragma unroll
     for (int j = 0; j < W; ++j) v[j] *= p.alpha;
@@ -637,6 +645,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           float v[32];
           tmem_ld32(tbase + c, v);
           const int nb = n0 + c;
+          if (p.rowstats && valid) {
+            const float2 s = p.rowstats[o * p.n_inner + i];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fmaf(s.x, v[j], s.y * ((nb + j < p.N) ? __ldg(p.colvec + nb + j) : 0.f));
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
           if (p.bias) {
@@ -740,10 +753,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         if (has_res) mbar_wait(rf, use & 1);
         uint8_t* srow = hbuf + row * (HC * 2);
+        const int64_t srow_m = (p.rowstats && valid) ? o * p.n_inner + i : -1;   // folded-LN row
         auto finish32 = [&](int c) {
           float v[32];
           tmem_ld32(tbase + eh * HC + c, v);
-          epi_columns<32>(p, v, hn0 + c, o);
+          epi_columns<32>(p, v, hn0 + c, o, srow_m);
           bf16x8* sp = reinterpret_cast<bf16x8*>(srow + c * 2);
           if (has_res) {
 #pragma unroll
@@ -763,7 +777,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int c = HC - 16;
           float v[16];
           tmem_ld16(tbase + eh * HC + c, v);
-          epi_columns<16>(p, v, hn0 + c, o);
+          epi_columns<16>(p, v, hn0 + c, o, srow_m);
           bf16x8* sp = reinterpret_cast<bf16x8*>(srow + c * 2);
           if (has_res) {
 #pragma unroll
@@ -817,6 +831,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nb = n0 + c;
         if (valid && nb < p.N) {
           const int ncols = min(32, p.N - nb);
+          if (p.rowstats) {
+            const float2 s = p.rowstats[o * p.n_inner + i];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncols) v[j] = fmaf(s.x, v[j], s.y * __ldg(p.colvec + nb + j));
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
           if (p.bias) {
@@ -1125,6 +1145,8 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   p.bias = a.bias;
   p.rowbias = a.rowbias;
   p.rowbias_stride = a.rowbias_stride;
+  p.rowstats = reinterpret_cast<const float2*>(a.rowstats);
+  p.colvec = a.colvec;
   p.act = a.act;
   p.res = a.res;
   p.res_bstride = a.res_bstride;

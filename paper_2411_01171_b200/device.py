@@ -119,7 +119,7 @@ class DeviceWeights:
 def gemm_args(*, mode, n_outer, n_inner, cin, n, a: Rows, w: torch.Tensor, w_ld=None, w_kmajor=True,
               out: Rows, out_fp32=False, bias=None, rowbias=None, rowbias_stride=0, act=N.ACT_NONE,
               res: Rows | None = None, H=0, W=0, T=0, batch=1, a_bstride=0, w_bstride=0, out_bstride=0,
-              res_bstride=0, alpha=1.0, backend=0, w_ptr=None):
+              res_bstride=0, alpha=1.0, backend=0, w_ptr=None, rowstats=None, colvec=None):
     args = N.GemmArgs()
     args.mode, args.n_outer, args.n_inner = mode, n_outer, n_inner
     args.H, args.W, args.T = H, W, T
@@ -139,6 +139,8 @@ def gemm_args(*, mode, n_outer, n_inner, cin, n, a: Rows, w: torch.Tensor, w_ld=
     args.out, args.out_bstride = out.view(), out_bstride
     args.out_fp32 = 1 if out_fp32 else 0
     args.backend = backend
+    args.rowstats = rowstats.data_ptr() if rowstats is not None else None
+    args.colvec = colvec.data_ptr() if colvec is not None else None
     return args
 
 
@@ -283,12 +285,33 @@ def _spatial_core_materialized(stream, frames, HW, C, scratch, backend):
          out_bstride=HW * C, backend=backend)
 
 
-def temporal_attention(stream, x: Rows, y: Rows, B, T, n_inner, C, prm, epi: Epilogue, scratch, backend=0):
-    """Per-pixel single-head attention over T frames (kernels.py:303-308)."""
+def ln_fold_weights(wqkv: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor) -> dict:
+    """A LayerNorm (kernels.py:240-244) folded into the projection that consumes it:
+    LN(x)_r . W_n = rstd_r * (x_r . W'_n - mean_r * sum_k W'_nk) + (beta . W_n), W' = W diag(gamma).
+    The column sums are taken over the bf16-rounded W' the GEMM multiplies by."""
+    w = wqkv.float()
+    wf = (w * gamma[None, :]).to(torch.bfloat16).contiguous()
+    return {"w": wf, "colsum": wf.float().sum(1).contiguous(), "cb": (w @ beta).contiguous()}
+
+
+def temporal_attention(stream, x: Rows, y: Rows, B, T, n_inner, C, prm, epi: Epilogue, scratch, backend=0,
+                       fold=None):
+    """Per-pixel single-head attention over T frames (kernels.py:303-308).
+
+    ``fold = (weights from ln_fold_weights, eps)``: ``x`` is the LayerNorm's raw input; one
+    statistics pass (mean, rstd per row) replaces the LayerNorm's normalised write + re-read, and
+    the QKV GEMM applies it in its epilogue."""
     qkv, o = scratch["qkv"], scratch["o"]
     bt = B * T
-    gemm(stream, mode=N.GEMM_PLAIN, n_outer=bt, n_inner=n_inner, cin=C, n=3 * C, a=x, w=prm["wqkv"],
-         out=Rows(qkv, 0, n_inner), backend=backend)
+    if fold is None:
+        gemm(stream, mode=N.GEMM_PLAIN, n_outer=bt, n_inner=n_inner, cin=C, n=3 * C, a=x, w=prm["wqkv"],
+             out=Rows(qkv, 0, n_inner), backend=backend)
+    else:
+        fw, eps = fold
+        stats = scratch["lnstats"]
+        N.call("sf_layer_norm_stats", x.view(), bt, n_inner, C, eps, stats.data_ptr(), stream)
+        gemm(stream, mode=N.GEMM_PLAIN, n_outer=bt, n_inner=n_inner, cin=C, n=3 * C, a=x, w=fw["w"],
+             out=Rows(qkv, 0, n_inner), bias=fw["cb"], rowstats=stats, colvec=fw["colsum"], backend=backend)
     N.call("sf_temporal_attention_core", Rows(qkv, 0, n_inner).view(), C, 2 * C, Rows(o, 0, n_inner).view(), B, T,
            n_inner, C, 1.0 / math.sqrt(C), stream)
     gemm(stream, mode=N.GEMM_PLAIN, n_outer=bt, n_inner=n_inner, cin=C, n=C, a=Rows(o, 0, n_inner), w=prm["wo"],

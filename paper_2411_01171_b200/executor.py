@@ -80,6 +80,7 @@ class ExecConfig:
     scratch_budget: int = 256 << 20
     slicing: str = "budget"
     slice_streams: int = 2      # consecutive slices of a sliced group alternate between two streams
+    ln_fold: bool = True        # LayerNorm -> temporal attention: statistics pass + folded QKV GEMM
     gemm_backend: int = 0
     device: str = "cuda"
     rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
@@ -803,9 +804,20 @@ class Plan:
         steps, pp_specs = [], {}        # name -> (rows per pixel, cols, dtype)
         i = nb = 0
         flops = 0.0
+        fold_ln = {}                    # temporal attention id -> the LayerNorm folded into its QKV GEMM
         while i < len(ops):
             o = ops[i]
             nxt = ops[i + 1] if i + 1 < len(ops) else None
+            if (self.cfg.ln_fold and o.kind is OpKind.LAYER_NORM and nxt is not None
+                    and nxt.kind is OpKind.TEMPORAL_ATTENTION):
+                fold_ln[nxt.id] = o
+                pt = self.dw.p[nxt.id]
+                if "fold" not in pt:
+                    pl = self.dw.p[o.id]
+                    pt["fold"] = D.ln_fold_weights(pt["wqkv"], pl["gamma"], pl["beta"])
+                pp_specs["lnstats"] = (B * T, 2, torch.float32)
+                i += 1
+                continue
             fuse_act = nxt is not None and nxt.kind is OpKind.SILU
             last = (i + (2 if fuse_act else 1)) >= len(ops)
             oc = self.shapes[ops[i + (1 if fuse_act else 0)].id].c
@@ -877,7 +889,9 @@ class Plan:
                     elif k is OpKind.LINEAR:
                         D.linear(st, X, Y, B * T, npx, cin, oc, prm, epi, backend)
                     elif k is OpKind.TEMPORAL_ATTENTION:
-                        D.temporal_attention(st, X, Y, B, T, npx, cin, prm, epi, scratch, backend)
+                        ln = fold_ln.get(o.id)
+                        fold = None if ln is None else (prm["fold"], float(ln.attrs.get("eps", 1e-5)))
+                        D.temporal_attention(st, X, Y, B, T, npx, cin, prm, epi, scratch, backend, fold)
                     else:
                         raise InvalidParam(f"no temporal lowering for {k.value}")
                     cin = oc
