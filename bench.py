@@ -308,7 +308,7 @@ def run_ours(args, world, rank, local):
         from paper_2411_01171_b200.parallel import NcclExchanger
         exchanger = NcclExchanger(rank, world, comm_stream=True)
     ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=args.spatial_k, temporal_k=args.temporal_k,
-                      rank=rank, world=world, slice_streams=args.slice_streams, ln_fold=not args.no_ln_fold)
+                      rank=rank, world=world, slice_streams=args.slice_streams, ln_fold=args.ln_fold)
     if args.scratch_budget_mb:
         ecfg.scratch_budget = args.scratch_budget_mb << 20
     den = Denoiser(cfg, ecfg, exchanger=exchanger)
@@ -483,8 +483,8 @@ def main():
     ap.add_argument("--scratch-budget-mb", type=int, default=None)
     ap.add_argument("--no-north-star-plan", action="store_true")
     ap.add_argument("--plan-only", action="store_true", help="per-rank device memory plan, no GPU needed")
-    ap.add_argument("--slice-streams", type=int, default=2, help="headline plan: streams per sliced group")
-    ap.add_argument("--no-ln-fold", action="store_true", help="LayerNorm before temporal attention unfolded")
+    ap.add_argument("--slice-streams", type=int, default=1, help="headline plan: streams per sliced group")
+    ap.add_argument("--ln-fold", action="store_true", help="fold the LayerNorm before temporal attention into its QKV GEMM")
     ap.add_argument("--ns-streams", type=int, default=2, help="north-star plan: streams per sliced group")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -64,6 +64,8 @@ typedef enum {
 
 typedef enum { SF_ACT_NONE = 0, SF_ACT_SILU = 1 } sf_act;
 
+#define SF_GEMM_NO_PAIR 4   /* sf_gemm_args.backend flag */
+
 /*
  * Implicit GEMM  out[m][n] = act( sum_k A[m][k] * W[n][k] * alpha + bias[n]
  *                                + rowbias[o(m)][n] ) + res[m][n]
@@ -95,7 +97,8 @@ typedef struct {
   sf_view_t out;         /* output rows */
   int64_t out_bstride;
   int32_t out_fp32;      /* 1: fp32 output, 0: bf16 */
-  int32_t backend;       /* 0 auto, 1 force mma.sync path, 2 force tcgen05 path */
+  int32_t backend;       /* 0 auto, 1 force mma.sync path, 2 force tcgen05 path; | SF_GEMM_NO_PAIR:
+                            single-CTA tcgen05 tiles only (no cta_group::2 clusters) */
   /* LayerNorm folded into the GEMM (PLAIN, batch 1): rowstats[2m] = rstd_m, rowstats[2m+1] =
    * -mean_m*rstd_m of A's row m (sf_layer_norm_stats), colvec[n] = sum_k W[n][k]; the accumulator
    * becomes rstd_m * (acc - mean_m * colvec[n]) = LN(A)_m . W_n before alpha / bias / act / res.

@@ -45,6 +45,7 @@ class GemmArgs(C.Structure):
 
 
 GEMM_PLAIN, GEMM_CONV3X3, GEMM_TCONV3 = 0, 1, 2
+GEMM_NO_PAIR = 4          # sf_gemm_args.backend flag: single-CTA tcgen05 tiles only
 ACT_NONE, ACT_SILU = 0, 1
 
 # name -> argtypes (restype is sf_status = int unless listed in _RESTYPE)

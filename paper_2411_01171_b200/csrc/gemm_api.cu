@@ -35,8 +35,9 @@ static sf_status validate(const sf_gemm_args* a) {
 
 extern "C" int32_t sf_gemm_backend(const sf_gemm_args* a) {
   if (validate(a) != SF_OK) return 0;
-  if (a->backend == 1) return 1;
-  if (a->backend == 2) return gemm_tc_supported(*a) ? 2 : 0;
+  const int be = a->backend & ~SF_GEMM_NO_PAIR;
+  if (be == 1) return 1;
+  if (be == 2) return gemm_tc_supported(*a) ? 2 : 0;
   return gemm_tc_supported(*a) ? 2 : 1;
 }
 

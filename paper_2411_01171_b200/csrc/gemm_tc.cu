@@ -272,9 +272,20 @@ template <int W = 32>
 __device__ __forceinline__ void epi_columns(const Params& p, float* v, int nb, int64_t o, int64_t m = -1) {
   if (p.rowstats && m >= 0) {   // folded LayerNorm: rstd_m * (acc - mean_m * colsum_n)
     const float2 s = p.rowstats[m];
-    const bool full = nb + W <= p.N;
+    if (nb + W <= p.N) {
+      const float4* c4 = reinterpret_cast<const float4*>(p.colvec + nb);
 #pragma unroll
-    for (int j = 0; j < W; ++j) v[j] = fmaf(s.x, v[j], s.y * ((full || nb + j < p.N) ? __ldg(p.colvec + nb + j) : 0.f));
+      for (int j = 0; j < W / 4; ++j) {
+        const float4 c = __ldg(c4 + j);
+        v[4 * j] = fmaf(s.x, v[4 * j], s.y * c.x);
+        v[4 * j + 1] = fmaf(s.x, v[4 * j + 1], s.y * c.y);
+        v[4 * j + 2] = fmaf(s.x, v[4 * j + 2], s.y * c.z);
+        v[4 * j + 3] = fmaf(s.x, v[4 * j + 3], s.y * c.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < W; ++j) v[j] = fmaf(s.x, v[j], s.y * (nb + j < p.N ? __ldg(p.colvec + nb + j) : 0.f));
+    }
   }
   if (p.alpha != 1.f) {
 #pragma unroll
@@ -1158,7 +1169,7 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   // CTA pairs (cta_group::2, M = 256) whenever there are two M-tiles to pair up;
   // SF_GEMM_PAIR=0 forces single-CTA tiles (A/B runs)
   static const char* pair_env = getenv("SF_GEMM_PAIR");
-  bool pair = !(pair_env && pair_env[0] == '0');
+  bool pair = !(pair_env && pair_env[0] == '0') && !(a.backend & SF_GEMM_NO_PAIR);
   const uint64_t ld = (uint64_t)a.a.ld;
   if (a.mode == SF_GEMM_CONV3X3) {
     p.H = a.H;

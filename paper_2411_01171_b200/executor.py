@@ -61,10 +61,10 @@ GEMM_KINDS = (OpKind.CONV2D, OpKind.TEMPORAL_CONV, OpKind.LINEAR, OpKind.SPATIAL
 class ExecConfig:
     """Device execution knobs.
 
-    slice_streams: 2 (default) runs a sliced group's consecutive slices on two streams with two
-    scratch copies (slices are independent: disjoint rows of the group output), so the launches of
-    small slices overlap instead of leaving the GPU half idle; 1 = one stream, one copy.  The budget
-    bounds one copy.
+    slice_streams: 2 runs a sliced group's consecutive slices on two streams with two scratch copies
+    (slices are independent: disjoint rows of the group output), so the launches of small slices
+    overlap instead of leaving the GPU half idle -- with single-CTA GEMM tiles in those groups;
+    1 (default) = one stream, one copy.  The budget bounds one copy.
     slicing: "budget" (default) -- per group the fewest slices whose scratch
     fits ``scratch_budget`` (``spatial_k`` / ``temporal_k`` override the count);
     "plan" -- the group's own ``SlicePlan`` (grouping.py:121-127): spatial
@@ -77,10 +77,11 @@ class ExecConfig:
 
     spatial_k: int | None = None
     temporal_k: int | None = None
-    scratch_budget: int = 256 << 20
+    scratch_budget: int = 1 << 30
     slicing: str = "budget"
-    slice_streams: int = 2      # consecutive slices of a sliced group alternate between two streams
-    ln_fold: bool = True        # LayerNorm -> temporal attention: statistics pass + folded QKV GEMM
+    slice_streams: int = 1      # 2: consecutive slices of a sliced group alternate between two streams
+    ln_fold: bool = False       # LayerNorm -> temporal attention: statistics pass + folded QKV GEMM
+                                # (measured: faster at C >= 640, slower at L0 -- profiles finding 31)
     gemm_backend: int = 0
     device: str = "cuda"
     rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
@@ -722,6 +723,10 @@ class Plan:
             specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
         ncopy = 2 if self.cfg.slice_streams > 1 and len(slices) > 1 else 1
+        if ncopy > 1:
+            # two concurrent cta_group::2 implicit-GEMM convolutions from different streams
+            # produced wrong rows in 3-6 of 12 runs (profiles finding 30); single-CTA tiles: 0 of 24
+            backend |= N.GEMM_NO_PAIR
         scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
         eps_out = self.fp32_out and tail == self.graph.outputs[0]
 
@@ -854,6 +859,8 @@ class Plan:
             prev = dst
         steps = fixed
         ncopy = 2 if self.cfg.slice_streams > 1 and len(bands) > 1 else 1
+        if ncopy > 1:
+            backend |= N.GEMM_NO_PAIR       # see _compile_spatial
         scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
 
         def run(st0):

@@ -124,15 +124,19 @@ def test_c3_full_size_slicing_properties():
     a2, _, _ = execute(g, ExecMode.SLICED_LOOP, inp, w)
     assert np.isfinite(a.data).all()
     assert np.array_equal(a.data, a2.data)
-    b, led, _ = execute(g, ExecMode.SLICED_LOOP, inp, w, cfg=ExecConfig(spatial_k=7, temporal_k=5))
+    b, led, _ = execute(g, ExecMode.SLICED_LOOP, inp, w, cfg=ExecConfig(spatial_k=7, temporal_k=5, slice_streams=2))
     led.assert_closed()
     r = float(np.abs(b.data - a.data).max() / np.abs(a.data).max())
     print("c3 ragged vs default rel", r)
     assert r <= 2e-2
     # the same ragged plan on one stream: bit-identical to the two-stream run (uneven 4- and
-    # 3-frame slices in flight together; each needs its own statistics workspace)
+    # 3-frame slices in flight together; each needs its own statistics workspace), several times
+    # (a race shows up intermittently, profiles finding 30)
     b1, _, _ = execute(g, ExecMode.SLICED_LOOP, inp, w, cfg=ExecConfig(spatial_k=7, temporal_k=5, slice_streams=1))
-    assert np.array_equal(b1.data, b.data)
+    for _ in range(4):
+        b2, _, _ = execute(g, ExecMode.SLICED_LOOP, inp, w,
+                           cfg=ExecConfig(spatial_k=7, temporal_k=5, slice_streams=2))
+        assert np.array_equal(b1.data, b2.data)
 
 
 def test_naive_clip_run_matches_oracle_naive_clip():
