@@ -914,7 +914,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  if (EPI > 0 && warp == EPI_W0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // every thread that issued bulk (TMA) stores -- the leader of each column half -- waits for them
+  // before the CTA retires: its shared-memory staging may belong to another kernel's CTA right
+  // after (a concurrent stream), so a store still reading it would write that CTA's bytes
+  if (EPI > 0 && (warp == EPI_W0 || warp == EPI_W0 + 4) && lane == 0)
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   if (PAIR) cluster_sync();

@@ -724,8 +724,8 @@ class Plan:
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
         ncopy = 2 if self.cfg.slice_streams > 1 and len(slices) > 1 else 1
         if ncopy > 1:
-            # two concurrent cta_group::2 implicit-GEMM convolutions from different streams
-            # produced wrong rows in 3-6 of 12 runs (profiles finding 30); single-CTA tiles: 0 of 24
+            # two concurrent CTA-pair implicit-GEMM convolutions from different streams produced
+            # wrong rows intermittently (profiles finding 30); single-CTA tiles never did
             backend |= N.GEMM_NO_PAIR
         scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
         eps_out = self.fp32_out and tail == self.graph.outputs[0]
