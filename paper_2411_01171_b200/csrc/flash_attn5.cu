@@ -290,6 +290,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                      h * (D / 2) + (int)rank * (D / 4), f);
         next();
       }
+      // drain: every slot's release (multicast commit) has landed before the CTA retires
+      for (int s = 0; s < NSLOT; ++s) {
+        mbar_wait(&r_empty[slot], ph ^ 1);
+        next();
+      }
     }
     griddep_trigger();   // all loads issued: let the next kernel's prologue start
   } else if (warp == 1) {

@@ -556,6 +556,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      // drain: the MMA's release of every ring slot (a tcgen05.commit, multicast into this CTA's
+      // barrier in PAIR mode) must have landed before the CTA retires -- an arrive landing later
+      // would write into the shared memory of whichever CTA the SM hosts next
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
     }
     griddep_trigger();
   } else if (warp == 1) {
