@@ -122,9 +122,12 @@ def dist_setup(n_gpus):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # SF_BENCH_ONE_GPU=1 (testing only): every rank on cuda:0 over gloo -- exercises the
+        # sharded launch sequences, exchanges and reductions of N > 1 on a one-GPU box
+        one = os.environ.get("SF_BENCH_ONE_GPU") == "1"
         if torch.cuda.is_available():
-            torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+            torch.cuda.set_device(0 if one else local)
+        dist.init_process_group("nccl" if torch.cuda.is_available() and not one else "gloo")
     return world, rank, local
 
 
