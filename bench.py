@@ -488,7 +488,7 @@ def main():
     ap.add_argument("--plan-only", action="store_true", help="per-rank device memory plan, no GPU needed")
     ap.add_argument("--slice-streams", type=int, default=1, help="headline plan: streams per sliced group")
     ap.add_argument("--ln-fold", action="store_true", help="fold the LayerNorm before temporal attention into its QKV GEMM")
-    ap.add_argument("--ns-streams", type=int, default=2, help="north-star plan: streams per sliced group")
+    ap.add_argument("--ns-streams", type=int, default=4, help="north-star plan: streams per sliced group")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args.gpus)

@@ -620,6 +620,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc_phase = 0;
     uint32_t tcount = 0;
     const uint32_t tempty_l = PAIR ? leader_addr(&tempty[0]) : 0;
+    int chunk = 0;   // EPI 3: this half's chunk count over all its tiles (staging buffer = chunk & 1)
     for (int64_t tile = t_first; tile < n_tiles; tile += t_step, ++tcount) {
       const int64_t tm = my_tm(tile);
       const int n0 = (int)(tile % p.tiles_n) * BN;
@@ -655,14 +656,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // fp32 output through two 16 KB staging chunks (128 rows x 32 cols, 128-byte swizzle:
         // a thread's row lands in a different bank group than its 7 neighbours), one TMA
         // store per chunk; a chunk buffer is refilled once its store from two chunks ago is read
-        // each column half (4 warps) stages its own chunks: buffers 2*eh + (k & 1), its own
-        // leader and named barrier (2 + eh)
+        // each column half (4 warps) stages its own chunks: buffers 2*eh + (chunk & 1), its own
+        // leader and named barrier (2 + eh).  The chunk count runs across tiles: with BN = 64
+        // a half has one chunk per tile, and a per-tile count would refill the buffer whose
+        // store (the previous tile's) wait_group.read 1 leaves in flight -- corrupted rows
+        // whenever that store's shared-memory read was slow (concurrent streams: profiles
+        // finding 30)
         const bool store_leader = warp == EPI_W0 + 4 * eh && lane == 0;
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        int k = 0;
 #pragma unroll 1
-        for (int c = eh * 32; c < BN; c += 64, ++k) {
+        for (int c = eh * 32; c < BN; c += 64, ++chunk) {
           float v[32];
           tmem_ld32(tbase + c, v);
           const int nb = n0 + c;
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
           }
-          uint8_t* buf = sOut + (2 * eh + (k & 1)) * F32_CHUNK_BYTES;
+          uint8_t* buf = sOut + (2 * eh + (chunk & 1)) * F32_CHUNK_BYTES;
           if (store_leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           if (eh) asm volatile("bar.sync 3, 128;" ::: "memory");
           else asm volatile("bar.sync 2, 128;" ::: "memory");

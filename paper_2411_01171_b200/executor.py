@@ -34,6 +34,7 @@ in the tests.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -61,10 +62,10 @@ GEMM_KINDS = (OpKind.CONV2D, OpKind.TEMPORAL_CONV, OpKind.LINEAR, OpKind.SPATIAL
 class ExecConfig:
     """Device execution knobs.
 
-    slice_streams: 2 runs a sliced group's consecutive slices on two streams with two scratch copies
-    (slices are independent: disjoint rows of the group output), so the launches of small slices
-    overlap instead of leaving the GPU half idle -- with single-CTA GEMM tiles in those groups;
-    1 (default) = one stream, one copy.  The budget bounds one copy.
+    slice_streams: s > 1 runs a sliced group's consecutive slices round-robin on s streams with s
+    scratch copies (slices are independent: disjoint rows of the group output), so the launches of
+    small slices overlap instead of leaving the GPU idle -- with single-CTA GEMM tiles in those
+    groups; 1 (default) = one stream, one copy.  The budget bounds one copy.
     slicing: "budget" (default) -- per group the fewest slices whose scratch
     fits ``scratch_budget`` (``spatial_k`` / ``temporal_k`` override the count);
     "plan" -- the group's own ``SlicePlan`` (grouping.py:121-127): spatial
@@ -79,7 +80,7 @@ class ExecConfig:
     temporal_k: int | None = None
     scratch_budget: int = 1 << 30
     slicing: str = "budget"
-    slice_streams: int = 1      # 2: consecutive slices of a sliced group alternate between two streams
+    slice_streams: int = 1      # s > 1: consecutive slices of a sliced group round-robin over s streams
     ln_fold: bool = False       # LayerNorm -> temporal attention: statistics pass + folded QKV GEMM
                                 # (measured: faster at C >= 640, slower at L0 -- profiles finding 31)
     gemm_backend: int = 0
@@ -557,25 +558,26 @@ class Plan:
         return holders if copies > 1 else holders[0]
 
     def _fork(self, st, n):
-        """Streams for ``n`` concurrent slice chains: the launch stream and a side stream ordered
-        after everything already issued on it (ExecConfig.slice_streams)."""
+        """Streams for ``n`` concurrent slice chains: the launch stream and n - 1 side streams
+        ordered after everything already issued on it (ExecConfig.slice_streams)."""
         if n == 1:
             return [st]
         from .parallel import stream_of
-        if getattr(self, "_side", None) is None:
-            self._side = torch.cuda.Stream(device=self.dev)
+        sides = self.__dict__.setdefault("_sides", [])
+        while len(sides) < n - 1:
+            sides.append(torch.cuda.Stream(device=self.dev))
         ev = torch.cuda.Event()
         ev.record(stream_of(st))
-        self._side.wait_event(ev)
-        return [st, self._side.cuda_stream]
+        for s in sides[:n - 1]:
+            s.wait_event(ev)
+        return [st] + [s.cuda_stream for s in sides[:n - 1]]
 
     def _join(self, st, streams):
-        if len(streams) == 1:
-            return
         from .parallel import stream_of
-        ev = torch.cuda.Event()
-        ev.record(self._side)
-        stream_of(st).wait_event(ev)
+        for s in self.__dict__.get("_sides", [])[:len(streams) - 1]:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            stream_of(st).wait_event(ev)
 
     def _epilogue(self, tail_id, rows_fn):
         """Epilogue for a GEMM-ending group whose output feeds a fused Add."""
@@ -722,10 +724,11 @@ class Plan:
         if gn_need:
             specs["gn_work"] = ((gn_need + 3) // 4, 1, torch.float32)
             specs["gn_stats"] = (2 * fmax * max_groups, 1, torch.float32)
-        ncopy = 2 if self.cfg.slice_streams > 1 and len(slices) > 1 else 1
-        if ncopy > 1:
-            # two concurrent CTA-pair implicit-GEMM convolutions from different streams produced
-            # wrong rows intermittently (profiles finding 30); single-CTA tiles never did
+        ncopy = max(1, min(self.cfg.slice_streams, len(slices)))
+        if ncopy > 1 and os.environ.get("SF_STREAM_PAIRS") != "1":
+            # concurrent slices: single-CTA GEMM tiles pack the SMs better than CTA pairs
+            # (north-star plan, same box: 48.6 / 61.0 / 63.3 steps/s at 2 / 4 / 6 streams vs
+            # 45.9 / 58.1 / 60.6 with pairs; SF_STREAM_PAIRS=1 is the A/B knob)
             backend |= N.GEMM_NO_PAIR
         scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
         eps_out = self.fp32_out and tail == self.graph.outputs[0]
@@ -858,8 +861,8 @@ class Plan:
             fixed.append((o, prev, dst, act, last, oc))
             prev = dst
         steps = fixed
-        ncopy = 2 if self.cfg.slice_streams > 1 and len(bands) > 1 else 1
-        if ncopy > 1:
+        ncopy = max(1, min(self.cfg.slice_streams, len(bands)))
+        if ncopy > 1 and os.environ.get("SF_STREAM_PAIRS") != "1":
             backend |= N.GEMM_NO_PAIR       # see _compile_spatial
         scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
 

@@ -114,6 +114,50 @@ def test_conv3x3_tapwise(backend, F_, H, W, C, Co):
     assert rel(out, ref) <= 1e-3
 
 
+@pytest.mark.parametrize("backend", [2, 2 | N.GEMM_NO_PAIR])
+def test_fp32_epilogue_concurrent_streams(backend):
+    """fp32-output GEMMs with one 32-column staging chunk per column half (N = 36 -> BN = 64,
+    the out_conv's tap projection) on four streams at once, next to a 1 GiB HBM copy on a fifth
+    stream, 20 times, against the same GEMMs run one after another: bit-identical.  Regression
+    for the staging-buffer reuse that let a tile overwrite the chunk its previous tile's TMA
+    store was still reading (profiles finding 30): with the copy slowing the stores, the old
+    kernel corrupted rows in 34-38 of 40 such runs (tools/race_tapwise.py --hog-mb)."""
+    torch.manual_seed(9)
+    HW, C, Nn, S, nf = 9216, 320, 36, 4, 4
+    xs = [rnd(nf * HW, C) for _ in range(S)]
+    w = rnd(Nn, C, scale=C ** -0.5)
+    outs = [torch.empty(nf * HW, Nn, dtype=torch.float32, device=dev) for _ in range(S)]
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    hog = torch.cuda.Stream()
+    hog_src = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    hog_dst = torch.empty_like(hog_src)
+
+    def launch(k, st):
+        D.gemm(st, mode=N.GEMM_PLAIN, n_outer=nf, n_inner=HW, cin=C, n=Nn, a=Rows(xs[k], 0, HW), w=w,
+               out=Rows(outs[k], 0, HW), out_fp32=True, backend=backend)
+
+    main = torch.cuda.current_stream()
+    for k in range(S):
+        launch(k, main.cuda_stream)
+    torch.cuda.synchronize()
+    ref = [o.clone() for o in outs]
+    assert rel(ref[0], xs[0].float() @ w.float().t()) <= 1e-2
+    for _ in range(20):
+        for o in outs:
+            o.fill_(float("nan"))
+        ev = torch.cuda.Event()
+        ev.record(main)
+        hog.wait_event(ev)
+        with torch.cuda.stream(hog):
+            hog_dst.copy_(hog_src)
+            hog_dst.copy_(hog_src)
+        for k, s in enumerate(streams):
+            s.wait_event(ev)
+            launch(k, s.cuda_stream)
+        torch.cuda.synchronize()
+        assert all(torch.equal(o, r) for o, r in zip(outs, ref))
+
+
 @pytest.mark.parametrize("backend", [1, 2])
 @pytest.mark.parametrize("B,T,P,C,band", [(1, 25, 576, 320, None), (1, 25, 144, 128, None), (2, 8, 64, 64, None),
                                           (1, 16, 1024, 64, (100, 612))])
