@@ -163,6 +163,15 @@ sf_status sf_spatial_attention_core(sf_view_t q, sf_view_t k, const void* vt, sf
  * scale) v into out.  T <= 64. */
 sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, sf_view_t out, int32_t B,
                                      int32_t T, int32_t n_inner, int32_t C, float scale, void* stream);
+/* Whole temporal attention op, fused (tcgen05/TMEM; replaces the QKV projection, the core and
+ * the output projection of kernels.py:276-308 for one LayerNorm'd input x):
+ *   out = softmax(x Mqk x^T) x Mvo  (+ res),  per pixel over its T frames,
+ * with w = [Mqk^T ; Mvo^T] bf16 [2C][C] row-major, Mqk = Wq Wk^T log2(e)/sqrt(C), Mvo = Wv Wo.
+ * x, res, out: bf16 row views (o = b*T + t, i = pixel).  res may be null.
+ * Supported: T <= 128, C in {64, 128, 192, 256, 320}. */
+int32_t sf_temporal_attention_fused_supported(int32_t T, int32_t C);
+sf_status sf_temporal_attention_fused(sf_view_t x, const void* w, sf_view_t res, sf_view_t out, int32_t B,
+                                      int32_t T, int32_t n_inner, int32_t C, void* stream);
 
 /* ---- network edges ---- */
 /* in_conv with tiny cin: x fp32 channels-last [frames][H*W][cin] -> bf16 rows */

@@ -66,6 +66,8 @@ _PROTOS = {
     "sf_flash_supported": [i32, i32],
     "sf_spatial_attention_core": [View, View, vp, View, i32, i32, i32, f32, vp],
     "sf_temporal_attention_core": [View, i32, i32, View, i32, i32, i32, i32, f32, vp],
+    "sf_temporal_attention_fused_supported": [i32, i32],
+    "sf_temporal_attention_fused": [View, vp, View, View, i32, i32, i32, i32, vp],
     "sf_conv3x3_smallcin": [vp, i32, i32, i32, i32, vp, vp, i32, View, vp],
     "sf_conv3x3_tapsum": [vp, i32, i32, i32, i32, i32, vp, View, vp],
     "sf_gemv_f32": [vp, vp, vp, vp, i32, i32, vp],
@@ -85,6 +87,7 @@ _RESTYPE = {
     "sf_gram_workspace": i64,
     "sf_gemm_backend": i32,
     "sf_flash_supported": i32,
+    "sf_temporal_attention_fused_supported": i32,
     "sf_last_error": C.c_char_p,
     "sf_version": i32,
 }

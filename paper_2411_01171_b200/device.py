@@ -22,6 +22,7 @@ the C ABI.  Nothing here computes on the host.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -68,6 +69,18 @@ def f32(a: np.ndarray, dev) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).contiguous()
 
 
+def temporal_fused_weights(wq, wk, wv, wo, dev) -> torch.Tensor:
+    """[Mqk^T ; Mvo^T] (bf16 [2C][C], K-major B operands) for sf_temporal_attention_fused:
+    Mqk = Wq Wk^T log2(e)/sqrt(C) and Mvo = Wv Wo in fp64 (kernels.py:285-292 right-multiplies:
+    q = x Wq, ..., out = ctx Wo), so x Mqk x^T is the reference's scaled score in log2 units and
+    (P x) Mvo its P (x Wv) Wo."""
+    wq, wk, wv, wo = (np.asarray(w, dtype=np.float64) for w in (wq, wk, wv, wo))
+    C = wq.shape[0]
+    mqk = (wq @ wk.T) * (1.4426950408889634 / math.sqrt(C))
+    mvo = wv @ wo
+    return bf16(np.concatenate([mqk.T, mvo.T], axis=0), dev)
+
+
 class DeviceWeights:
     """All parameters of a WeightBundle in kernel layout on one device."""
 
@@ -108,7 +121,11 @@ class DeviceWeights:
             return {"gamma": f32(prm["gamma"], d), "beta": f32(prm["beta"], d)}
         if k in (OpKind.SPATIAL_ATTENTION, OpKind.TEMPORAL_ATTENTION):
             qkv = np.concatenate([np.asarray(prm[n]).T for n in ("wq", "wk", "wv")], axis=0)
-            return {"wqkv": bf16(qkv, d), "wo": bf16(np.asarray(prm["wo"]).T, d)}
+            out = {"wqkv": bf16(qkv, d), "wo": bf16(np.asarray(prm["wo"]).T, d)}
+            C = qkv.shape[1]
+            if k is OpKind.TEMPORAL_ATTENTION and C % 64 == 0 and C <= 320:
+                out["wfused"] = temporal_fused_weights(prm["wq"], prm["wk"], prm["wv"], prm["wo"], d)
+            return out
         raise InvalidParam(f"no device layout for {k}")
 
 
@@ -294,6 +311,18 @@ def ln_fold_weights(wqkv: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor)
     return {"w": wf, "colsum": wf.float().sum(1).contiguous(), "cb": (w @ beta).contiguous()}
 
 
+def fused_temporal_ok(prm, T, C, epi=None, backend=0, fold=None) -> bool:
+    """Whether the op runs as one sf_temporal_attention_fused launch (tcgen05; C <= 320, T <= 128,
+    epilogue = residual only).  ``SF_TATTN_FUSED=0`` keeps the three-launch path (A/B runs)."""
+    if os.environ.get("SF_TATTN_FUSED") == "0" or "wfused" not in prm or fold is not None:
+        return False
+    if (backend & 3) == 1:      # mma.sync forced: no tcgen05 kernels
+        return False
+    if epi is not None and (epi.rowbias is not None or epi.act):
+        return False
+    return bool(N.query("sf_temporal_attention_fused_supported", T, C))
+
+
 def temporal_attention(stream, x: Rows, y: Rows, B, T, n_inner, C, prm, epi: Epilogue, scratch, backend=0,
                        fold=None):
     """Per-pixel single-head attention over T frames (kernels.py:303-308).
@@ -301,6 +330,10 @@ def temporal_attention(stream, x: Rows, y: Rows, B, T, n_inner, C, prm, epi: Epi
     ``fold = (weights from ln_fold_weights, eps)``: ``x`` is the LayerNorm's raw input; one
     statistics pass (mean, rstd per row) replaces the LayerNorm's normalised write + re-read, and
     the QKV GEMM applies it in its epilogue."""
+    if fused_temporal_ok(prm, T, C, epi, backend, fold):
+        N.call("sf_temporal_attention_fused", x.view(), prm["wfused"].data_ptr(),
+               epi.res.view() if epi.res is not None else N.View(0, 0, 0), y.view(), B, T, n_inner, C, stream)
+        return
     qkv, o = scratch["qkv"], scratch["o"]
     bt = B * T
     if fold is None:

@@ -840,8 +840,12 @@ class Plan:
                 flops += 2.0 * B * T * HW * C * oc
             elif o.kind is OpKind.TEMPORAL_ATTENTION:
                 flops += B * HW * (8.0 * T * C * C + 4.0 * T * T * C)
-                pp_specs["qkv"] = (B * T, 3 * C, torch.bfloat16)
-                pp_specs["o"] = (B * T, C, torch.bfloat16)
+                emb_epi = last and self.epilogue_of.get(tail, (None, None, False))[2]
+                if fuse_act or emb_epi or not D.fused_temporal_ok(self.dw.p[o.id], T, self.shapes[o.id].c,
+                                                                  backend=backend, fold=fold_ln.get(o.id)):
+                    # three launches (QKV GEMM, core, output GEMM) through slice scratch
+                    pp_specs["qkv"] = (B * T, 3 * C, torch.bfloat16)
+                    pp_specs["o"] = (B * T, C, torch.bfloat16)
             i += 2 if fuse_act else 1
         # exact per-pixel slice scratch -> band count under the budget
         per_pix = sum(r * c * torch.empty((), dtype=dt).element_size() for r, c, dt in pp_specs.values())

@@ -231,6 +231,47 @@ def test_temporal_core(B, T, P, C):
     assert rel(o, ref) <= 1.5e-2
 
 
+@pytest.mark.parametrize("B,T,P,C,res,band", [
+    (1, 25, 600, 320, True, None),      # C3 L0 shape: 5 pixels x 25 frames per tile
+    (1, 25, 9216, 320, True, None),     # a full C3 L0 frame plane (1844 tiles, persistent grid)
+    (2, 25, 333, 320, False, None),     # B = 2, ragged last tile
+    (1, 64, 100, 320, True, None),      # C4: T = 64 -> 2 pixels per tile
+    (1, 8, 250, 128, True, None), (1, 16, 130, 128, False, None), (1, 25, 77, 192, True, None),
+    (1, 5, 90, 256, True, None), (1, 100, 7, 320, True, None),
+    (1, 25, 1000, 320, True, (300, 517)),   # a pixel band of a wider plane (row stride 1000)
+])
+def test_temporal_attention_fused(B, T, P, C, res, band):
+    """sf_temporal_attention_fused (x Mqk x^T softmax, (P x) Mvo, + residual) vs torch fp32 of the
+    reference's op order: q = x Wq, k = x Wk, v = x Wv, softmax(q k^T / sqrt(C)) v Wo
+    (kernels.py:276-308), per pixel over its T frames.  max_rel <= 1.5e-2 (bf16 inputs, one
+    bf16 rounding of x Mqk and of P x)."""
+    torch.manual_seed(11)
+    x = rnd(B * T * P, C, scale=1.0)
+    ws = [torch.randn(C, C, device=dev, dtype=torch.float64) * (1.0 / C ** 0.5) for _ in range(4)]
+    wq, wk, wv, wo = ws
+    wf = D.temporal_fused_weights(*(w.cpu().numpy() for w in ws), dev)
+    r = rnd(B * T * P, C) if res else None
+    out = torch.full((B * T * P, C), float("nan"), dtype=torch.bfloat16, device=dev)
+    p0, p1 = band if band else (0, P)
+    n = p1 - p0
+    view = lambda t: Rows(t, p0, P)
+    N.call("sf_temporal_attention_fused", view(x).view(), wf.data_ptr(), view(r).view() if res else N.View(0, 0, 0),
+           view(out).view(), B, T, n, C, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    xs = x.double().view(B, T, P, C)[:, :, p0:p1].permute(0, 2, 1, 3)      # [B, n, T, C]
+    q, k, v = xs @ wq, xs @ wk, xs @ wv
+    ref = (torch.softmax(q @ k.transpose(-1, -2) / C ** 0.5, dim=-1) @ v) @ wo
+    ref = ref.permute(0, 2, 1, 3)
+    if res:
+        ref = ref + r.double().view(B, T, P, C)[:, :, p0:p1]
+    got = out.view(B, T, P, C)[:, :, p0:p1]
+    print("fused temporal attention max_rel", rel(got, ref))
+    assert rel(got, ref) <= 1.5e-2
+    if band:   # rows outside the band untouched
+        assert torch.isnan(out.view(B, T, P, C)[:, :, :p0].float()).all()
+        assert torch.isnan(out.view(B, T, P, C)[:, :, p1:].float()).all()
+
+
 @pytest.mark.parametrize("C", [8, 32, 64, 96, 128, 192, 320, 640, 960, 1280, 1920, 2560])
 def test_layer_norm_widths(C):
     """sf_layer_norm vs torch layer_norm at every lanes-per-row / vectors-per-lane dispatch."""
