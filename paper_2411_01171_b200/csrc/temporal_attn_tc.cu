@@ -38,15 +38,18 @@ struct Cfg {
   static constexpr int C = NCH * 64;
   static constexpr int HALF = C / 2;                   // weight stage: [C/2 output ch][64 input ch]
   static constexpr int W_STAGE = HALF * 128;
-  static constexpr int NW_FIT = (SMEM_CAP - 1024 - 1024 - NCH * CHUNK) / W_STAGE;
+  static constexpr int NW_FIT = (SMEM_CAP - 1024 - 1536 - NCH * CHUNK) / W_STAGE;
   static constexpr int NW = NW_FIT > 12 ? 12 : NW_FIT; // weight ring slots
   static constexpr int X_OFF = 0, W_OFF = NCH * CHUNK;
   static constexpr int BAR_OFF = W_OFF + NW * W_STAGE;
-  static constexpr int BAR_BYTES = (2 + 2 * NW + 8) * 8 + 8;   // mbarriers + TMEM slot
-  static constexpr int INV_OFF = BAR_OFF + 512;                // float[128]: softmax 1/row sum
-  static constexpr int TOTAL = 1024 + INV_OFF + 512;
+  static constexpr int BAR_BYTES = (2 + 2 * NW + 14) * 8 + 8;  // mbarriers + TMEM slot
+  static constexpr int INV_OFF = BAR_OFF + 512;                // float[2][128]: softmax row max / sum
+  static constexpr int TOTAL = 1024 + INV_OFF + 1024;
   // TMEM column map (see the header)
   static constexpr int A32 = 0, A16 = C, S = 0, B32 = 512 - C, B16 = 0, Y = 512 - C;
+  // B = P x in two N pieces split on a 64-channel (swizzle atom) boundary: [0, NLO), [NLO, C)
+  static constexpr int NLO = HALF / 64 * 64;
+  static_assert(NLO >= 64 && C - NLO <= 256, "B pieces");
   static_assert(C >= 128 && C + C / 2 <= 512 && 128 <= 512 - C, "TMEM column map");
   static_assert(W_STAGE % 1024 == 0, "swizzle atom alignment");
   static_assert(NW >= 3 && BAR_BYTES <= 512 && TOTAL <= SMEM_CAP, "shared memory budget");
@@ -209,16 +212,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* x_empty = bars + 1;     // MMA: last read of the x tile (B = P x) done
   uint64_t* w_full = bars + 2;      // [NW]
   uint64_t* w_empty = w_full + NW;  // [NW]
-  uint64_t* a_full = w_empty + NW;  // MMA: A = x Mqk in TMEM
-  uint64_t* a_st = a_full + 1;      // 8 warps: A packed to bf16
-  uint64_t* s_full = a_st + 1;      // MMA: S in TMEM
-  uint64_t* p_full = s_full + 1;    // 4 warps: P written over S
-  uint64_t* b_full = p_full + 1;    // MMA: B = P x in TMEM
-  uint64_t* b_st = b_full + 1;      // 8 warps: B packed
-  uint64_t* y_full = b_st + 1;      // MMA: Y in TMEM
-  uint64_t* y_free = y_full + 1;    // 8 warps: Y read out of TMEM
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(y_free + 1);
-  float* inv_sum = reinterpret_cast<float*>(base + L::INV_OFF);
+  uint64_t* a_full = w_empty + NW;  // [2] MMA: column half h of A = x Mqk in TMEM
+  uint64_t* a_st = a_full + 2;      // [2] 4 warps of half h: A half packed to bf16
+  uint64_t* s_full = a_st + 2;      // MMA: S in TMEM
+  uint64_t* p_full = s_full + 1;    // 8 warps: P written over S
+  uint64_t* b_full = p_full + 1;    // [2] MMA: B = P x columns of half h in TMEM
+  uint64_t* b_st = b_full + 2;      // [2] 4 warps of half h: B half packed
+  uint64_t* y_full = b_st + 2;      // [2] MMA: output half h of Y in TMEM
+  uint64_t* y_free = y_full + 2;    // [2] 4 warps of half h: Y half read out of TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(y_free + 2);
+  float* red = reinterpret_cast<float*>(base + L::INV_OFF);   // [2 halves][128 rows] row max / sum
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -228,14 +231,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
     }
-    mbar_init(a_full, 1);
-    mbar_init(a_st, 8);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&a_full[h], 1);
+      mbar_init(&a_st[h], 4);
+      mbar_init(&b_full[h], 1);
+      mbar_init(&b_st[h], 4);
+      mbar_init(&y_full[h], 1);
+      mbar_init(&y_free[h], 4);
+    }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
-    mbar_init(b_full, 1);
-    mbar_init(b_st, 8);
-    mbar_init(y_full, 1);
-    mbar_init(y_free, 8);
+    mbar_init(p_full, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // rows R..127 of the x tile are never written by TMA (the box has R rows): zero them once, so
@@ -275,10 +280,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(x_empty, (it & 1) ^ 1);
       mbar_expect_tx_e(x_full, NCH * 128 * p.R);
       for (int j = 0; j < NCH; ++j) tma4_e(&mX, x_full, sX + j * CHUNK, j * 64, i0, 0, z);
-      for (int j = 0; j < NCH; ++j)
-        for (int h = 0; h < 2; ++h) wload(j * 64, h * HALF);          // Mqk^T
-      for (int j = 0; j < NCH; ++j)
-        for (int h = 0; h < 2; ++h) wload(j * 64, C + h * HALF);      // Mvo^T
+      for (int h = 0; h < 2; ++h)
+        for (int j = 0; j < NCH; ++j) wload(j * 64, h * HALF);        // Mqk^T, output half h
+      for (int h = 0; h < 2; ++h)
+        for (int j = 0; j < NCH; ++j) wload(j * 64, C + h * HALF);    // Mvo^T, output half h
     }
     // drain: every weight slot released before the CTA retires
     for (int s = 0; s < NW; ++s) {
@@ -293,41 +298,46 @@ __global__ void __launch_bounds__(THREADS, 1)
     int slot = 0;
     uint32_t wph = 0;
     const uint32_t xb = smem_u32(sX), wb = smem_u32(sW);
-    // D[0, C) (at dcol) = A x W^T over NCH x 2 weight stages; A from the x tile (smem) or,
-    // a_tmem >= 0, packed bf16 in TMEM
-    auto gemm_w = [&](uint32_t dcol, int a_tmem) {
+    // output half h of D (at dcol) = A x W^T over NCH weight stages; A from the x tile (smem)
+    // or, a_tmem >= 0, packed bf16 in TMEM
+    auto gemm_half = [&](uint32_t dcol, int a_tmem, int h) {
 #pragma unroll 1
-      for (int j = 0; j < NCH; ++j)
-        for (int h = 0; h < 2; ++h) {
-          mbar_wait(&w_full[slot], wph);
-          fence_after();
-          const uint64_t bd = kdesc(wb + slot * L::W_STAGE);
-          const uint32_t d = tmem + dcol + h * HALF;
-          if (a_tmem < 0) {
-            const uint64_t ad = kdesc(xb + j * CHUNK);
+      for (int j = 0; j < NCH; ++j) {
+        mbar_wait(&w_full[slot], wph);
+        fence_after();
+        const uint64_t bd = kdesc(wb + slot * L::W_STAGE);
+        const uint32_t d = tmem + dcol + h * HALF;
+        if (a_tmem < 0) {
+          const uint64_t ad = kdesc(xb + j * CHUNK);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) mma_ss(d, ad + 2 * k, bd + 2 * k, idesc(HALF), (j | k) != 0);
-          } else {
+          for (int k = 0; k < 4; ++k) mma_ss(d, ad + 2 * k, bd + 2 * k, idesc(HALF), (j | k) != 0);
+        } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_ts(d, tmem + a_tmem + (j * 4 + k) * 8, bd + 2 * k, idesc(HALF), (j | k) != 0);
-          }
-          commit_e(&w_empty[slot]);
-          if (++slot == NW) {
-            slot = 0;
-            wph ^= 1;
-          }
+          for (int k = 0; k < 4; ++k)
+            mma_ts(d, tmem + a_tmem + (j * 4 + k) * 8, bd + 2 * k, idesc(HALF), (j | k) != 0);
         }
+        commit_e(&w_empty[slot]);
+        if (++slot == NW) {
+          slot = 0;
+          wph ^= 1;
+        }
+      }
     };
     uint32_t it = 0;
     for (int64_t t = t0; t < p.n_tiles; t += dt, ++it) {
       const uint32_t ph = it & 1;
       mbar_wait(x_full, ph);
-      mbar_wait(y_free, ph ^ 1);    // the previous tile's Y has left TMEM
       fence_after();
-      gemm_w(L::A32, -1);           // A = x Mqk
-      commit_e(a_full);
-      mbar_wait(a_st, ph);
+      // A = x Mqk.  Half 0 ([0, C/2)) overlaps only operands the in-order pipe has consumed,
+      // so it runs under the previous tile's epilogue; half 1 overlaps that tile's Y half 0
+      gemm_half(L::A32, -1, 0);
+      commit_e(&a_full[0]);
+      mbar_wait(&y_free[0], ph ^ 1);
+      fence_after();
+      gemm_half(L::A32, -1, 1);
+      commit_e(&a_full[1]);
+      mbar_wait(&a_st[0], ph);
+      mbar_wait(&a_st[1], ph);
       fence_after();
 #pragma unroll 1
       for (int j = 0; j < NCH; ++j) {   // S = A x^T (x rows as the K-major B: [n = key][k = ch])
@@ -339,20 +349,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       commit_e(s_full);
       mbar_wait(p_full, ph);
       fence_after();
+      // B = P x: 16 keys per step, x MN-major, in two N pieces on swizzle-atom boundaries.
+      // The high piece [NLO, C) holds all of column half 1 and goes first: half 1 is packed
+      // into B16 [C/4, C/2) while the low piece still reads P -- disjoint from P [0, 64) when
+      // C >= 256; half 0's B16 [0, C/4) overlaps P, so it waits for the whole product
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {     // B = P x: 16 keys per step, x MN-major
-        const uint32_t pa = tmem + L::S + k * 8;
-        for (int n0 = 0; n0 < C; n0 += 256) {
-          const int nw = C - n0 < 256 ? C - n0 : 256;
-          mma_ts(tmem + L::B32 + n0, pa, mndesc(xb + (n0 / 64) * CHUNK + k * 2048), idesc(nw, true), k != 0);
-        }
-      }
+      for (int k = 0; k < 8; ++k)
+        mma_ts(tmem + L::B32 + L::NLO, tmem + L::S + k * 8, mndesc(xb + (L::NLO / 64) * CHUNK + k * 2048),
+               idesc(C - L::NLO, true), k != 0);
+      if (C >= 256) commit_e(&b_full[1]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        mma_ts(tmem + L::B32, tmem + L::S + k * 8, mndesc(xb + k * 2048), idesc(L::NLO, true), k != 0);
       commit_e(x_empty);
-      commit_e(b_full);
-      mbar_wait(b_st, ph);
+      commit_e(&b_full[0]);
+      if (C < 256) commit_e(&b_full[1]);
+      mbar_wait(&b_st[0], ph);
+      mbar_wait(&b_st[1], ph);
       fence_after();
-      gemm_w(L::Y, L::B16);         // Y = B Mvo
-      commit_e(y_full);
+      gemm_half(L::Y, L::B16, 0);   // Y = B Mvo, output half 0 ...
+      commit_e(&y_full[0]);
+      gemm_half(L::Y, L::B16, 1);   // ... and half 1
+      commit_e(&y_full[1]);
     }
   } else {
     // ---------------- packing / softmax / epilogue: tile row r, column half g ----------------
@@ -362,12 +380,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int pix = r % p.bi, fr = r / p.bi;
     const bool live = r < p.R;
-    uint32_t kmask[4];   // keys of my pixel: pix + k * bi, k < T
+    uint32_t kmask[2];   // my keys among [64 g, 64 g + 64): pix + k * bi, k < T
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < 2; ++w) {
       kmask[w] = 0u;
       for (int e = 0; e < 32; ++e) {
-        const int c = 32 * w + e;
+        const int c = 64 * g + 32 * w + e;
         if (live && c < p.R && c % p.bi == pix) kmask[w] |= 1u << e;
       }
     }
@@ -375,59 +393,56 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int64_t t = t0; t < p.n_tiles; t += dt, ++it) {
       const uint32_t ph = it & 1;
       const int z = (int)(t / p.n_pg), i0 = (int)(t % p.n_pg) * p.bi;
-      // A -> bf16 operand
-      mbar_wait(a_full, ph);
+      // my half of A -> bf16 operand
+      mbar_wait(&a_full[g], ph);
       fence_after();
       pack_cols<HALF>(trow + L::A32 + g * HALF, trow + L::A16 + g * (HALF / 2));
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(a_st);
-      if (g == 0) {
-        // softmax over this row's keys (same pixel, frames 0..T-1), streamed through TMEM in
-        // 32-key chunks: max, then exp2 + sum with the unnormalised P packed over the S
-        // columns already read; 1/sum is applied to Y in the epilogue (it commutes with P x Mvo)
-        mbar_wait(s_full, ph);
-        fence_after();
-        float m = -INFINITY;
+      if (lane == 0) mbar_arrive(&a_st[g]);
+      // softmax over this row's keys (same pixel, frames 0..T-1); each half of the CTA holds 64
+      // keys of the row: row max exchanged through shared memory, the unnormalised P packed over
+      // S, 1/sum applied to Y in the epilogue (it commutes with (P x) Mvo)
+      mbar_wait(s_full, ph);
+      fence_after();
+      uint32_t sv[64];
+      tld32(trow + L::S + 64 * g, sv);
+      tld32(trow + L::S + 64 * g + 32, sv + 32);
+      tld_wait();
+      float m = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint32_t sv[32];
-          tld32(trow + L::S + 32 * k, sv);
-          tld_wait();
+      for (int e = 0; e < 64; ++e)
+        if ((kmask[e >> 5] >> (e & 31)) & 1u) m = fmaxf(m, __uint_as_float(sv[e]));
+      red[g * 128 + r] = m;
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // both halves' S read, maxima published
+      m = fmaxf(m, red[(g ^ 1) * 128 + r]);
+      float sum = 0.f;
+      uint32_t pk[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if ((kmask[k] >> e) & 1u) m = fmaxf(m, __uint_as_float(sv[e]));
-        }
-        float sum = 0.f;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint32_t sv[32], pk[16];
-          tld32(trow + L::S + 32 * k, sv);
-          tld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float x = ((kmask[k] >> e) & 1u) ? ex2(__uint_as_float(sv[e]) - m) : 0.f;
-            sv[e] = __float_as_uint(x);
-            sum += x;
-          }
-#pragma unroll
-          for (int e = 0; e < 16; ++e) pk[e] = pack2(sv[2 * e], sv[2 * e + 1]);
-          tst16(trow + L::S + 16 * k, pk);   // packed chunk k lands on columns already read
-        }
-        tst_wait();
-        inv_sum[r] = live ? 1.f / sum : 0.f;
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+      for (int e = 0; e < 32; ++e) {
+        const float a0 = ((kmask[(2 * e) >> 5] >> ((2 * e) & 31)) & 1u) ? ex2(__uint_as_float(sv[2 * e]) - m) : 0.f;
+        const float a1 =
+            ((kmask[(2 * e + 1) >> 5] >> ((2 * e + 1) & 31)) & 1u) ? ex2(__uint_as_float(sv[2 * e + 1]) - m) : 0.f;
+        sum += a0 + a1;
+        pk[e] = pack2(__float_as_uint(a0), __float_as_uint(a1));
       }
-      // B -> bf16 operand
-      mbar_wait(b_full, ph);
+      tst32(trow + L::S + 32 * g, pk);
+      tst_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // maxima consumed before the sums reuse red
+      red[g * 128 + r] = sum;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float inv = live ? 1.f / (sum + red[(g ^ 1) * 128 + r]) : 0.f;
+      // my half of B -> bf16 operand
+      mbar_wait(&b_full[g], ph);
       fence_after();
       pack_cols<HALF>(trow + L::B32 + g * HALF, trow + L::B16 + g * (HALF / 2));
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(b_st);
-      // epilogue: residual half-row prefetched while Y = B Mvo runs, then Y (+ res) -> out
+      if (lane == 0) mbar_arrive(&b_st[g]);
+      // epilogue, output half g: residual prefetched while Y = B Mvo runs, then Y/sum (+ res)
       const int i = i0 + pix;
       const bool valid = live && i < p.n_inner;
       const int64_t o = (int64_t)z * p.T + fr;
@@ -439,10 +454,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int u = 0; u < HALF / 8; ++u) rr[u] = __ldg(rs + u);
       }
-      mbar_wait(y_full, ph);
+      mbar_wait(&y_full[g], ph);
       fence_after();
-      asm volatile("bar.sync 1, 256;" ::: "memory");   // inv_sum of this tile written (warps 2..5)
-      const float inv = inv_sum[r];
 #pragma unroll
       for (int cc = 0; cc < HALF; cc += 32) {
         uint32_t y[32];
@@ -467,8 +480,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(y_free);
-      asm volatile("bar.sync 1, 256;" ::: "memory");   // inv_sum read before the next tile's softmax
+      if (lane == 0) mbar_arrive(&y_free[g]);
+      // both halves done with this tile's Y and sums before either packs the next tile's A
+      // into columns that overlap the other half's Y
+      asm volatile("bar.sync 1, 256;" ::: "memory");
     }
   }
   fence_before();

@@ -62,6 +62,10 @@ class CallProfiler:
             elif name == "sf_temporal_attention_core":
                 b, t, n_inner, c = a[4], a[5], a[6], a[7]
                 flops = 4.0 * b * n_inner * t * t * c
+            elif name == "sf_temporal_attention_fused":
+                b, t, n_inner, c = a[4], a[5], a[6], a[7]
+                # the reference op's algorithmic work: four C x C projections + two T x T products
+                flops = b * n_inner * (8.0 * t * c * c + 4.0 * t * t * c)
             self.records.append((name, s, e, flops, nbytes))
         N.call = timed
         return self
