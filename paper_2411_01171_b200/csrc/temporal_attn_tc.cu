@@ -197,6 +197,24 @@ __device__ __forceinline__ void pack_cols(uint32_t src, uint32_t dst) {
   tst_wait();
 }
 
+// -DTA_TRACE (tuning builds only): SM-clock stamps of CTA 0's pipeline events per role
+// (0 MMA warp, 1 warp 2 = half 0, 2 warp 6 = half 1); read with sf_debug_ta_trace
+#ifdef TA_TRACE
+__device__ unsigned long long g_ta_trace[3][1024];
+__device__ unsigned int g_ta_n[3];
+#define TA_TR(role, code)                                                                       \
+  do {                                                                                          \
+    if (blockIdx.x == 0 && lane == 0) {                                                         \
+      const unsigned i_ = g_ta_n[role]++;                                                       \
+      if (i_ < 1024) g_ta_trace[role][i_] = ((unsigned long long)clock64() << 8) | (code);      \
+    }                                                                                           \
+  } while (0)
+#else
+#define TA_TR(role, code) \
+  do {                    \
+  } while (0)
+#endif
+
 template <int NCH>
 __global__ void __launch_bounds__(THREADS, 1)
     tattn_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap mX,
@@ -327,17 +345,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int64_t t = t0; t < p.n_tiles; t += dt, ++it) {
       const uint32_t ph = it & 1;
       mbar_wait(x_full, ph);
+      TA_TR(0, 1);
       fence_after();
       // A = x Mqk.  Half 0 ([0, C/2)) overlaps only operands the in-order pipe has consumed,
       // so it runs under the previous tile's epilogue; half 1 overlaps that tile's Y half 0
       gemm_half(L::A32, -1, 0);
       commit_e(&a_full[0]);
+      TA_TR(0, 2);
       mbar_wait(&y_free[0], ph ^ 1);
+      TA_TR(0, 3);
       fence_after();
       gemm_half(L::A32, -1, 1);
       commit_e(&a_full[1]);
+      TA_TR(0, 4);
       mbar_wait(&a_st[0], ph);
       mbar_wait(&a_st[1], ph);
+      TA_TR(0, 5);
       fence_after();
 #pragma unroll 1
       for (int j = 0; j < NCH; ++j) {   // S = A x^T (x rows as the K-major B: [n = key][k = ch])
@@ -347,7 +370,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_ts(tmem + L::S, tmem + L::A16 + (j * 4 + k) * 8, bd + 2 * k, idesc(128), (j | k) != 0);
       }
       commit_e(s_full);
+      TA_TR(0, 6);
       mbar_wait(p_full, ph);
+      TA_TR(0, 7);
       fence_after();
       // B = P x: 16 keys per step, x MN-major, in two N pieces on swizzle-atom boundaries.
       // The high piece [NLO, C) holds all of column half 1 and goes first: half 1 is packed
@@ -364,13 +389,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       commit_e(x_empty);
       commit_e(&b_full[0]);
       if (C < 256) commit_e(&b_full[1]);
+      TA_TR(0, 9);
       mbar_wait(&b_st[0], ph);
       mbar_wait(&b_st[1], ph);
+      TA_TR(0, 10);
       fence_after();
       gemm_half(L::Y, L::B16, 0);   // Y = B Mvo, output half 0 ...
       commit_e(&y_full[0]);
+      TA_TR(0, 11);
       gemm_half(L::Y, L::B16, 1);   // ... and half 1
       commit_e(&y_full[1]);
+      TA_TR(0, 12);
     }
   } else {
     // ---------------- packing / softmax / epilogue: tile row r, column half g ----------------
@@ -394,9 +423,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t ph = it & 1;
       const int z = (int)(t / p.n_pg), i0 = (int)(t % p.n_pg) * p.bi;
       // my half of A -> bf16 operand
+      const int role = (warp == 2) ? 1 : (warp == 6) ? 2 : -1;
+#define TA_TRW(code) do { if (role > 0) TA_TR(role, code); } while (0)
       mbar_wait(&a_full[g], ph);
+      TA_TRW(20);
       fence_after();
       pack_cols<HALF>(trow + L::A32 + g * HALF, trow + L::A16 + g * (HALF / 2));
+      TA_TRW(21);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_st[g]);
@@ -404,6 +437,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // keys of the row: row max exchanged through shared memory, the unnormalised P packed over
       // S, 1/sum applied to Y in the epilogue (it commutes with (P x) Mvo)
       mbar_wait(s_full, ph);
+      TA_TRW(22);
       fence_after();
       uint32_t sv[64];
       tld32(trow + L::S + 64 * g, sv);
@@ -415,6 +449,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if ((kmask[e >> 5] >> (e & 31)) & 1u) m = fmaxf(m, __uint_as_float(sv[e]));
       red[g * 128 + r] = m;
       asm volatile("bar.sync 1, 256;" ::: "memory");   // both halves' S read, maxima published
+      TA_TRW(23);
       m = fmaxf(m, red[(g ^ 1) * 128 + r]);
       float sum = 0.f;
       uint32_t pk[32];
@@ -431,14 +466,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      TA_TRW(24);
       asm volatile("bar.sync 1, 256;" ::: "memory");   // maxima consumed before the sums reuse red
       red[g * 128 + r] = sum;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       const float inv = live ? 1.f / (sum + red[(g ^ 1) * 128 + r]) : 0.f;
+      TA_TRW(25);
       // my half of B -> bf16 operand
       mbar_wait(&b_full[g], ph);
+      TA_TRW(26);
       fence_after();
       pack_cols<HALF>(trow + L::B32 + g * HALF, trow + L::B16 + g * (HALF / 2));
+      TA_TRW(27);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&b_st[g]);
@@ -447,19 +486,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = live && i < p.n_inner;
       const int64_t o = (int64_t)z * p.T + fr;
       bf16* dst = valid ? row_ptr<bf16>(p.out, o, i) + g * HALF : nullptr;
-      uint4 rr[HALF / 8];
+      // residual: the first two 32-column chunks prefetched while Y = B Mvo runs, then two
+      // chunks ahead (a whole half row in registers spilled the packing loops)
+      constexpr int NCC = HALF / 32;
+      uint4 rr[2][4];
       const bool has_res = valid && p.res.ptr;
-      if (has_res) {
-        const uint4* rs = reinterpret_cast<const uint4*>(row_ptr<const bf16>(p.res, o, i) + g * HALF);
+      const uint4* rs = has_res ? reinterpret_cast<const uint4*>(row_ptr<const bf16>(p.res, o, i) + g * HALF) : nullptr;
 #pragma unroll
-        for (int u = 0; u < HALF / 8; ++u) rr[u] = __ldg(rs + u);
-      }
+      for (int c = 0; c < 2 && c < NCC; ++c)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rr[c][u] = has_res ? __ldg(rs + 4 * c + u) : make_uint4(0, 0, 0, 0);
+      TA_TRW(28);
       mbar_wait(&y_full[g], ph);
+      TA_TRW(29);
       fence_after();
 #pragma unroll
-      for (int cc = 0; cc < HALF; cc += 32) {
+      for (int c = 0; c < NCC; ++c) {
         uint32_t y[32];
-        tld32(trow + L::Y + g * HALF + cc, y);
+        tld32(trow + L::Y + g * HALF + 32 * c, y);
         tld_wait();
         if (valid) {
           float v[32];
@@ -469,18 +513,23 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               float f[8];
-              unpack8(*reinterpret_cast<const bf16x8*>(&rr[cc / 8 + u]), f);
+              unpack8(*reinterpret_cast<const bf16x8*>(&rr[c & 1][u]), f);
 #pragma unroll
               for (int e = 0; e < 8; ++e) v[8 * u + e] += f[e];
             }
+            if (c + 2 < NCC) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) rr[c & 1][u] = __ldg(rs + 4 * (c + 2) + u);
+            }
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) reinterpret_cast<bf16x8*>(dst + cc)[u] = pack8(v + 8 * u);
+          for (int u = 0; u < 4; ++u) reinterpret_cast<bf16x8*>(dst + 32 * c)[u] = pack8(v + 8 * u);
         }
       }
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&y_free[g]);
+      TA_TRW(30);
       // both halves done with this tile's Y and sums before either packs the next tile's A
       // into columns that overlap the other half's Y
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -555,6 +604,17 @@ static sf_status launch(const Params& p, const sf_view_t& x, const void* w, cuda
 }
 
 }  // namespace ta
+
+#ifdef TA_TRACE
+extern "C" int32_t sf_debug_ta_trace(unsigned long long* host, uint32_t* counts) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(counts, ta::g_ta_n, sizeof(unsigned) * 3);
+  cudaMemcpyFromSymbol(host, ta::g_ta_trace, sizeof(unsigned long long) * 3 * 1024);
+  const unsigned zero[3] = {0, 0, 0};
+  cudaMemcpyToSymbol(ta::g_ta_n, zero, sizeof(zero));
+  return 0;
+}
+#endif
 
 extern "C" int32_t sf_temporal_attention_fused_supported(int32_t T, int32_t C) {
   return T >= 1 && T <= 128 && C >= 128 && C <= 320 && C % 64 == 0;
