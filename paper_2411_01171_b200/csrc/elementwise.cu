@@ -1316,10 +1316,17 @@ sf_status sf_softmax_rows(const float* s, int64_t lds, void* p, int64_t ldp, int
   return launch_status("sf_softmax_rows");
 }
 
+bool temporal_core_tc_supported(int T, int C, int koff, int voff, sf_view_t qkv, sf_view_t out);
+sf_status temporal_core_tc_launch(sf_view_t qkv, int koff, int voff, sf_view_t out, int B, int T, int n_inner, int C,
+                                  float scale, cudaStream_t st);
+
 sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, sf_view_t out, int32_t B, int32_t T,
                                      int32_t n_inner, int32_t C, float scale, void* stream) {
-  SF_CHECK_ARG(T >= 1 && T <= TA_MAXT, SF_ERR_SHAPE, "temporal attention supports 1 <= T <= 64");
   SF_CHECK_ARG(B >= 1 && n_inner >= 1 && C >= 1, SF_ERR_SHAPE, "bad extents");
+  // 32 < T <= 128: tcgen05 tiles of floor(128 / T) pixels (csrc/temporal_attn_tc.cu)
+  if (temporal_core_tc_supported(T, C, koff, voff, qkv, out))
+    return temporal_core_tc_launch(qkv, koff, voff, out, B, T, n_inner, C, scale, (cudaStream_t)stream);
+  SF_CHECK_ARG(T >= 1 && T <= TA_MAXT, SF_ERR_SHAPE, "temporal attention supports 1 <= T <= 64 (128 on tcgen05)");
   if (T <= 32 && C % 8 == 0 && koff % 8 == 0 && voff % 8 == 0 && view_vec8_ok(qkv) && out.ld % 2 == 0) {
     const int smem = TQ_WARPS * 3 * 32 * TQ_LD * 2;
     static bool init = false;

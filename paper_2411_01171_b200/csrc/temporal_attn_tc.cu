@@ -605,6 +605,320 @@ static sf_status launch(const Params& p, const sf_view_t& x, const void* w, cuda
 
 }  // namespace ta
 
+// ---------------------------------------------------------------------------------------------
+// Temporal attention CORE on tcgen05 for long clips (32 < T <= 128: BASELINE C4's T = 64 at the
+// C >= 640 levels, where the fused kernel's x tile and accumulator do not fit): q | k | v rows
+// already projected (the QKV GEMM), out = softmax(q k^T * scale) v per pixel over its T frames.
+// Same tiles as the fused kernel (bi = floor(128 / T) pixels x T frames per 128 rows, block-
+// diagonal mask), HBM-bound: q, k and v stream through a ring of 64-channel chunks (4-D TMA
+// boxes of the qkv view), S = sum_c Q_c K_c^T accumulates in TMEM [0, 128), the unnormalised P is
+// packed over S, and O = P V_j is produced one 64-channel chunk at a time (V read MN-major) into a
+// 4-deep ring of TMEM buffers that the epilogue warps drain (1/rowsum applied there) while the
+// next chunks multiply.  Warps: 0 TMA, 1 MMA, 2..5 softmax, 6..9 epilogue (one tile row each).
+// ---------------------------------------------------------------------------------------------
+namespace tcore {
+
+constexpr int THREADS = 320, CHUNK = 128 * 128, NSLOT = 12, NOB = 4;
+constexpr int SLOT_OFF = 0, BAR_OFF = NSLOT * CHUNK, INV_OFF = BAR_OFF + 512;
+constexpr int TOTAL = 1024 + INV_OFF + 1024;
+static_assert(TOTAL <= ta::SMEM_CAP, "shared memory budget");
+
+struct Params {
+  int T, bi, R, n_inner, n_pg, nch, koff, voff;
+  int64_t n_tiles;
+  float scale_log2;
+  sf_view_t out;
+};
+
+__global__ void __launch_bounds__(THREADS, 1) tcore_kernel(const __grid_constant__ Params p,
+                                                           const __grid_constant__ CUtensorMap mQKV) {
+  using namespace ta;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = base + SLOT_OFF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + BAR_OFF);
+  uint64_t* r_full = bars;                // [NSLOT]
+  uint64_t* r_empty = r_full + NSLOT;     // [NSLOT]
+  uint64_t* s_full = r_empty + NSLOT;     // MMA: S of the tile in TMEM
+  uint64_t* p_full = s_full + 1;          // 4 softmax warps: P packed over S
+  uint64_t* o_full = p_full + 1;          // [NOB] MMA: O chunk in buffer b
+  uint64_t* o_free = o_full + NOB;        // [NOB] 4 epilogue warps: buffer b read
+  uint64_t* inv_ready = o_free + NOB;     // [2] softmax: 1/rowsum of the tile (parity) written
+  uint64_t* inv_free = inv_ready + 2;     // [2] epilogue: ... read
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(inv_free + 2);
+  float* inv_sum = reinterpret_cast<float*>(base + INV_OFF);   // [2][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    for (int b = 0; b < NOB; ++b) {
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_free[b], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&inv_ready[b], 4);
+      mbar_init(&inv_free[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // rows R..127 of every ring slot stay zero (the TMA box has R rows)
+  for (int idx = threadIdx.x; idx < NSLOT * (128 - p.R) * 8; idx += THREADS) {
+    const int j = idx / ((128 - p.R) * 8), rem = idx % ((128 - p.R) * 8);
+    *reinterpret_cast<uint4*>(ring + j * CHUNK + (p.R + rem / 8) * 128 + (rem % 8) * 16) = make_uint4(0, 0, 0, 0);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  griddep_wait();
+
+  const int64_t t0 = blockIdx.x, dt = gridDim.x;
+  const int nch = p.nch;
+  if (warp == 0) {
+    // ---------------- TMA: Q_0 K_0 Q_1 K_1 ... then V_0 V_1 ... per tile ----------------
+    int slot = 0;
+    uint32_t ph = 0;
+    auto load = [&](int col, int i0, int z) {
+      mbar_wait(&r_empty[slot], ph ^ 1);
+      mbar_expect_tx_e(&r_full[slot], 128 * p.R);
+      tma4_e(&mQKV, &r_full[slot], ring + slot * CHUNK, col, i0, 0, z);
+      if (++slot == NSLOT) {
+        slot = 0;
+        ph ^= 1;
+      }
+    };
+    for (int64_t t = t0; t < p.n_tiles; t += dt) {
+      const int z = (int)(t / p.n_pg), i0 = (int)(t % p.n_pg) * p.bi;
+      for (int c = 0; c < nch; ++c) {
+        load(c * 64, i0, z);
+        load(p.koff + c * 64, i0, z);
+      }
+      for (int c = 0; c < nch; ++c) load(p.voff + c * 64, i0, z);
+    }
+    for (int s = 0; s < NSLOT; ++s) {   // drain: every slot released before the CTA retires
+      mbar_wait(&r_empty[slot], ph ^ 1);
+      if (++slot == NSLOT) {
+        slot = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    int slot = 0;
+    uint32_t ph = 0;
+    int ob = 0;
+    uint32_t oph = 0;
+    const uint32_t rb = smem_u32(ring);
+    auto next = [&]() {
+      if (++slot == NSLOT) {
+        slot = 0;
+        ph ^= 1;
+      }
+    };
+    uint32_t it = 0;
+    for (int64_t t = t0; t < p.n_tiles; t += dt, ++it) {
+#pragma unroll 1
+      for (int c = 0; c < nch; ++c) {     // S += Q_c K_c^T
+        const int sq = slot;
+        mbar_wait(&r_full[sq], ph);
+        next();
+        const int sk = slot;
+        mbar_wait(&r_full[sk], ph);
+        fence_after();
+        const uint64_t ad = kdesc(rb + sq * CHUNK), bd = kdesc(rb + sk * CHUNK);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mma_ss(tmem, ad + 2 * k, bd + 2 * k, idesc(128), (c | k) != 0);
+        commit_e(&r_empty[sq]);
+        commit_e(&r_empty[sk]);
+        next();
+      }
+      commit_e(s_full);
+      mbar_wait(p_full, it & 1);
+      fence_after();
+#pragma unroll 1
+      for (int c = 0; c < nch; ++c) {     // O_c = P V_c into TMEM buffer ob
+        mbar_wait(&r_full[slot], ph);
+        mbar_wait(&o_free[ob], oph ^ 1);
+        fence_after();
+        const uint32_t vb = rb + slot * CHUNK;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mma_ts(tmem + 128 + ob * 64, tmem + k * 8, mndesc(vb + k * 2048), idesc(64, true), k != 0);
+        commit_e(&r_empty[slot]);
+        commit_e(&o_full[ob]);
+        next();
+        if (++ob == NOB) {
+          ob = 0;
+          oph ^= 1;
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- softmax (one tile row per thread) ----------------
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int pix = r % p.bi;
+    const bool live = r < p.R;
+    uint32_t kmask[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      kmask[w] = 0u;
+      for (int e = 0; e < 32; ++e) {
+        const int c = 32 * w + e;
+        if (live && c < p.R && c % p.bi == pix) kmask[w] |= 1u << e;
+      }
+    }
+    const float sl = p.scale_log2;
+    uint32_t it = 0;
+    for (int64_t t = t0; t < p.n_tiles; t += dt, ++it) {
+      mbar_wait(s_full, it & 1);
+      fence_after();
+      float m = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t sv[32];
+        tld32(trow + 32 * k, sv);
+        tld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if ((kmask[k] >> e) & 1u) m = fmaxf(m, __uint_as_float(sv[e]));
+      }
+      m *= sl;
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t sv[32], pk[16];
+        tld32(trow + 32 * k, sv);
+        tld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float x = ((kmask[k] >> e) & 1u) ? ex2(fmaf(__uint_as_float(sv[e]), sl, -m)) : 0.f;
+          sv[e] = __float_as_uint(x);
+          sum += x;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = pack2(sv[2 * e], sv[2 * e + 1]);
+        tst16(trow + 16 * k, pk);   // packed chunk k lands on columns already read
+      }
+      tst_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      const int ib = it & 1;
+      mbar_wait(&inv_free[ib], ((it >> 1) & 1) ^ 1);
+      inv_sum[ib * 128 + r] = live ? 1.f / sum : 0.f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&inv_ready[ib]);
+    }
+  } else {
+    // ---------------- epilogue: O chunks (1/rowsum) -> out rows ----------------
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int pix = r % p.bi, fr = r / p.bi;
+    const bool live = r < p.R;
+    int ob = 0;
+    uint32_t oph = 0;
+    uint32_t it = 0;
+    for (int64_t t = t0; t < p.n_tiles; t += dt, ++it) {
+      const int z = (int)(t / p.n_pg), i0 = (int)(t % p.n_pg) * p.bi;
+      const int i = i0 + pix;
+      const bool valid = live && i < p.n_inner;
+      bf16* dst = valid ? row_ptr<bf16>(p.out, (int64_t)z * p.T + fr, i) : nullptr;
+      const int ib = it & 1;
+      mbar_wait(&inv_ready[ib], (it >> 1) & 1);
+      const float inv = inv_sum[ib * 128 + r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&inv_free[ib]);
+#pragma unroll 1
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&o_full[ob], oph);
+        fence_after();
+        uint32_t a[32], b2[32];
+        tld32(trow + 128 + ob * 64, a);
+        tld32(trow + 128 + ob * 64 + 32, b2);
+        tld_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_free[ob]);
+        if (valid) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(a[8 * u + e]) * inv;
+            reinterpret_cast<bf16x8*>(dst + c * 64)[u] = pack8(v);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(b2[8 * u + e]) * inv;
+            reinterpret_cast<bf16x8*>(dst + c * 64)[4 + u] = pack8(v);
+          }
+        }
+        if (++ob == NOB) {
+          ob = 0;
+          oph ^= 1;
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+}  // namespace tcore
+
+
+// internal entry points of sf_temporal_attention_core (elementwise.cu); C linkage, not in the header
+extern "C" __attribute__((visibility("hidden"))) bool temporal_core_tc_supported(int T, int C, int koff, int voff, sf_view_t qkv, sf_view_t out) {
+  return T > 32 && T <= 128 && C % 64 == 0 && koff % 64 == 0 && voff % 64 == 0 && aligned16(qkv.ptr) &&
+         qkv.ld % 8 == 0 && view_vec8_ok(out);
+}
+
+extern "C" __attribute__((visibility("hidden"))) sf_status temporal_core_tc_launch(
+    sf_view_t qkv, int koff, int voff, sf_view_t out, int B, int T, int n_inner, int C, float scale, cudaStream_t st) {
+  tcore::Params p{};
+  p.T = T;
+  p.bi = 128 / T;
+  p.R = p.bi * T;
+  p.n_inner = n_inner;
+  p.n_pg = (n_inner + p.bi - 1) / p.bi;
+  p.n_tiles = (int64_t)B * p.n_pg;
+  p.nch = C / 64;
+  p.koff = koff;
+  p.voff = voff;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  const uint64_t es = 2, ost = (uint64_t)(qkv.ostride ? qkv.ostride : n_inner);
+  CUtensorMap m;
+  uint64_t dims[4] = {(uint64_t)(voff + C), (uint64_t)n_inner, (uint64_t)T, (uint64_t)B};
+  uint64_t str[3] = {(uint64_t)qkv.ld * es, ost * qkv.ld * es, (uint64_t)T * ost * qkv.ld * es};
+  uint32_t box[4] = {64, (uint32_t)p.bi, (uint32_t)T, 1};
+  SF_CHECK_ARG(ta::encode(&m, qkv.ptr, 4, dims, str, box), SF_ERR_CUDA, "tensor map qkv (temporal core)");
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(tcore::tcore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tcore::TOTAL);
+    init = true;
+  }
+  const int64_t grid = p.n_tiles < num_sms() ? p.n_tiles : num_sms();
+  launch_k(tcore::tcore_kernel, dim3((unsigned)grid), dim3(tcore::THREADS), tcore::TOTAL, st, p, m);
+  return launch_status("sf_temporal_attention_core(tcgen05)");
+}
+
 #ifdef TA_TRACE
 extern "C" int32_t sf_debug_ta_trace(unsigned long long* host, uint32_t* counts) {
   cudaDeviceSynchronize();

@@ -217,7 +217,10 @@ def test_flash_core(Fr, HW, C):
                                      # one warp per pixel (many pixels) and the channel-split block per
                                      # pixel (few pixels: C3 L2 / L3, uneven chunk counts, B = 2)
                                      (1, 25, 2400, 320), (1, 25, 576, 1280), (1, 25, 144, 1280),
-                                     (1, 25, 200, 192), (2, 25, 300, 320)])
+                                     (1, 25, 200, 192), (2, 25, 300, 320),
+                                     # 32 < T <= 128: the tcgen05 core (BASELINE C4: T = 64 at C = 640 / 1280)
+                                     (1, 64, 300, 640), (2, 64, 77, 1280), (1, 48, 90, 320), (1, 100, 9, 128),
+                                     (1, 128, 5, 64), (1, 64, 2304, 640)])
 def test_temporal_core(B, T, P, C):
     """Per-pixel attention over T frames vs torch (rows o = b*T+t, i = pixel)."""
     torch.manual_seed(5)
