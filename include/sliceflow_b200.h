@@ -160,7 +160,8 @@ sf_status sf_spatial_attention_core(sf_view_t q, sf_view_t k, const void* vt, sf
                                     int32_t HW, int32_t C, float scale, void* stream);
 /* Temporal attention core per pixel: q|k|v rows (o = b*T+t, i = pixel), q at
  * column 0, k at qkv_koff, v at qkv_voff of view qkv; writes softmax(q k^T *
- * scale) v into out.  T <= 64. */
+ * scale) v into out.  T <= 32: mma.sync; 32 < T <= 128 with C, koff, voff
+ * multiples of 64: tcgen05; otherwise SIMT (T <= 64). */
 sf_status sf_temporal_attention_core(sf_view_t qkv, int32_t koff, int32_t voff, sf_view_t out, int32_t B,
                                      int32_t T, int32_t n_inner, int32_t C, float scale, void* stream);
 /* Whole temporal attention op, fused (tcgen05/TMEM; replaces the QKV projection, the core and
