@@ -228,43 +228,60 @@ def slice_summary(plan) -> dict:
 def north_star_plan(args, cfg, den, sched, x0) -> dict:
     """The north star's slice plan: one frame per spatial slice and T pixel bands per temporal
     group (a band of HW/T pixels x all T frames = one frame's worth of rows), same weights and
-    schedule.  Reports its throughput and peak HBM next to the headline plan's."""
+    schedule.  Reports its throughput and peak HBM next to the headline plan's: the first of
+    ``--ns-streams`` (fewest slice streams = lowest peak) as the line's numbers, the others as
+    ``variants`` (more streams overlap the small slices: faster, one scratch copy each)."""
+    import gc
+
     import torch
     from paper_2411_01171_b200.executor import ExecConfig
     from paper_2411_01171_b200.harness import Denoiser
     dw = den.model.dw
     bt = cfg.frames * cfg.effective_batch
-    ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=bt, temporal_k=bt, slice_streams=args.ns_streams)
     # drop the headline plan's buffers (weights are shared) before measuring this plan's peak
-    import gc
     den._graphs.clear()
     den.plan = den.model.plan = None
-    gc.collect()
-    torch.cuda.empty_cache()
-    torch.cuda.reset_peak_memory_stats()
-    d2 = Denoiser(cfg, ecfg, device_weights=dw)
-    key = d2.prepare(sched)
-    d2.set_latent(x0)
-    x0_rows = d2.plan.latent.clone()
-    for _ in range(2):
-        d2.plan.latent.copy_(x0_rows)
-        d2.launch(key)
-    torch.cuda.synchronize()
-    n = max(2, min(args.steps, 5))
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st.record()
-    for _ in range(n):
-        d2.plan.latent.copy_(x0_rows)
-        d2.launch(key)
-    en.record()
-    torch.cuda.synchronize()
-    ms = st.elapsed_time(en) / n
-    return {"plan": f"spatial k = {bt} (one frame per slice), temporal k = {bt} pixel bands, "
-                    f"{args.ns_streams} slice stream(s)",
-            "value": round(cfg.steps / (ms / 1e3), 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
-            "runs": n, "peak_hbm_bytes": int(torch.cuda.max_memory_allocated()),
-            "arena_bytes": d2.plan.arena_bytes, "scratch_bytes": d2.plan.scratch_bytes,
-            "slices": slice_summary(d2.plan), "gpu_launches_per_run": d2.launches[key]}
+    out = None
+    for streams in args.ns_streams:
+        gc.collect()
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+        ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=bt, temporal_k=bt, slice_streams=streams)
+        d2 = Denoiser(cfg, ecfg, device_weights=dw)
+        key = d2.prepare(sched)
+        d2.set_latent(x0)
+        x0_rows = d2.plan.latent.clone()
+        for _ in range(2):
+            d2.plan.latent.copy_(x0_rows)
+            d2.launch(key)
+        torch.cuda.synchronize()
+        n = max(2, min(args.steps, 5))
+        if os.environ.get("SF_BENCH_MEMDUMP") == "1":   # diagnostics: the live allocations behind the peak
+            blocks = sorted((b["size"] for seg in torch.cuda.memory_snapshot() for b in seg["blocks"]
+                             if b["state"] == "active_allocated"), reverse=True)
+            print("north-star plan live blocks (MB):", [round(b / 1e6, 1) for b in blocks[:16]],
+                  "total", round(sum(blocks) / 1e6, 1), "peak", round(torch.cuda.max_memory_allocated() / 1e6, 1),
+                  file=sys.stderr)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for _ in range(n):
+            d2.plan.latent.copy_(x0_rows)
+            d2.launch(key)
+        en.record()
+        torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / n
+        rec = {"plan": f"spatial k = {bt} (one frame per slice), temporal k = {bt} pixel bands, "
+                       f"{streams} slice stream(s)",
+               "value": round(cfg.steps / (ms / 1e3), 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
+               "runs": n, "peak_hbm_bytes": int(torch.cuda.max_memory_allocated()),
+               "arena_bytes": d2.plan.arena_bytes, "scratch_bytes": d2.plan.scratch_bytes}
+        if out is None:
+            out = dict(rec, slices=slice_summary(d2.plan), gpu_launches_per_run=d2.launches[key], variants=[])
+        else:
+            out["variants"].append({k: rec[k] for k in ("plan", "value", "ms_per_step", "peak_hbm_bytes",
+                                                          "scratch_bytes")})
+        del d2
+    return out
 
 
 def run_plan_only(args, world, rank):
@@ -488,7 +505,9 @@ def main():
     ap.add_argument("--plan-only", action="store_true", help="per-rank device memory plan, no GPU needed")
     ap.add_argument("--slice-streams", type=int, default=1, help="headline plan: streams per sliced group")
     ap.add_argument("--ln-fold", action="store_true", help="fold the LayerNorm before temporal attention into its QKV GEMM")
-    ap.add_argument("--ns-streams", type=int, default=4, help="north-star plan: streams per sliced group")
+    ap.add_argument("--ns-streams", type=int, nargs="+", default=[2, 4],
+                    help="north-star plan: slice streams per sliced group; the first is the reported plan, "
+                         "the rest are listed as variants")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args.gpus)

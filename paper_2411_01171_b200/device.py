@@ -69,6 +69,21 @@ def f32(a: np.ndarray, dev) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).contiguous()
 
 
+def attention_weights(prm, dev) -> dict:
+    """[wq^T; wk^T; wv^T] and wo^T (bf16) for the projection GEMMs (the reference right-multiplies,
+    kernels.py:285-291)."""
+    qkv = np.concatenate([np.asarray(prm[n]).T for n in ("wq", "wk", "wv")], axis=0)
+    return {"wqkv": bf16(qkv, dev), "wo": bf16(np.asarray(prm["wo"]).T, dev)}
+
+
+def unfused_weights(prm: dict, dev) -> dict:
+    """Make sure a temporal attention's three-launch weights exist (built at plan compile time,
+    never during graph capture); returns ``prm``."""
+    if "wqkv" not in prm:
+        prm.update(attention_weights(prm["host"], dev))
+    return prm
+
+
 def temporal_fused_weights(wq, wk, wv, wo, dev) -> torch.Tensor:
     """[Mqk^T ; Mvo^T] (bf16 [2C][C], K-major B operands) for sf_temporal_attention_fused:
     Mqk = Wq Wk^T log2(e)/sqrt(C) and Mvo = Wv Wo in fp64 (kernels.py:285-292 right-multiplies:
@@ -120,12 +135,13 @@ class DeviceWeights:
         if k in (OpKind.GROUP_NORM, OpKind.LAYER_NORM):
             return {"gamma": f32(prm["gamma"], d), "beta": f32(prm["beta"], d)}
         if k in (OpKind.SPATIAL_ATTENTION, OpKind.TEMPORAL_ATTENTION):
-            qkv = np.concatenate([np.asarray(prm[n]).T for n in ("wq", "wk", "wv")], axis=0)
-            out = {"wqkv": bf16(qkv, d), "wo": bf16(np.asarray(prm["wo"]).T, d)}
-            C = qkv.shape[1]
+            C = np.asarray(prm["wq"]).shape[0]
             if k is OpKind.TEMPORAL_ATTENTION and C % 64 == 0 and C <= 320:
-                out["wfused"] = temporal_fused_weights(prm["wq"], prm["wk"], prm["wv"], prm["wo"], d)
-            return out
+                # one fused launch (sf_temporal_attention_fused): the projection weights of the
+                # three-launch path are uploaded only if a plan needs it (unfused_weights)
+                return {"wfused": temporal_fused_weights(prm["wq"], prm["wk"], prm["wv"], prm["wo"], d),
+                        "host": {n: np.asarray(prm[n]) for n in ("wq", "wk", "wv", "wo")}}
+            return attention_weights(prm, d)
         raise InvalidParam(f"no device layout for {k}")
 
 
@@ -276,8 +292,8 @@ def use_flash(HW, C) -> bool:
 def spatial_attention_scratch(rows, HW, C) -> dict:
     """Slice scratch the spatial attention lowering needs: {name: (rows, cols, dtype)}."""
     flash = HW > SMALL_SEQ and use_flash(HW, C)
-    # the fused core reads q|k from a 2C-wide buffer and V^T from its own (spatial_attention)
-    out = {"qkv": (rows, (2 if flash else 3) * C, torch.bfloat16), "o": (rows, C, torch.bfloat16)}
+    # above SMALL_SEQ tokens q|k live in a 2C-wide buffer and V^T in its own (spatial_attention)
+    out = {"qkv": (rows, (2 if HW > SMALL_SEQ else 3) * C, torch.bfloat16), "o": (rows, C, torch.bfloat16)}
     frames = rows // HW
     if HW > SMALL_SEQ:
         out["vt"] = (frames * C, HW, torch.bfloat16)
@@ -291,9 +307,10 @@ def _spatial_core_materialized(stream, frames, HW, C, scratch, backend):
     qkv, s, p, o = scratch["qkv"], scratch["s"], scratch["p"], scratch["o"]
     if HW % 8:
         raise ShapeMismatch(f"spatial attention over {HW} tokens needs a multiple of 8 above {SMALL_SEQ}")
+    ld = qkv.stride(0)   # q | k (2C wide)
     gemm(stream, mode=N.GEMM_PLAIN, n_outer=1, n_inner=HW, cin=C, n=HW, a=Rows(qkv, 0, 0),
-         w=qkv, w_ptr=qkv.data_ptr() + C * qkv.element_size(), w_ld=3 * C, w_kmajor=True,
-         out=Rows(s, 0, 0), out_fp32=True, batch=frames, a_bstride=HW * 3 * C, w_bstride=HW * 3 * C,
+         w=qkv, w_ptr=qkv.data_ptr() + C * qkv.element_size(), w_ld=ld, w_kmajor=True,
+         out=Rows(s, 0, 0), out_fp32=True, batch=frames, a_bstride=HW * ld, w_bstride=HW * ld,
          out_bstride=HW * HW, alpha=1.0 / math.sqrt(C), backend=backend)
     N.call("sf_softmax_rows", s.data_ptr(), HW, p.data_ptr(), HW, frames * HW, HW, stream)
     vt = scratch["vt"]
@@ -336,6 +353,7 @@ def temporal_attention(stream, x: Rows, y: Rows, B, T, n_inner, C, prm, epi: Epi
         return
     qkv, o = scratch["qkv"], scratch["o"]
     bt = B * T
+    unfused_weights(prm, y.t.device)
     if fold is None:
         gemm(stream, mode=N.GEMM_PLAIN, n_outer=bt, n_inner=n_inner, cin=C, n=3 * C, a=x, w=prm["wqkv"],
              out=Rows(qkv, 0, n_inner), backend=backend)

@@ -822,6 +822,7 @@ class Plan:
                 pt = self.dw.p[nxt.id]
                 if "fold" not in pt:
                     pl = self.dw.p[o.id]
+                    D.unfused_weights(pt, self.dev)
                     pt["fold"] = D.ln_fold_weights(pt["wqkv"], pl["gamma"], pl["beta"])
                 pp_specs["lnstats"] = (B * T, 2, torch.float32)
                 i += 1
@@ -844,6 +845,7 @@ class Plan:
                 if fuse_act or emb_epi or not D.fused_temporal_ok(self.dw.p[o.id], T, self.shapes[o.id].c,
                                                                   backend=backend, fold=fold_ln.get(o.id)):
                     # three launches (QKV GEMM, core, output GEMM) through slice scratch
+                    D.unfused_weights(self.dw.p[o.id], self.dev)
                     pp_specs["qkv"] = (B * T, 3 * C, torch.bfloat16)
                     pp_specs["o"] = (B * T, C, torch.bfloat16)
             i += 2 if fuse_act else 1
