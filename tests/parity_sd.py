@@ -42,6 +42,9 @@ CONFIGS = {
     "c2": dict(channels=4, frames=16, height=64, width=64, base_channels=320, norm_groups=32, steps=25),
     "c3": dict(channels=4, frames=25, height=72, width=128, base_channels=320, norm_groups=32, steps=25),
     "wide": dict(channels=4, frames=4, height=16, width=16, base_channels=64, norm_groups=32, steps=10),
+    # long clip (BASELINE C4's T = 64) on a small plane: the fused temporal attention with 2 pixels
+    # per tile at L0 and the tcgen05 temporal core at C = 640 / 1280
+    "long": dict(channels=4, frames=64, height=32, width=32, base_channels=320, norm_groups=32, steps=25),
 }
 
 

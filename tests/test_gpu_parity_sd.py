@@ -1,4 +1,4 @@
-"""Parity at BASELINE configs 2 and 3 (SD widths, base 320) against the fp64 oracle.  -m gpu.
+"""Parity at BASELINE configs 2 and 3 (SD widths, base 320) and a 64-frame clip (C4's T) against the fp64 oracle.  -m gpu.
 
 The oracle is ``oracle/torch_ref.py`` (torch fp64 on the same B200, pinned to the
 reference's fp64 goldens at <= 1e-12 by tests/test_oracle_golden.py).  Gates, for
@@ -35,7 +35,7 @@ from paper_2411_01171_b200.build import build  # noqa: E402
 build()
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "long"])
 def test_sd_width_parity(name):
     r = run(name)
     print({k: v for k, v in r.items() if k not in ("S_dev", "S_ref")})
