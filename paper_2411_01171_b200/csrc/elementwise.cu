@@ -24,14 +24,19 @@ void set_error(const std::string& m) { g_err = m; }
 static int gn_splits(int frames, int n_inner) {
   // ~2 CTAs per SM: each partial is a full (C) row of fp64 sums the finalize
   // pass has to walk, so long CTAs beat many light ones (measured on B200)
-  int want = (2 * num_sms() + frames - 1) / frames;
-  int most = (n_inner + 63) / 64;                        // >= 64 rows per CTA
+  static const int per_sm = getenv("SF_GN_CTAS") ? atoi(getenv("SF_GN_CTAS")) : 2;        // tuning knobs
+  static const int min_rows = getenv("SF_GN_MINROWS") ? atoi(getenv("SF_GN_MINROWS")) : 64;
+  int want = (per_sm * num_sms() + frames - 1) / frames;
+  int most = (n_inner + min_rows - 1) / min_rows;        // >= min_rows rows per CTA
   int s = want < most ? want : most;
   return s < 1 ? 1 : s;
 }
 
 // partial[frame][split][c] = (sum x, sum x^2) over the split's rows, fp64
-constexpr int GN_U = 8;
+#ifndef GN_UNROLL
+#define GN_UNROLL 8   // 16-byte loads in flight per thread (tuning: -DGN_UNROLL=n)
+#endif
+constexpr int GN_U = GN_UNROLL;
 __global__ void __launch_bounds__(256, 4) gn_partial_kernel(sf_view_t x, int n_inner, int C, int splits,
                                                             double2* partial) {
   griddep_wait();
