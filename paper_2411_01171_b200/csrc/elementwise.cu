@@ -189,6 +189,96 @@ static void launch_gn_finalize(const T* partial, int frames, int splits, int C, 
            groups, gpb, count, eps, mean, rstd);
 }
 
+// Small planes (deep levels, n_inner <= GN_DIRECT_MAX_ROWS): ONE launch, one block per (frame,
+// run of gpb whole groups = W channels): 8-channel vectors x rows_per_iter row lanes read the
+// block's rows (GN_U loads in flight), fp32 per thread -> fp64 per channel in shared memory ->
+// fp64 per group -> mean / rstd.  Fixed order: bitwise reproducible.  (The split + finalize pair
+// costs two dependent launches over 9-37 MB here: 17-27 us at 0.5-1.4 TB/s.)
+constexpr int GN_DIRECT_MAX_ROWS = 1024;
+__global__ void __launch_bounds__(256) gn_stats_direct_kernel(sf_view_t x, int n_inner, int C, int groups, int gpb,
+                                                              float eps, float* mean, float* rstd) {
+  griddep_wait();
+  extern __shared__ double2 red[];   // [rows_per_iter][W], then [W] channel totals in row 0
+  const int cg = C / groups, W = gpb * cg, nv = W / 8;
+  const int frame = blockIdx.y, g0 = blockIdx.x * gpb, c0 = g0 * cg;
+  const int rpi = (int)blockDim.x / nv;
+  const int v = threadIdx.x % nv, lr = threadIdx.x / nv;
+  if (lr < rpi) {
+    float s[8], q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] = q[j] = 0.f;
+    const bf16* base = row_ptr<const bf16>(x, frame, 0) + c0 + v * 8;
+    int r = lr;
+    for (; r + (GN_U - 1) * rpi < n_inner; r += GN_U * rpi) {
+      bf16x8 in[GN_U];
+#pragma unroll
+      for (int u = 0; u < GN_U; ++u) in[u] = *reinterpret_cast<const bf16x8*>(base + (int64_t)(r + u * rpi) * x.ld);
+#pragma unroll
+      for (int u = 0; u < GN_U; ++u) {
+        float f[8];
+        unpack8(in[u], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s[j] += f[j];
+          q[j] += f[j] * f[j];
+        }
+      }
+    }
+    for (; r < n_inner; r += rpi) {
+      float f[8];
+      unpack8(*reinterpret_cast<const bf16x8*>(base + (int64_t)r * x.ld), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s[j] += f[j];
+        q[j] += f[j] * f[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[lr * W + v * 8 + j] = make_double2((double)s[j], (double)q[j]);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    double ss = 0, qq = 0;
+    for (int rr = 0; rr < rpi; ++rr) {
+      const double2 t = red[rr * W + c];
+      ss += t.x;
+      qq += t.y;
+    }
+    red[c] = make_double2(ss, qq);   // row 0 is only read by this thread above
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ng = min(gpb, groups - g0);
+  const double count = (double)n_inner * cg;
+  for (int gi = warp; gi < ng; gi += blockDim.x >> 5) {
+    double ss = 0, qq = 0;
+    for (int c = lane; c < cg; c += 32) {
+      ss += red[gi * cg + c].x;
+      qq += red[gi * cg + c].y;
+    }
+    ss = warp_sum_d(ss);
+    qq = warp_sum_d(qq);
+    if (lane == 0) {
+      const double mu = ss / count;
+      double var = qq / count - mu * mu;
+      if (var < 0) var = 0;
+      const int o = frame * groups + g0 + gi;
+      mean[o] = (float)mu;
+      rstd[o] = (float)(1.0 / sqrt(var + (double)eps));
+    }
+  }
+}
+
+// groups per block of the direct statistics kernel: about 160 channels (20 vectors x 12 row lanes)
+// and a multiple of 8 channels; 0 = not applicable
+static int gn_direct_gpb(int C, int groups, int n_inner) {
+  if (n_inner > GN_DIRECT_MAX_ROWS) return 0;
+  const int cg = C / groups;
+  for (int gpb = std::max(1, 160 / cg); gpb >= 1; --gpb)
+    if ((gpb * cg) % 8 == 0 && gpb * cg <= 256 * 8 && groups % gpb == 0) return gpb;
+  return 0;
+}
+
 // y = act((x - mean[f][g]) * (rstd[f][g] * gamma[c]) + beta[c]).  Persistent: each
 // block takes an equal contiguous share of all frames*n_inner rows (no tail wave);
 // each thread owns one 8-channel vector (mean / scale / shift in registers, reloaded
@@ -1155,6 +1245,19 @@ sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int3
   SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
   SF_CHECK_ARG(view_vec8_ok(x) && work && mean && rstd, SF_ERR_PARAM, "unaligned view or null buffer");
   cudaStream_t st = (cudaStream_t)stream;
+  static const bool direct_on = !(getenv("SF_GN_DIRECT") && getenv("SF_GN_DIRECT")[0] == '0');   // A/B knob
+  if (const int gpb = direct_on ? gn_direct_gpb(C, groups, n_inner) : 0) {
+    const int W = gpb * (C / groups), nv = W / 8, rpi = 256 / nv;
+    const size_t smem = (size_t)rpi * W * sizeof(double2);
+    static size_t set = 48 * 1024;
+    if (smem > set) {
+      cudaFuncSetAttribute(gn_stats_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set = smem;
+    }
+    launch_k(gn_stats_direct_kernel, dim3((unsigned)(groups / gpb), (unsigned)frames), dim3(rpi * nv), smem, st, x,
+             n_inner, C, groups, gpb, eps, mean, rstd);
+    return launch_status("sf_group_norm_stats");
+  }
   int splits = gn_splits(frames, n_inner);
   int nvec = C / 8;
   int threads = nvec <= 256 ? (256 / nvec) * nvec : 256;
