@@ -25,6 +25,7 @@
 #include "common.cuh"
 
 #include <cuda.h>
+#include <cstdlib>
 #include <mutex>
 
 namespace sf {
@@ -885,7 +886,8 @@ __global__ void __launch_bounds__(THREADS, 1) tcore_kernel(const __grid_constant
 
 // internal entry points of sf_temporal_attention_core (elementwise.cu); C linkage, not in the header
 extern "C" __attribute__((visibility("hidden"))) bool temporal_core_tc_supported(int T, int C, int koff, int voff, sf_view_t qkv, sf_view_t out) {
-  return T > 32 && T <= 128 && C % 64 == 0 && koff % 64 == 0 && voff % 64 == 0 && aligned16(qkv.ptr) &&
+  static const int min_t = getenv("SF_TCORE_MIN_T") ? atoi(getenv("SF_TCORE_MIN_T")) : 33;   // A/B knob
+  return T >= min_t && T <= 128 && C % 64 == 0 && koff % 64 == 0 && voff % 64 == 0 && aligned16(qkv.ptr) &&
          qkv.ld % 8 == 0 && view_vec8_ok(out);
 }
 
