@@ -36,6 +36,13 @@ from .weights import WeightBundle
 
 # kernels launched per C-ABI call (for the gpu_launches count of the bench)
 KERNELS_PER_CALL = {"sf_group_norm_stats": 2, "sf_dot3_bf16": 2, "sf_gram_bf16": 3}
+GN_DIRECT_MAX_ROWS = 1024   # elementwise.cu: planes this small get one statistics launch
+
+
+def kernels_per_call(name: str, args) -> int:
+    if name == "sf_group_norm_stats" and args[2] <= GN_DIRECT_MAX_ROWS:   # (x, frames, n_inner, ...)
+        return 1
+    return KERNELS_PER_CALL.get(name, 1)
 
 
 def alpha(s: int, K: int) -> float:
@@ -55,7 +62,7 @@ class _LaunchCounter:
         self._orig = N.call
 
         def counted(name, *a):
-            self.n += KERNELS_PER_CALL.get(name, 1)
+            self.n += kernels_per_call(name, a)
             return self._orig(name, *a)
         N.call = counted
         return self
