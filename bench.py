@@ -308,7 +308,12 @@ def run_plan_only(args, world, rank):
                           "per_rank_arena_bytes": arenas, "world1_arena_bytes": one,
                           "max_rank_fraction": max(arenas) / one,
                           "exchanges_per_eval": mine.get("exchanges_per_eval", 0),
-                          "hoisted_exchanges": mine.get("hoisted_exchanges", 0)}), flush=True)
+                          "hoisted_exchanges": mine.get("hoisted_exchanges", 0),
+                          # a model, not a measurement: the bytes a rank sends per evaluation over
+                          # NVLink 5 at 900 GB/s per direction, no overlap
+                          "exchange_bytes_per_rank_per_eval": mine.get("exchange_bytes_per_rank", 0),
+                          "exchange_ms_per_eval_at_900GBps": round(mine.get("exchange_bytes_per_rank", 0)
+                                                                   / 900e9 * 1e3, 3)}), flush=True)
 
 
 def run_ours(args, world, rank, local):

@@ -1089,6 +1089,14 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
         ex = exchange_schedule(plan)
         out["exchanges_per_eval"] = len(ex)
         out["hoisted_exchanges"] = sum(1 for op in ex if op.at < op.need)
+        # bytes this rank sends per evaluation: of each exchanged value it holds 1/world (its frames or
+        # its pixel band) and keeps the 1/world of that block which stays local
+        w = plan.cfg.world
+        sent = 0.0
+        for op in ex:
+            s = plan.shapes[op.value]
+            sent += s.b * s.t * s.h * s.w * s.c * 2 / w * (w - 1) / w
+        out["exchange_bytes_per_rank"] = int(sent)
     return out
 
 
