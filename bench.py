@@ -230,7 +230,9 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
     group (a band of HW/T pixels x all T frames = one frame's worth of rows), same weights and
     schedule.  Reports its throughput and peak HBM next to the headline plan's: the first of
     ``--ns-streams`` (fewest slice streams = lowest peak) as the line's numbers, the others as
-    ``variants`` (more streams overlap the small slices: faster, one scratch copy each)."""
+    ``variants`` (more streams overlap the small slices: faster, one scratch copy each).
+    ``equal_peak_plan``: the budget policy with that plan's scratch as the budget (same peak HBM,
+    one frame per slice only where the scratch needs it)."""
     import gc
 
     import torch
@@ -241,12 +243,11 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
     # drop the headline plan's buffers (weights are shared) before measuring this plan's peak
     den._graphs.clear()
     den.plan = den.model.plan = None
-    out = None
-    for streams in args.ns_streams:
+
+    def measure(ecfg):
         gc.collect()
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats()
-        ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=bt, temporal_k=bt, slice_streams=streams)
         d2 = Denoiser(cfg, ecfg, device_weights=dw)
         key = d2.prepare(sched)
         d2.set_latent(x0)
@@ -259,7 +260,7 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
         if os.environ.get("SF_BENCH_MEMDUMP") == "1":   # diagnostics: the live allocations behind the peak
             blocks = sorted((b["size"] for seg in torch.cuda.memory_snapshot() for b in seg["blocks"]
                              if b["state"] == "active_allocated"), reverse=True)
-            print("north-star plan live blocks (MB):", [round(b / 1e6, 1) for b in blocks[:16]],
+            print("plan live blocks (MB):", [round(b / 1e6, 1) for b in blocks[:16]],
                   "total", round(sum(blocks) / 1e6, 1), "peak", round(torch.cuda.max_memory_allocated() / 1e6, 1),
                   file=sys.stderr)
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -270,16 +271,33 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
         en.record()
         torch.cuda.synchronize()
         ms = st.elapsed_time(en) / n
-        rec = {"plan": f"spatial k = {bt} (one frame per slice), temporal k = {bt} pixel bands, "
-                       f"{streams} slice stream(s)",
-               "value": round(cfg.steps / (ms / 1e3), 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
+        rec = {"value": round(cfg.steps / (ms / 1e3), 3), "unit": "steps/s", "ms_per_step": round(ms, 3),
                "runs": n, "peak_hbm_bytes": int(torch.cuda.max_memory_allocated()),
                "arena_bytes": d2.plan.arena_bytes, "scratch_bytes": d2.plan.scratch_bytes}
+        return rec, d2, key
+
+    out = None
+    for streams in args.ns_streams:
+        ecfg = ExecConfig(gemm_backend=args.backend, spatial_k=bt, temporal_k=bt, slice_streams=streams)
+        rec, d2, key = measure(ecfg)
+        rec = dict(plan=f"spatial k = {bt} (one frame per slice), temporal k = {bt} pixel bands, "
+                        f"{streams} slice stream(s)", **rec)
         if out is None:
             out = dict(rec, slices=slice_summary(d2.plan), gpu_launches_per_run=d2.launches[key], variants=[])
         else:
             out["variants"].append({k: rec[k] for k in ("plan", "value", "ms_per_step", "peak_hbm_bytes",
                                                           "scratch_bytes")})
+        del d2
+    # the same peak without per-frame launches where memory does not need them: the Feature Slicer's
+    # budget policy with the per-frame plan's whole scratch as the budget -- the largest (L0) groups
+    # still run one frame at a time, the deep levels take as many frames per slice as fit
+    if out is not None:
+        budget = int(out["scratch_bytes"])
+        ecfg = ExecConfig(gemm_backend=args.backend, scratch_budget=budget, slice_streams=1)
+        rec, d2, key = measure(ecfg)
+        out["equal_peak_plan"] = dict(
+            plan=f"budget slicing at the per-frame plan's scratch ({budget / 2**20:.1f} MiB), 1 slice stream",
+            **rec, slices=slice_summary(d2.plan), gpu_launches_per_run=d2.launches[key])
         del d2
     return out
 

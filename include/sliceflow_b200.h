@@ -105,6 +105,13 @@ typedef struct {
    * NULL = off. */
   const float* rowstats;
   const float* colvec;
+  /* GroupNorm statistics of the output from the epilogue (CONV3X3, bf16 output): per (frame,
+   * split, channel) fp32 (sum, sum of squares) of the STORED bf16 values, layout
+   * [n_outer][sf_conv_gn_splits(H, W)][N] float2; a split = one half (64 rows) of a 128-pixel
+   * tile, or one frame's rows of a tail tile.  Finished by sf_group_norm_finalize.  NULL = off.
+   * Replaces the statistics pass of the GroupNorm that reads this conv's output
+   * (kernels.py:228-237; unet.py:191-193, res.conv1 -> res.norm2). */
+  void* gn_partial;
 } sf_gemm_args;
 
 /* ---- GEMM core: conv2d / temporal_conv / linear / attention projections ---- */
@@ -121,6 +128,16 @@ int32_t sf_gemm_backend(const sf_gemm_args* args);
 int64_t sf_group_norm_workspace(int32_t frames, int32_t n_inner, int32_t C);
 sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
                               float eps, void* work, float* mean, float* rstd, void* stream);
+/* Partial-sum splits per frame of a CONV3X3 sf_gemm with gn_partial (frame-geometry only). */
+int32_t sf_conv_gn_splits(int32_t H, int32_t W);
+/* The same partials as a pass over a stored conv output y (frames of H x W rows, C channels):
+ * identical layout and summation order (the mma.sync backend's path, and the fused one's checker). */
+sf_status sf_conv_gn_partials(sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, void* partial,
+                              void* stream);
+/* mean / rstd per (frame, group) from [frames][splits][C] float2 (sum, sum sq) partials,
+ * fp64 fixed-order combine; n_inner = rows per frame. */
+sf_status sf_group_norm_finalize(const void* partial, int32_t frames, int32_t splits, int32_t n_inner, int32_t C,
+                                 int32_t groups, float eps, float* mean, float* rstd, void* stream);
 /* y = act((x - mean) * rstd * gamma + beta), per (frame, group) stats. */
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C,
                               int32_t groups, const float* mean, const float* rstd, const float* gamma,

@@ -41,6 +41,7 @@ class GemmArgs(C.Structure):
         ("out", View), ("out_bstride", i64),
         ("out_fp32", i32), ("backend", i32),
         ("rowstats", vp), ("colvec", vp),
+        ("gn_partial", vp),
     ]
 
 
@@ -54,6 +55,9 @@ _PROTOS = {
     "sf_gemm_backend": [C.POINTER(GemmArgs)],
     "sf_group_norm_workspace": [i32, i32, i32],
     "sf_group_norm_stats": [View, i32, i32, i32, i32, f32, vp, vp, vp, vp],
+    "sf_conv_gn_splits": [i32, i32],
+    "sf_conv_gn_partials": [View, i32, i32, i32, i32, vp, vp],
+    "sf_group_norm_finalize": [vp, i32, i32, i32, i32, i32, f32, vp, vp, vp],
     "sf_group_norm_apply": [View, View, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp],
     "sf_layer_norm": [View, View, i32, i32, i32, vp, vp, f32, i32, vp],
     "sf_layer_norm_stats": [View, i32, i32, i32, f32, vp, vp],
@@ -86,6 +90,7 @@ _RESTYPE = {
     "sf_dot3_workspace": i64,
     "sf_gram_workspace": i64,
     "sf_gemm_backend": i32,
+    "sf_conv_gn_splits": i32,
     "sf_flash_supported": i32,
     "sf_temporal_attention_fused_supported": i32,
     "sf_last_error": C.c_char_p,

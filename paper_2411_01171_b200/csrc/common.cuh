@@ -142,4 +142,33 @@ inline int num_sms() {
   return n;
 }
 
+// Row tiling of a CONV3X3 implicit GEMM over one frame (gemm_tc.cu): 128-row tiles of
+// w_t x h_t pixels (w_t = the largest power of two <= min(W, 128)); when H % h_t = rem divides
+// h_t, the last rem rows of h_t / rem consecutive frames form one *tail tile* per x-tile
+// (SF_GEMM_TAIL=0 turns that off, and the last band then overhangs the frame).  The epilogue's
+// GroupNorm partials use one split per 64-row half of a main tile and one per tail tile:
+// splits per frame = 2 * tiles_x * tiles_y + (tail ? tiles_x : 0).
+struct ConvTiling {
+  int w_t, h_t, tiles_x, tiles_y, tail_rows, tail_fb;
+  __host__ __device__ int gn_splits() const { return 2 * tiles_x * tiles_y + (tail_rows ? tiles_x : 0); }
+};
+inline ConvTiling conv_tiling(int H, int W) {
+  ConvTiling t{};
+  int p = 1;
+  const int cap = W < 128 ? W : 128;
+  while (p * 2 <= cap) p *= 2;
+  t.w_t = p;
+  t.h_t = 128 / p;
+  t.tiles_x = (W + t.w_t - 1) / t.w_t;
+  t.tiles_y = (H + t.h_t - 1) / t.h_t;
+  const int rem = H % t.h_t;
+  static const char* tail_env = getenv("SF_GEMM_TAIL");
+  if (rem && t.h_t % rem == 0 && !(tail_env && tail_env[0] == '0')) {
+    t.tail_rows = rem;
+    t.tail_fb = t.h_t / rem;
+    t.tiles_y = H / t.h_t;
+  }
+  return t;
+}
+
 }  // namespace sf

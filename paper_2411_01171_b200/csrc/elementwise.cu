@@ -189,6 +189,53 @@ static void launch_gn_finalize(const T* partial, int frames, int splits, int C, 
            groups, gpb, count, eps, mean, rstd);
 }
 
+// GroupNorm partials of a CONV3X3 output as a separate pass, in the layout and summation order
+// of the tcgen05 GEMM epilogue's (gemm_tc.cu gn_tile_partials): the mma.sync backend's
+// counterpart, and the checker of the fused partials (identical bits).  Block = (split, frame),
+// thread = a column pair.
+__global__ void __launch_bounds__(128) conv_gn_partials_kernel(sf_view_t y, int H, int W, int N, ConvTiling ct,
+                                                               float2* part) {
+  griddep_wait();
+  const int s = blockIdx.x, fr = blockIdx.y, splits = ct.gn_splits();
+  const int n_main = 2 * ct.tiles_x * ct.tiles_y;
+  int x0, y0, r0, nrows;
+  if (s < n_main) {
+    const int tile = s >> 1;
+    x0 = (tile % ct.tiles_x) * ct.w_t;
+    y0 = (tile / ct.tiles_x) * ct.h_t;
+    r0 = (s & 1) * 64;
+    nrows = 64;
+  } else {
+    x0 = (s - n_main) * ct.w_t;
+    y0 = ct.tiles_y * ct.h_t;
+    r0 = 0;
+    nrows = ct.tail_rows * ct.w_t;
+  }
+  for (int c2 = threadIdx.x; 2 * c2 < N; c2 += blockDim.x) {
+    float a0 = 0.f, a1 = 0.f, q0 = 0.f, q1 = 0.f;
+    for (int r = r0; r < r0 + nrows; ++r) {
+      const int yy = y0 + r / ct.w_t, xx = x0 + r % ct.w_t;
+      if (yy < H && xx < W) {
+        const float2 f =
+            __bfloat1622float2(*reinterpret_cast<const bf162*>(row_ptr<const bf16>(y, fr, (int64_t)yy * W + xx) + 2 * c2));
+        a0 += f.x;
+        q0 = fmaf(f.x, f.x, q0);
+        a1 += f.y;
+        q1 = fmaf(f.y, f.y, q1);
+      }
+    }
+    part[((int64_t)fr * splits + s) * N + 2 * c2] = make_float2(a0, q0);
+    part[((int64_t)fr * splits + s) * N + 2 * c2 + 1] = make_float2(a1, q1);
+  }
+}
+
+sf_status conv_gn_partials(sf_view_t y, int frames, int H, int W, int N, void* part, cudaStream_t st) {
+  const ConvTiling ct = conv_tiling(H, W);
+  launch_k(conv_gn_partials_kernel, dim3((unsigned)ct.gn_splits(), (unsigned)frames), dim3(128), 0, st, y, H, W, N,
+           ct, (float2*)part);
+  return launch_status("conv_gn_partials");
+}
+
 // Small planes (deep levels, n_inner <= GN_DIRECT_MAX_ROWS): ONE launch, one block per (frame,
 // run of gpb whole groups = W channels): 8-channel vectors x rows_per_iter row lanes read the
 // block's rows (GN_U loads in flight), fp32 per thread -> fp64 per channel in shared memory ->
@@ -1269,6 +1316,29 @@ sf_status sf_group_norm_stats(sf_view_t x, int32_t frames, int32_t n_inner, int3
   launch_gn_finalize((const double2*)work, frames, splits, C, groups, (int64_t)n_inner * (C / groups), eps, mean,
                      rstd, st);
   return launch_status("sf_group_norm_stats");
+}
+
+int32_t sf_conv_gn_splits(int32_t H, int32_t W) {
+  if (H < 1 || W < 1) return 0;
+  return conv_tiling(H, W).gn_splits();
+}
+
+sf_status sf_conv_gn_partials(sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, void* partial,
+                              void* stream) {
+  SF_CHECK_ARG(frames >= 1 && H >= 1 && W >= 1 && C >= 2 && C % 2 == 0, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(y.ptr && partial && (y.ld % 2) == 0 && ((uintptr_t)y.ptr & 3) == 0 && ((uintptr_t)partial & 7) == 0,
+               SF_ERR_PARAM, "null or unaligned buffer");
+  return conv_gn_partials(y, frames, H, W, C, partial, (cudaStream_t)stream);
+}
+
+sf_status sf_group_norm_finalize(const void* partial, int32_t frames, int32_t splits, int32_t n_inner, int32_t C,
+                                 int32_t groups, float eps, float* mean, float* rstd, void* stream) {
+  SF_CHECK_ARG(frames >= 1 && splits >= 1 && n_inner >= 1 && C >= 1, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
+  SF_CHECK_ARG(partial && mean && rstd && ((uintptr_t)partial & 7) == 0, SF_ERR_PARAM, "null or unaligned buffer");
+  launch_gn_finalize((const float2*)partial, frames, splits, C, groups, (int64_t)n_inner * (C / groups), eps, mean,
+                     rstd, (cudaStream_t)stream);
+  return launch_status("sf_group_norm_finalize");
 }
 
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,

@@ -7,6 +7,7 @@ namespace sf {
 sf_status gemm_mma_launch(const sf_gemm_args& p, cudaStream_t st);
 bool gemm_tc_supported(const sf_gemm_args& p);
 sf_status gemm_tc_launch(const sf_gemm_args& p, cudaStream_t st);
+sf_status conv_gn_partials(sf_view_t y, int frames, int H, int W, int N, void* part, cudaStream_t st);
 }  // namespace sf
 
 using namespace sf;
@@ -30,6 +31,9 @@ static sf_status validate(const sf_gemm_args* a) {
   if (a->rowstats)
     SF_CHECK_ARG(a->colvec && a->mode == SF_GEMM_PLAIN && a->batch == 1 && ((uintptr_t)a->rowstats & 7) == 0,
                  SF_ERR_PARAM, "folded LayerNorm needs colvec, PLAIN mode, batch 1, 8-byte aligned stats");
+  if (a->gn_partial)
+    SF_CHECK_ARG(a->mode == SF_GEMM_CONV3X3 && !a->out_fp32 && a->N % 2 == 0 && aligned16(a->gn_partial),
+                 SF_ERR_PARAM, "GroupNorm partials need CONV3X3, bf16 output, even N, 16-byte aligned buffer");
   return SF_OK;
 }
 
@@ -47,5 +51,9 @@ extern "C" sf_status sf_gemm(const sf_gemm_args* a, void* stream) {
   int be = sf_gemm_backend(a);
   SF_CHECK_ARG(be != 0, SF_ERR_UNSUPPORTED, "forced tcgen05 backend cannot take this shape");
   if (be == 2) return gemm_tc_launch(*a, (cudaStream_t)stream);
-  return gemm_mma_launch(*a, (cudaStream_t)stream);
+  s = gemm_mma_launch(*a, (cudaStream_t)stream);
+  // the mma.sync kernel has no fused statistics: the same partials from a pass over its output
+  if (s == SF_OK && a->gn_partial)
+    s = conv_gn_partials(a->out, a->n_outer, a->H, a->W, a->N, a->gn_partial, (cudaStream_t)stream);
+  return s;
 }

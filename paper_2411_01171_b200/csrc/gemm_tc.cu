@@ -61,7 +61,10 @@ struct Params {
   sf_view_t out;
   int64_t out_bstride;
   int out_fp32;
-  // optional GroupNorm partial sums of the bf16 output (conv, whole-frame tiles):
+  // CONV, bf16 output: GroupNorm partials of the stored output, [frame][gn_splits][N] (sum, sum sq)
+  // (sf_gemm_args.gn_partial; split = 64-row half of a main tile, or a frame's rows of a tail tile)
+  float2* gn_part;
+  int gn_splits;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -413,6 +416,38 @@ __device__ unsigned int g_tc_trace_n[4];
   do {                    \
   } while (0)
 #endif
+
+// Per-(frame, split, channel) (sum, sum sq) of one staged bf16 half-tile (128 rows x HC columns,
+// row-major): thread t sums column pair t % 64 over the 64 rows of half t / 64 -- one frame in a
+// main tile; in a tail tile the half holds 64 / per whole frame segments of per rows each.
+template <int HC>
+__device__ __forceinline__ void gn_tile_partials(const Params& p, const MTile& mt, const uint8_t* hbuf, int hn0,
+                                                 int t) {
+  const int pair = t & 63, rh = t >> 6;
+  if (2 * pair >= HC || hn0 + 2 * pair >= p.N) return;
+  const int lg = __ffs(p.w_t) - 1;                      // w_t is a power of two
+  const int per = mt.tail ? p.tail_rows * p.w_t : 64;   // rows per frame segment (<= 64)
+  for (int s0 = rh * 64; s0 < rh * 64 + 64; s0 += per) {
+    const int fr = mt.tail ? mt.f + s0 / per : mt.f;
+    if (fr >= p.n_frames) break;
+    float a0 = 0.f, a1 = 0.f, q0 = 0.f, q1 = 0.f;
+    for (int r = s0; r < s0 + per; ++r) {
+      const int rr = mt.tail ? r - s0 : r;
+      const int y = mt.y0 + (rr >> lg), x = mt.x0 + (rr & (p.w_t - 1));
+      if (y < p.H && x < p.W) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const bf162*>(hbuf + r * (HC * 2) + pair * 4));
+        a0 += f.x;
+        q0 = fmaf(f.x, f.x, q0);
+        a1 += f.y;
+        q1 = fmaf(f.y, f.y, q1);
+      }
+    }
+    const int split = mt.tail ? 2 * p.tiles_x * p.tiles_y + (mt.x0 >> lg)
+                              : 2 * ((mt.y0 / p.h_t) * p.tiles_x + (mt.x0 >> lg)) + rh;
+    *reinterpret_cast<float4*>(p.gn_part + ((int64_t)fr * p.gn_splits + split) * p.N + hn0 + 2 * pair) =
+        make_float4(a0, q0, a1, q1);
+  }
+}
 
 // PAIR: CTA pairs (cluster of 2) run tcgen05.mma.cta_group::2 with M = 256:
 // CTA rank r owns M-tile 2*pair + r (its A rows, TMEM accumulator and epilogue)
@@ -827,6 +862,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // my half-tile complete -> my leader stores it with TMA (OOB rows/cols are clipped)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         half_sync();
+        if constexpr (CONV) {
+          // GroupNorm partials of the next op (res.norm2 reads this conv's output, unet.py:191-193)
+          // from the staged bf16 half-tile -- the exact values stored -- while the TMA store reads
+          // it too: thread = (64-row half, column pair); fixed order, no atomics
+          if (p.gn_part != nullptr && !phantom) {
+            gn_tile_partials<HC>(p, mt, hbuf, hn0, row);
+            half_sync();   // staging reads done before the buffer is refilled (residual / next tile)
+          }
+        }
         if (hleader) {
           if (hn0 < p.N) {
             if (CONV)
@@ -981,12 +1025,6 @@ static bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* d
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
-}
-
-static int pow2_floor(int v) {
-  int p = 1;
-  while (p * 2 <= v) p *= 2;
-  return p;
 }
 
 static int pick_bn(int N) {
@@ -1192,9 +1230,10 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
   if (a.mode == SF_GEMM_CONV3X3) {
     p.H = a.H;
     p.W = a.W;
-    p.w_t = pow2_floor(a.W < 128 ? a.W : 128);
-    p.h_t = BM / p.w_t;
-    p.tiles_x = (a.W + p.w_t - 1) / p.w_t;
+    const ConvTiling ct = conv_tiling(a.H, a.W);
+    p.w_t = ct.w_t;
+    p.h_t = ct.h_t;
+    p.tiles_x = ct.tiles_x;
     p.tiles_y = (a.H + p.h_t - 1) / p.h_t;
     p.tiles_m = (int64_t)p.tiles_x * p.tiles_y * a.n_outer;
     uint64_t dims[4] = {(uint64_t)a.cin, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.n_outer};
@@ -1207,9 +1246,8 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
     p.n_frames = a.n_outer;
     p.n_main = p.tiles_m;
     const int rem = a.H % p.h_t;
-    static const char* tail_env = getenv("SF_GEMM_TAIL");
-    if (rem && p.h_t % rem == 0 && !(tail_env && tail_env[0] == '0')) {
-      const int fb = p.h_t / rem;
+    if (ct.tail_rows) {
+      const int fb = ct.tail_fb;
       uint32_t tbox[4] = {BK, (uint32_t)p.w_t, (uint32_t)rem, (uint32_t)fb};
       if (encode(&mat, a.a.ptr, 4, dims, str, tbox)) {
         p.tail_rows = rem;
@@ -1219,6 +1257,11 @@ sf_status gemm_tc_launch(const sf_gemm_args& a, cudaStream_t st) {
         p.n_main = (int64_t)p.tiles_x * p.tiles_y * a.n_outer;
         p.tiles_m = p.n_main + (int64_t)p.tiles_x * ((a.n_outer + fb - 1) / fb);
       }
+    }
+    if (a.gn_partial) {
+      p.gn_part = reinterpret_cast<float2*>(a.gn_partial);
+      p.gn_splits = 2 * p.tiles_x * p.tiles_y + (p.tail_rows ? p.tiles_x : 0);
+      SF_CHECK_ARG(p.gn_splits == ct.gn_splits(), SF_ERR_CUDA, "conv tiling disagrees with sf_conv_gn_splits");
     }
   } else {
     int n_inner = a.n_inner, n_outer = a.n_outer;

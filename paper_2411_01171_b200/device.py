@@ -152,7 +152,7 @@ class DeviceWeights:
 def gemm_args(*, mode, n_outer, n_inner, cin, n, a: Rows, w: torch.Tensor, w_ld=None, w_kmajor=True,
               out: Rows, out_fp32=False, bias=None, rowbias=None, rowbias_stride=0, act=N.ACT_NONE,
               res: Rows | None = None, H=0, W=0, T=0, batch=1, a_bstride=0, w_bstride=0, out_bstride=0,
-              res_bstride=0, alpha=1.0, backend=0, w_ptr=None, rowstats=None, colvec=None):
+              res_bstride=0, alpha=1.0, backend=0, w_ptr=None, rowstats=None, colvec=None, gn_partial=None):
     args = N.GemmArgs()
     args.mode, args.n_outer, args.n_inner = mode, n_outer, n_inner
     args.H, args.W, args.T = H, W, T
@@ -174,6 +174,7 @@ def gemm_args(*, mode, n_outer, n_inner, cin, n, a: Rows, w: torch.Tensor, w_ld=
     args.backend = backend
     args.rowstats = rowstats.data_ptr() if rowstats is not None else None
     args.colvec = colvec.data_ptr() if colvec is not None else None
+    args.gn_partial = gn_partial
     return args
 
 
@@ -190,13 +191,15 @@ class Epilogue:
         self.act, self.rowbias, self.res = act, rowbias, res
 
 
-def conv2d(stream, x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue, backend=0, out_fp32=False):
-    """3x3 conv (kernels.py:181-201) as an implicit GEMM."""
+def conv2d(stream, x: Rows, y: Rows, frames, H, W, cin, cout, prm, epi: Epilogue, backend=0, out_fp32=False,
+           gn_partial=None):
+    """3x3 conv (kernels.py:181-201) as an implicit GEMM.  ``gn_partial``: device address of
+    [frames][sf_conv_gn_splits(H, W)][cout] float2 GroupNorm partials of the stored output."""
     if "w" not in prm:
         raise ShapeMismatch(f"conv2d with cin={cin} needs the small-channel path")
     return gemm(stream, mode=N.GEMM_CONV3X3, n_outer=frames, n_inner=H * W, H=H, W=W, cin=cin, n=cout, a=x,
                 w=prm["w"], out=y, out_fp32=out_fp32, bias=prm["bias"], rowbias=epi.rowbias, act=epi.act,
-                res=epi.res, backend=backend)
+                res=epi.res, backend=backend, gn_partial=gn_partial)
 
 
 TAPWISE_MAX_COUT = 16

@@ -83,6 +83,8 @@ class ExecConfig:
     slice_streams: int = 1      # s > 1: consecutive slices of a sliced group round-robin over s streams
     ln_fold: bool = False       # LayerNorm -> temporal attention: statistics pass + folded QKV GEMM
                                 # (measured: faster at C >= 640, slower at L0 -- profiles finding 31)
+    gn_from_conv: bool = True   # a GroupNorm reading a conv's output takes its statistics from the
+                                # conv epilogue's partials (sf_gemm gn_partial) instead of a stats pass
     gemm_backend: int = 0
     device: str = "cuda"
     rank: int = 0          # frame/pixel shard owned by this plan (parallel.py)
@@ -148,6 +150,8 @@ class Plan:
         self.epilogue_of: dict[str, tuple[str, str, bool]] = {}  # producer tail -> (add id, operand, is_emb)
         self.units: list[Unit] = []
         self.emb_nodes: list[str] = []
+        self.gn_feed: dict[str, str] = {}        # conv node id -> GroupNorm input value it produces
+        self.gn_part: dict[str, tuple] = {}      # that value -> (partials tensor, splits per frame)
         self.exchanger = None
         self._analyse()
         self._layout()
@@ -186,6 +190,65 @@ class Plan:
                 continue
             self.fused_adds[nid] = (a, b)
             self.epilogue_of[a] = (nid, b, is_emb)
+        if self.cfg.gn_from_conv and os.environ.get("SF_GN_FROM_CONV") != "0":
+            self._analyse_gn_feed()
+
+    def _analyse_gn_feed(self):
+        """GroupNorms whose input is the stored output of a 3x3 conv (res.conv1 (+ step embedding)
+        -> res.norm2, unet.py:186-193): the conv's GEMM epilogue emits per-(frame, tile) partial
+        sums of exactly the values it stores, so the GroupNorm needs only the finalize."""
+        for grp in self.grouped.groups:
+            if grp.domain is not Domain.SPATIAL or grp.ops[0].kind is not OpKind.GROUP_NORM:
+                continue
+            v = grp.head_input
+            src = self.fused_adds[v][0] if v in self.fused_adds else v
+            _, pg = self._producer_group(src)
+            if pg is None or pg.domain is not Domain.SPATIAL:
+                continue
+            conv = pg.ops[-1]
+            if conv.kind is not OpKind.CONV2D or "w" not in self.dw.p.get(conv.id, {}):
+                continue
+            if pg.head_input == "x" or conv.id in self.gn_feed:
+                continue
+            if self.shapes[conv.id] != self.shapes[v]:
+                continue
+            self.gn_feed[conv.id] = v
+        # partial buffers: one slot per set of producer -> consumer intervals that do not overlap
+        # in the schedule (each norm2 group directly follows its conv1 group: one slot in the U-Net)
+        spos = {(k, r): i for i, (k, r) in enumerate(self.grouped.schedule)}
+
+        def gpos(vid):
+            gi, _ = self._producer_group(vid)
+            return spos[("group", gi)]
+        cons_pos = {grp.head_input: spos[("group", gi)] for gi, grp in enumerate(self.grouped.groups)}
+        f0, f1 = self._frames()
+        self._gn_slot_of, self._gn_slot_elems, free_after = {}, [], []
+        for conv_id, v in sorted(self.gn_feed.items(), key=lambda kv: gpos(kv[0])):
+            a, b = gpos(conv_id), cons_pos[v]
+            s = self.shapes[v]
+            elems = (f1 - f0) * int(N.query("sf_conv_gn_splits", s.h, s.w)) * s.c * 2
+            for k, fa in enumerate(free_after):
+                if fa < a:
+                    break
+            else:
+                k = len(free_after)
+                free_after.append(-1)
+                self._gn_slot_elems.append(0)
+            free_after[k] = b
+            self._gn_slot_elems[k] = max(self._gn_slot_elems[k], elems)
+            self._gn_slot_of[v] = k
+        self._gn_slots: list[torch.Tensor | None] = [None] * len(self._gn_slot_elems)
+
+    def gn_partials(self, vid):
+        """(partials buffer over this rank's frames, splits per frame) for a GroupNorm input fed
+        by a conv epilogue; the slot tensor is allocated when the first user compiles."""
+        if vid not in self.gn_part:
+            k = self._gn_slot_of[vid]
+            if self._gn_slots[k] is None:
+                self._gn_slots[k] = torch.empty((self._gn_slot_elems[k],), dtype=torch.float32, device=self.dev)
+            s = self.shapes[vid]
+            self.gn_part[vid] = (self._gn_slots[k], int(N.query("sf_conv_gn_splits", s.h, s.w)))
+        return self.gn_part[vid]
 
     # ------------------------------------------------------------------ layout
     def _storage_id(self, vid):
@@ -732,6 +795,10 @@ class Plan:
             backend |= N.GEMM_NO_PAIR
         scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
         eps_out = self.fp32_out and tail == self.graph.outputs[0]
+        # GroupNorm statistics handed over through conv-epilogue partials (_analyse_gn_feed)
+        fr0 = self._frames()[0]
+        gn_out = self.gn_partials(self.gn_feed[tail]) if tail in self.gn_feed else None
+        gn_in = self.gn_partials(x_id) if x_id in self.gn_feed.values() else None
 
         def run(st0):
             streams = self._fork(st0, ncopy)
@@ -763,8 +830,12 @@ class Plan:
                         stats = scratch["gn_stats"]
                         mean = stats[:nf * groups, 0]
                         rstd = stats[fmax * max_groups: fmax * max_groups + nf * groups, 0]
-                        D.group_norm_stats(st, X, nf, ihw, ish.c, groups, float(o.attrs.get("eps", 1e-5)),
-                                           scratch["gn_work"], mean, rstd)
+                        eps = float(o.attrs.get("eps", 1e-5))
+                        if src == "IN" and gn_in is not None:
+                            N.call("sf_group_norm_finalize", gn_in[0].data_ptr() + (sl[0] - fr0) * gn_in[1] * ish.c * 8,
+                                   nf, gn_in[1], ihw, ish.c, groups, eps, mean.data_ptr(), rstd.data_ptr(), st)
+                        else:
+                            D.group_norm_stats(st, X, nf, ihw, ish.c, groups, eps, scratch["gn_work"], mean, rstd)
                         D.group_norm_apply(st, X, Y, nf, ihw, ish.c, groups, mean, rstd, prm, act)
                     elif k is OpKind.LAYER_NORM:
                         D.layer_norm(st, X, Y, nf, ihw, ish.c, prm, float(o.attrs.get("eps", 1e-5)), act)
@@ -785,7 +856,10 @@ class Plan:
                                 D.conv2d(st, X, out, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend,
                                          out_fp32=True)
                         else:
-                            D.conv2d(st, X, Y, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend)
+                            gp = None
+                            if last and gn_out is not None:
+                                gp = gn_out[0].data_ptr() + (sl[0] - fr0) * gn_out[1] * osh.c * 8
+                            D.conv2d(st, X, Y, nf, ish.h, ish.w, ish.c, osh.c, prm, epi, backend, gn_partial=gp)
                     elif k is OpKind.LINEAR:
                         D.linear(st, X, Y, nf, ihw, ish.c, osh.c, prm, epi, backend)
                     elif k is OpKind.SPATIAL_ATTENTION:
@@ -980,6 +1054,7 @@ class _GroupPlan(Plan):
         self.pos = {n: i for i, n in enumerate(self.topo)}
         self.cons = graph.consumers()
         self.values, self.fused_adds, self.epilogue_of, self.units, self.emb_nodes = {}, {}, {}, [], []
+        self.gn_feed, self.gn_part = {}, {}     # one group: no statistics handed across groups
         self.exchanger = None
         so = self.shapes[group.tail]
         self.inp = torch.empty(in_shape.rows, in_shape.c, dtype=torch.bfloat16, device=self.dev)
@@ -1078,12 +1153,14 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     plan.pos = {n: i for i, n in enumerate(plan.topo)}
     plan.cons = graph.consumers()
     plan.values, plan.fused_adds, plan.epilogue_of, plan.units, plan.emb_nodes = {}, {}, {}, [], []
+    plan.gn_feed, plan.gn_part = {}, {}
     plan.exchanger = None
     plan._analyse()
     plan._layout()
     led = plan.memory_ledger()
     out = {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers), "ledger": led,
-           "ledger_peak_bytes": led.peak_bytes}
+           "ledger_peak_bytes": led.peak_bytes,
+           "gn_partial_bytes": 4 * sum(getattr(plan, "_gn_slot_elems", [])), "gn_from_conv": len(plan.gn_feed)}
     if plan.cfg.world > 1:
         from .parallel import exchange_schedule
         ex = exchange_schedule(plan)

@@ -1,0 +1,148 @@
+"""GroupNorm statistics from the conv epilogue (sf_gemm gn_partial) on the B200.
+
+The res-block GroupNorm res.norm2 reads the stored output of res.conv1 (+ step embedding)
+(/root/reference/pkg/src/sliceflow/unet.py:186-193); the tcgen05 conv's epilogue emits
+per-(frame, split, channel) (sum, sum sq) of exactly the bf16 values it stores, and
+sf_group_norm_finalize turns them into the (frame, group) mean / rstd of _group_norm
+(kernels.py:228-237).  Checked here:
+  * the fused partials equal the separate pass (sf_conv_gn_partials) over the same output bit for
+    bit -- same layout, same fp32 summation order -- on main tiles, tail tiles, CTA pairs and
+    single-CTA tiles, with residual / per-frame bias epilogues;
+  * their per-frame totals equal a torch fp64 reduction of the output (1e-5);
+  * finalize(partials) equals the statistics pass (sf_group_norm_stats) on the same tensor;
+  * the mma.sync backend (toy widths) produces the same partials through the pass.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2411_01171_b200 import _native as N  # noqa: E402
+from paper_2411_01171_b200 import device as D  # noqa: E402
+from paper_2411_01171_b200.build import build  # noqa: E402
+from paper_2411_01171_b200.device import Rows  # noqa: E402
+
+build()
+dev = torch.device("cuda")
+
+
+def rnd(*shape, scale=1.0):
+    return (torch.randn(*shape, device=dev) * scale).to(torch.bfloat16)
+
+
+def conv(x, wk, out, F_, H, W, C, Co, backend, part=None, res=None, emb=None, bias=None):
+    st = torch.cuda.current_stream().cuda_stream
+    return D.gemm(st, mode=N.GEMM_CONV3X3, n_outer=F_, n_inner=H * W, H=H, W=W, cin=C, n=Co,
+                  a=Rows(x.view(-1, C), 0, H * W), w=wk, out=Rows(out, 0, H * W), bias=bias, rowbias=emb,
+                  rowbias_stride=Co if emb is not None and emb.dim() == 2 else 0,
+                  res=Rows(res, 0, H * W) if res is not None else None, backend=backend,
+                  gn_partial=part.data_ptr() if part is not None else None)
+
+
+CASES = [  # frames, H, W, cin, cout  (C3 levels, tail tiles of 64 / 16-row segments, toy widths)
+    (3, 72, 128, 320, 320), (2, 36, 64, 320, 640), (5, 18, 32, 640, 1280), (25, 9, 16, 256, 1280),
+    (7, 4, 16, 64, 64), (3, 9, 16, 64, 128), (4, 8, 8, 64, 192)]
+
+
+@pytest.mark.parametrize("backend", [2, 2 | 4])
+@pytest.mark.parametrize("F_,H,W,C,Co", CASES)
+@pytest.mark.parametrize("epi", ["emb", "res"])
+def test_fused_partials_equal_pass(backend, F_, H, W, C, Co, epi):
+    torch.manual_seed(3)
+    x = rnd(F_, H, W, C)
+    wk = rnd(Co, 9 * C, scale=(9 * C) ** -0.5)
+    bias = torch.randn(Co, device=dev)
+    emb = torch.randn(F_, Co, device=dev) if epi == "emb" else None
+    res = rnd(F_ * H * W, Co) if epi == "res" else None
+    splits = N.query("sf_conv_gn_splits", H, W)
+    part = torch.full((F_, splits, Co, 2), float("nan"), device=dev)
+    out = torch.empty(F_ * H * W, Co, dtype=torch.bfloat16, device=dev)
+    args = conv(x, wk, out, F_, H, W, C, Co, backend, part=part, res=res, emb=emb, bias=bias)
+    assert N.query("sf_gemm_backend", args) == 2
+    chk = torch.full_like(part, float("nan"))
+    N.call("sf_conv_gn_partials", Rows(out, 0, H * W).view(), F_, H, W, Co, chk.data_ptr(),
+           torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert not torch.isnan(part).any(), "every (frame, split, channel) written"
+    assert torch.equal(part, chk), "fused partials == pass, bit for bit"
+    # per-frame totals vs fp64
+    y = out.double().view(F_, H * W, Co)
+    tot = part.double().sum(1)
+    assert torch.allclose(tot[..., 0], y.sum(1), rtol=1e-5, atol=1e-3)
+    assert torch.allclose(tot[..., 1], (y * y).sum(1), rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("F_,H,W,C,Co", [(3, 72, 128, 320, 320), (5, 18, 32, 640, 1280), (25, 9, 16, 256, 1280)])
+def test_finalize_matches_stats_pass(F_, H, W, C, Co):
+    torch.manual_seed(4)
+    groups = 32
+    x = rnd(F_, H, W, C)
+    wk = rnd(Co, 9 * C, scale=(9 * C) ** -0.5)
+    bias = torch.randn(Co, device=dev) + 0.5
+    splits = N.query("sf_conv_gn_splits", H, W)
+    part = torch.empty((F_, splits, Co, 2), device=dev)
+    out = torch.empty(F_ * H * W, Co, dtype=torch.bfloat16, device=dev)
+    conv(x, wk, out, F_, H, W, C, Co, 0, part=part, bias=bias)
+    st = torch.cuda.current_stream().cuda_stream
+    m1, r1 = torch.empty(F_ * groups, device=dev), torch.empty(F_ * groups, device=dev)
+    m2, r2 = torch.empty_like(m1), torch.empty_like(r1)
+    N.call("sf_group_norm_finalize", part.data_ptr(), F_, splits, H * W, Co, groups, 1e-5, m1.data_ptr(),
+           r1.data_ptr(), st)
+    work = torch.empty((N.query("sf_group_norm_workspace", F_, H * W, Co) + 3) // 4, device=dev)
+    N.call("sf_group_norm_stats", Rows(out, 0, H * W).view(), F_, H * W, Co, groups, 1e-5, work.data_ptr(),
+           m2.data_ptr(), r2.data_ptr(), st)
+    torch.cuda.synchronize()
+    y = out.double().view(F_, H * W, groups, Co // groups)
+    mu = y.mean((1, 3)).flatten()
+    var = y.var((1, 3), unbiased=False).flatten()
+    assert torch.allclose(m1.double(), mu, rtol=1e-5, atol=1e-6)
+    assert torch.allclose(r1.double(), 1 / torch.sqrt(var + 1e-5), rtol=1e-5)
+    assert torch.allclose(m1, m2, rtol=1e-5, atol=1e-6) and torch.allclose(r1, r2, rtol=1e-5)
+
+
+@pytest.mark.parametrize("F_,H,W,C,Co", [(2, 16, 16, 16, 24), (3, 8, 8, 8, 8)])
+def test_mma_backend_partials(F_, H, W, C, Co):
+    """Toy widths run on mma.sync; sf_gemm then produces the partials with the pass."""
+    torch.manual_seed(5)
+    x = rnd(F_, H, W, C)
+    wk = rnd(Co, 9 * C, scale=(9 * C) ** -0.5)
+    splits = N.query("sf_conv_gn_splits", H, W)
+    part = torch.empty((F_, splits, Co, 2), device=dev)
+    out = torch.empty(F_ * H * W, Co, dtype=torch.bfloat16, device=dev)
+    args = conv(x, wk, out, F_, H, W, C, Co, 0, part=part)
+    assert N.query("sf_gemm_backend", args) == 1
+    torch.cuda.synchronize()
+    y = out.double().view(F_, H * W, Co)
+    assert torch.allclose(part.double().sum(1)[..., 0], y.sum(1), rtol=1e-5, atol=1e-3)
+
+
+def test_plan_uses_conv_partials_and_matches_stats_path():
+    """A tcgen05-width network (base 64): the plan hands res.norm2 its statistics from the conv1
+    epilogue; the denoised result stays within bf16 noise of the statistics-pass plan."""
+    from paper_2411_01171_b200.executor import ExecConfig
+    from paper_2411_01171_b200.harness import Denoiser, initial_latent
+    from paper_2411_01171_b200.rehash import StepSchedule
+    from paper_2411_01171_b200.unet import UNetConfig
+    cfg = UNetConfig(channels=4, frames=4, height=16, width=16, base_channels=64, norm_groups=8, steps=3)
+    x0 = initial_latent(cfg)
+    sched = StepSchedule([0, 1, 2], 3)
+    d1 = Denoiser(cfg, ExecConfig(gn_from_conv=True))
+    a = d1.run(x0, sched)
+    assert len(d1.plan.gn_feed) == 9
+    d2 = Denoiser(cfg, ExecConfig(gn_from_conv=False), device_weights=d1.model.dw)
+    b = d2.run(x0, sched)
+    assert not d2.plan.gn_feed
+    assert np.abs(a - b).max() / np.abs(b).max() < 2e-3
+    # ragged frame slices on two streams: the partial buffer is indexed by frame, so every slice
+    # finalises its own frames (the conv partials do not depend on the slicing)
+    d3 = Denoiser(cfg, ExecConfig(gn_from_conv=True, spatial_k=3, temporal_k=2, slice_streams=2),
+                  device_weights=d1.model.dw)
+    c = d3.run(x0, sched)
+    assert np.abs(c - b).max() / np.abs(b).max() < 2e-3
+    d4 = Denoiser(cfg, ExecConfig(gn_from_conv=True, spatial_k=3, temporal_k=2, slice_streams=1),
+                  device_weights=d1.model.dw)
+    assert np.array_equal(c, d4.run(x0, sched))
