@@ -212,20 +212,25 @@ __global__ void __launch_bounds__(128) conv_gn_partials_kernel(sf_view_t y, int 
     nrows = ct.tail_rows * ct.w_t;
   }
   for (int c2 = threadIdx.x; 2 * c2 < N; c2 += blockDim.x) {
-    float a0 = 0.f, a1 = 0.f, q0 = 0.f, q1 = 0.f;
-    for (int r = r0; r < r0 + nrows; ++r) {
-      const int yy = y0 + r / ct.w_t, xx = x0 + r % ct.w_t;
+    // row r -> accumulator r % 4, combined (0+1)+(2+3): gemm_tc.cu gn_tile_partials' order
+    float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+    float q0[4] = {0.f, 0.f, 0.f, 0.f}, q1[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < nrows; ++r) {
+      const int yy = y0 + (r0 + r) / ct.w_t, xx = x0 + (r0 + r) % ct.w_t;
       if (yy < H && xx < W) {
         const float2 f =
             __bfloat1622float2(*reinterpret_cast<const bf162*>(row_ptr<const bf16>(y, fr, (int64_t)yy * W + xx) + 2 * c2));
-        a0 += f.x;
-        q0 = fmaf(f.x, f.x, q0);
-        a1 += f.y;
-        q1 = fmaf(f.y, f.y, q1);
+        const int u = r & 3;
+        a0[u] += f.x;
+        q0[u] = fmaf(f.x, f.x, q0[u]);
+        a1[u] += f.y;
+        q1[u] = fmaf(f.y, f.y, q1[u]);
       }
     }
-    part[((int64_t)fr * splits + s) * N + 2 * c2] = make_float2(a0, q0);
-    part[((int64_t)fr * splits + s) * N + 2 * c2 + 1] = make_float2(a1, q1);
+    part[((int64_t)fr * splits + s) * N + 2 * c2] =
+        make_float2((a0[0] + a0[1]) + (a0[2] + a0[3]), (q0[0] + q0[1]) + (q0[2] + q0[3]));
+    part[((int64_t)fr * splits + s) * N + 2 * c2 + 1] =
+        make_float2((a1[0] + a1[1]) + (a1[2] + a1[3]), (q1[0] + q1[1]) + (q1[2] + q1[3]));
   }
 }
 

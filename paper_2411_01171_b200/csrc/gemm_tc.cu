@@ -419,7 +419,9 @@ __device__ unsigned int g_tc_trace_n[4];
 
 // Per-(frame, split, channel) (sum, sum sq) of one staged bf16 half-tile (128 rows x HC columns,
 // row-major): thread t sums column pair t % 64 over the 64 rows of half t / 64 -- one frame in a
-// main tile; in a tail tile the half holds 64 / per whole frame segments of per rows each.
+// main tile; in a tail tile the half holds 64 / per whole frame segments of per (16/32/64) rows.
+// Rows r = 4i + u go to accumulator u (four independent chains), combined as (0+1)+(2+3); the
+// pass kernel (elementwise.cu conv_gn_partials_kernel) uses the same order.
 template <int HC>
 __device__ __forceinline__ void gn_tile_partials(const Params& p, const MTile& mt, const uint8_t* hbuf, int hn0,
                                                  int t) {
@@ -430,22 +432,27 @@ __device__ __forceinline__ void gn_tile_partials(const Params& p, const MTile& m
   for (int s0 = rh * 64; s0 < rh * 64 + 64; s0 += per) {
     const int fr = mt.tail ? mt.f + s0 / per : mt.f;
     if (fr >= p.n_frames) break;
-    float a0 = 0.f, a1 = 0.f, q0 = 0.f, q1 = 0.f;
-    for (int r = s0; r < s0 + per; ++r) {
-      const int rr = mt.tail ? r - s0 : r;
-      const int y = mt.y0 + (rr >> lg), x = mt.x0 + (rr & (p.w_t - 1));
-      if (y < p.H && x < p.W) {
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const bf162*>(hbuf + r * (HC * 2) + pair * 4));
-        a0 += f.x;
-        q0 = fmaf(f.x, f.x, q0);
-        a1 += f.y;
-        q1 = fmaf(f.y, f.y, q1);
+    float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+    float q0[4] = {0.f, 0.f, 0.f, 0.f}, q1[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int r = s0; r < s0 + per; r += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = (mt.tail ? r - s0 : r) + u;
+        const int y = mt.y0 + (rr >> lg), x = mt.x0 + (rr & (p.w_t - 1));
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const bf162*>(hbuf + (r + u) * (HC * 2) + pair * 4));
+        if (y < p.H && x < p.W) {
+          a0[u] += f.x;
+          q0[u] = fmaf(f.x, f.x, q0[u]);
+          a1[u] += f.y;
+          q1[u] = fmaf(f.y, f.y, q1[u]);
+        }
       }
     }
     const int split = mt.tail ? 2 * p.tiles_x * p.tiles_y + (mt.x0 >> lg)
                               : 2 * ((mt.y0 / p.h_t) * p.tiles_x + (mt.x0 >> lg)) + rh;
     *reinterpret_cast<float4*>(p.gn_part + ((int64_t)fr * p.gn_splits + split) * p.N + hn0 + 2 * pair) =
-        make_float4(a0, q0, a1, q1);
+        make_float4((a0[0] + a0[1]) + (a0[2] + a0[3]), (q0[0] + q0[1]) + (q0[2] + q0[3]),
+                    (a1[0] + a1[1]) + (a1[2] + a1[3]), (q1[0] + q1[1]) + (q1[2] + q1[3]));
   }
 }
 
@@ -862,15 +869,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // my half-tile complete -> my leader stores it with TMA (OOB rows/cols are clipped)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         half_sync();
-        if constexpr (CONV) {
-          // GroupNorm partials of the next op (res.norm2 reads this conv's output, unet.py:191-193)
-          // from the staged bf16 half-tile -- the exact values stored -- while the TMA store reads
-          // it too: thread = (64-row half, column pair); fixed order, no atomics
-          if (p.gn_part != nullptr && !phantom) {
-            gn_tile_partials<HC>(p, mt, hbuf, hn0, row);
-            half_sync();   // staging reads done before the buffer is refilled (residual / next tile)
-          }
-        }
         if (hleader) {
           if (hn0 < p.N) {
             if (CONV)
@@ -879,6 +877,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tma_store_4d(&mapO, hbuf, hn0, mt.i0, mt.o0, mt.z);
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if constexpr (CONV) {
+          // GroupNorm partials of the next op (res.norm2 reads this conv's output, unet.py:191-193)
+          // from the staged bf16 half-tile -- the exact values stored -- while the TMA store reads
+          // it too: thread = (64-row half, column pair); fixed order, no atomics.  The buffer is
+          // next written after the next tile's opening half_sync, except by EPI 1's residual load,
+          // which its leader issues before that barrier: then wait for every reader here
+          if (p.gn_part != nullptr && !phantom) {
+            gn_tile_partials<HC>(p, mt, hbuf, hn0, row);
+            if (EPI == 1 && has_res) half_sync();
+          }
+        }
+        if (hleader) {
           // the other buffer's store (tile t-1) must drain before it is refilled
           if (EPI == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           TC_TR(2 + eh, 7);

@@ -796,9 +796,9 @@ class Plan:
         scratches = self._scratch(specs, ncopy) if ncopy > 1 else [self._scratch(specs)]
         eps_out = self.fp32_out and tail == self.graph.outputs[0]
         # GroupNorm statistics handed over through conv-epilogue partials (_analyse_gn_feed)
-        fr0 = self._frames()[0]
         gn_out = self.gn_partials(self.gn_feed[tail]) if tail in self.gn_feed else None
         gn_in = self.gn_partials(x_id) if x_id in self.gn_feed.values() else None
+        fr0 = self._frames()[0] if gn_out or gn_in else 0
 
         def run(st0):
             streams = self._fork(st0, ncopy)
