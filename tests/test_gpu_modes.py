@@ -240,3 +240,35 @@ def test_ln_fold_matches_unfolded(cfg):
     d = float(np.abs(a - b).max() / np.abs(ref).max())
     print(cfg.base_channels, "unfolded", ra, "folded", rb, "diff", d)
     assert rb <= 5e-3 and d <= 5e-3
+
+
+def test_eager_replay_fallback_matches_graph(monkeypatch):
+    """Denoiser.prepare falls back to eager replay when a launch in the run cannot be captured (e.g. a
+    collective whose transport refuses CUDA-graph capture): same result, bit for bit, and the same
+    launch count; also the explicit use_graph=False path."""
+    import torch
+
+    from paper_2411_01171_b200.harness import Denoiser
+    from paper_2411_01171_b200.rehash import StepSchedule
+    cfg = UNetConfig(channels=4, frames=4, height=16, width=16, base_channels=64, norm_groups=8, steps=4)
+    x0 = initial_latent(cfg)
+    sched = StepSchedule([0, 2, 3], 4)
+    den = Denoiser(cfg)
+    want = den.run(x0, sched)
+    assert den._graphs[den._key(sched, False)] is not None
+    eager = Denoiser(cfg, device_weights=den.model.dw)
+    key = eager.prepare(sched, use_graph=False)
+    assert eager._graphs[key] is None
+    eager.set_latent(x0)
+    eager.launch(key)
+    assert np.array_equal(eager.result(), want)
+
+    class Uncapturable:
+        def __init__(self, *a, **k):
+            raise RuntimeError("operation not permitted when stream is capturing")
+    monkeypatch.setattr(torch.cuda, "graph", Uncapturable)
+    fb = Denoiser(cfg, device_weights=den.model.dw)
+    got = fb.run(x0, sched)
+    assert fb._graphs[fb._key(sched, False)] is None
+    assert fb.launches[fb._key(sched, False)] == den.launches[den._key(sched, False)]
+    assert np.array_equal(got, want)
