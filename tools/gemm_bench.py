@@ -28,6 +28,7 @@ def main():
     ap.add_argument("n", type=int)
     ap.add_argument("--res", action="store_true")
     ap.add_argument("--silu", action="store_true")
+    ap.add_argument("--gn", action="store_true", help="conv: GroupNorm partials from the epilogue (gn_partial)")
     ap.add_argument("--reps", type=int, default=20)
     a = ap.parse_args()
     dev = torch.device("cuda")
@@ -43,6 +44,10 @@ def main():
     out = torch.empty(rows, a.n, device=dev, dtype=torch.bfloat16)
     res = torch.randn(rows, a.n, device=dev).to(torch.bfloat16) if a.res else None
     act = N.ACT_SILU if a.silu else N.ACT_NONE
+    part = None
+    if a.gn and a.mode == "conv":
+        F_, H, W = dims
+        part = torch.empty(F_ * N.query("sf_conv_gn_splits", H, W) * a.n * 2, device=dev)
 
     def run():
         if a.mode == "plain":
@@ -52,7 +57,8 @@ def main():
             F_, H, W = dims
             D.gemm(st, mode=N.GEMM_CONV3X3, n_outer=F_, n_inner=H * W, H=H, W=W, cin=a.cin, n=a.n,
                    a=Rows(x, 0, H * W), w=w, out=Rows(out, 0, H * W), bias=bias, act=act,
-                   res=Rows(res, 0, H * W) if res is not None else None)
+                   res=Rows(res, 0, H * W) if res is not None else None,
+                   gn_partial=part.data_ptr() if part is not None else None)
         elif a.mode == "vt":
             # the spatial-attention v^T projection (device.spatial_attention): A = wv (M = C),
             # B = the frame's tokens (K-major), batched over frames
@@ -75,7 +81,7 @@ def main():
     ms = s.elapsed_time(e) / a.reps
     fl = 2.0 * rows * a.n * taps * a.cin
     by = rows * a.cin * 2 + rows * a.n * 2 * (2 if a.res else 1)
-    print(f"gemm {a.mode} M={rows} K={taps * a.cin} N={a.n} res={a.res}: {ms * 1e3:.1f} us  "
+    print(f"gemm {a.mode} M={rows} K={taps * a.cin} N={a.n} res={a.res} gn={part is not None}: {ms * 1e3:.1f} us  "
           f"{fl / ms / 1e9:.1f} TF/s  {by / ms / 1e6:.0f} GB/s algorithmic")
 
 
