@@ -19,7 +19,7 @@ dev = torch.device("cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream().cuda_stream
 out = {}
-for (hw, C) in ((9216, 320), (2304, 640), (576, 1280), (144, 1280), (576, 2560)):
+for (hw, C) in ((9216, 320), (9216, 960), (2304, 640), (2304, 1920), (576, 1280), (144, 1280), (576, 2560)):
     F = 25
     x = torch.randn(F * hw, C, device=dev).to(torch.bfloat16)
     y = torch.empty_like(x)
