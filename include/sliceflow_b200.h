@@ -163,6 +163,16 @@ sf_status sf_downsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, i
 /* nearest-neighbour x2, frames of H x W -> 2H x 2W */
 sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C,
                         void* stream);
+/* The same resampling, also writing GroupNorm partials (float2 (sum, sum sq) per (frame, split,
+ * channel) at part[(frame * splits + split) * ld + c0 + c]; split = a contiguous range of the
+ * coarse pixels) for the GroupNorm that reads the result, or (downsample, in_part) the skip tensor
+ * it reads (unet.py:221-244: downsample -> next res.norm1; skip and upsample halves of
+ * up_blocks.i.concat -> res.norm1).  Finished by sf_group_norm_finalize.  NULL part = off. */
+sf_status sf_downsample2x_gn(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C,
+                             int32_t splits, void* out_part, int32_t out_ld, void* in_part, int32_t in_ld,
+                             void* stream);
+sf_status sf_upsample2x_gn(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, int32_t splits,
+                           void* out_part, int32_t out_ld, int32_t out_c0, void* stream);
 
 /* ---- attention cores (kernels.py:269-308) ---- */
 /* Row softmax of fp32 scores S[rows][n] (already scaled) -> bf16 P[rows][n]. */

@@ -66,6 +66,8 @@ _PROTOS = {
     "sf_copy_rows": [View, View, i32, i32, i32, vp],
     "sf_downsample2x": [View, View, i32, i32, i32, i32, vp],
     "sf_upsample2x": [View, View, i32, i32, i32, i32, vp],
+    "sf_downsample2x_gn": [View, View, i32, i32, i32, i32, i32, vp, i32, vp, i32, vp],
+    "sf_upsample2x_gn": [View, View, i32, i32, i32, i32, i32, vp, i32, i32, vp],
     "sf_softmax_rows": [vp, i64, vp, i64, i64, i32, vp],
     "sf_flash_supported": [i32, i32],
     "sf_spatial_attention_core": [View, View, vp, View, i32, i32, i32, f32, vp],

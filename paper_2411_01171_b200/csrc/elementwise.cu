@@ -605,6 +605,122 @@ __global__ void upsample_kernel(sf_view_t x, sf_view_t y, int frames, int H, int
   }
 }
 
+// Resampling with GroupNorm partials (the statistics the next GroupNorm would otherwise take in a
+// pass of its own; unet.py:221-244: down_blocks.i.downsample -> down_blocks.i+1.res.norm1, and the
+// skip / upsampled halves of up_blocks.i.concat -> up_blocks.i.res.norm1).  Block = (split, frame):
+// the split's contiguous range of COARSE pixels (the downsample's outputs, the upsample's inputs),
+// thread = (row lane, 8-channel vector); fp32 sums per thread, row lanes combined in lane order in
+// shared memory.  Partials land at part[(frame * splits + split) * ld + c0 + c] as float2 (sum,
+// sum sq):
+//   UP = 0: out_part = the stored (bf16-rounded) pooled output, in_part = the 4 input pixels read;
+//   UP = 1: out_part = the 2x2 copies written (4 x the input's sums, exact in fp32).
+template <int UP>
+__global__ void __launch_bounds__(256) resample_gn_kernel(sf_view_t x, sf_view_t y, int H, int W, int C, int splits,
+                                                          float2* out_part, int out_ld, int out_c0, float2* in_part,
+                                                          int in_ld) {
+  griddep_wait();
+  extern __shared__ float4 rsm[];   // [rows_per_iter][C] (out sum, out sq, in sum, in sq)
+  const int f = blockIdx.y, sp = blockIdx.x;
+  const int nvec = C / 8;
+  const int Wc = UP ? W : W / 2, coarse = UP ? H * W : (H / 2) * (W / 2);
+  const int chunk = (coarse + splits - 1) / splits;
+  const int p0 = sp * chunk, p1 = min(coarse, p0 + chunk);
+  const bool fits = nvec <= (int)blockDim.x;
+  const int rpi = fits ? blockDim.x / nvec : 1;
+  const int lane_v = fits ? threadIdx.x % nvec : threadIdx.x, lane_r = fits ? threadIdx.x / nvec : 0;
+  const bool active = lane_r < rpi;
+  for (int vb = lane_v; vb < nvec; vb += fits ? nvec : blockDim.x) {
+    float os[8], oq[8], is[8], iq[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) os[j] = oq[j] = is[j] = iq[j] = 0.f;
+    if (active) {
+      for (int pc = p0 + lane_r; pc < p1; pc += rpi) {
+        const int xc = pc % Wc, yc = pc / Wc;
+        if (UP) {
+          const bf16x8 val = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (int64_t)yc * W + xc) + vb * 8);
+          const int64_t o = (int64_t)(2 * yc) * (2 * W) + 2 * xc;
+          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o) + vb * 8) = val;
+          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 1) + vb * 8) = val;
+          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 2 * W) + vb * 8) = val;
+          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 2 * W + 1) + vb * 8) = val;
+          float v[8];
+          unpack8(val, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            os[j] += v[j];
+            oq[j] = fmaf(v[j], v[j], oq[j]);
+          }
+        } else {
+          float a[8], b[8], c[8], d[8], r[8];
+          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc) * W + 2 * xc) + vb * 8), a);
+          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc) * W + 2 * xc + 1) + vb * 8), b);
+          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc + 1) * W + 2 * xc) + vb * 8), c);
+          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc + 1) * W + 2 * xc + 1) + vb * 8),
+                  d);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) r[j] = (((a[j] + b[j]) + c[j]) + d[j]) * 0.25f;
+          const bf16x8 pk = pack8(r);
+          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, (int64_t)yc * Wc + xc) + vb * 8) = pk;
+          unpack8(pk, r);   // the statistics of what is stored
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            os[j] += r[j];
+            oq[j] = fmaf(r[j], r[j], oq[j]);
+            is[j] += ((a[j] + b[j]) + c[j]) + d[j];
+            iq[j] += ((a[j] * a[j] + b[j] * b[j]) + c[j] * c[j]) + d[j] * d[j];
+          }
+        }
+      }
+    }
+    if (fits) {
+      if (active) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) rsm[lane_r * C + vb * 8 + j] = make_float4(os[j], oq[j], is[j], iq[j]);
+      }
+      __syncthreads();
+      if (lane_r == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 t = rsm[vb * 8 + j];
+          for (int rr = 1; rr < rpi; ++rr) {
+            const float4 u = rsm[rr * C + vb * 8 + j];
+            t.x += u.x;
+            t.y += u.y;
+            t.z += u.z;
+            t.w += u.w;
+          }
+          os[j] = t.x;
+          oq[j] = t.y;
+          is[j] = t.z;
+          iq[j] = t.w;
+        }
+      }
+    }
+    if (lane_r == 0) {
+      const float k = UP ? 4.f : 1.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (out_part)
+          out_part[((int64_t)f * splits + sp) * out_ld + out_c0 + vb * 8 + j] = make_float2(k * os[j], k * oq[j]);
+        if (!UP && in_part) in_part[((int64_t)f * splits + sp) * in_ld + vb * 8 + j] = make_float2(is[j], iq[j]);
+      }
+    }
+  }
+}
+
+static sf_status launch_resample_gn(int up, sf_view_t x, sf_view_t y, int frames, int H, int W, int C, int splits,
+                                    void* out_part, int out_ld, int out_c0, void* in_part, int in_ld,
+                                    cudaStream_t st) {
+  const int nvec = C / 8;
+  const int rpi = nvec <= 256 ? 256 / nvec : 1;
+  const size_t smem = nvec <= 256 ? (size_t)rpi * C * sizeof(float4) : 0;
+  auto kern = up ? resample_gn_kernel<1> : resample_gn_kernel<0>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_k(kern, dim3((unsigned)splits, (unsigned)frames), dim3(nvec <= 256 ? rpi * nvec : 256), smem, st, x, y, H, W,
+           C, splits, (float2*)out_part, out_ld, out_c0, (float2*)in_part, in_ld);
+  return launch_status(up ? "sf_upsample2x_gn" : "sf_downsample2x_gn");
+}
+
 // ---------------------------------------------------------------------------
 // softmax rows: fp32 scores -> bf16 probabilities (kernels.py:272-276)
 // ---------------------------------------------------------------------------
@@ -1499,6 +1615,26 @@ sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int
   SF_CHECK_ARG(total < (1ll << 31), SF_ERR_SHAPE, "upsample input too large for 32-bit indexing");
   launch_k(upsample_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, frames, H, W, C);
   return launch_status("sf_upsample2x");
+}
+
+sf_status sf_downsample2x_gn(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C,
+                             int32_t splits, void* out_part, int32_t out_ld, void* in_part, int32_t in_ld,
+                             void* stream) {
+  SF_CHECK_ARG(H % 2 == 0 && W % 2 == 0, SF_ERR_SHAPE, "downsample2x needs even h, w");
+  SF_CHECK_ARG(frames >= 1 && C % 8 == 0 && view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "bad view");
+  SF_CHECK_ARG(splits >= 1 && splits <= (H / 2) * (W / 2), SF_ERR_PARAM, "1 <= splits <= output pixels");
+  SF_CHECK_ARG((!out_part || out_ld >= C) && (!in_part || in_ld >= C), SF_ERR_PARAM, "partial row too short");
+  return launch_resample_gn(0, x, y, frames, H, W, C, splits, out_part, out_ld, 0, in_part, in_ld,
+                            (cudaStream_t)stream);
+}
+
+sf_status sf_upsample2x_gn(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C, int32_t splits,
+                           void* out_part, int32_t out_ld, int32_t out_c0, void* stream) {
+  SF_CHECK_ARG(frames >= 1 && C % 8 == 0 && view_vec8_ok(x) && view_vec8_ok(y), SF_ERR_PARAM, "bad view");
+  SF_CHECK_ARG(splits >= 1 && splits <= H * W, SF_ERR_PARAM, "1 <= splits <= input pixels");
+  SF_CHECK_ARG(out_part && out_c0 >= 0 && out_ld >= out_c0 + C, SF_ERR_PARAM, "partial row too short");
+  return launch_resample_gn(1, x, y, frames, H, W, C, splits, out_part, out_ld, out_c0, nullptr, 0,
+                            (cudaStream_t)stream);
 }
 
 sf_status sf_softmax_rows(const float* s, int64_t lds, void* p, int64_t ldp, int64_t rows, int32_t n, void* stream) {

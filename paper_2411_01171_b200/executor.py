@@ -152,6 +152,8 @@ class Plan:
         self.emb_nodes: list[str] = []
         self.gn_feed: dict[str, str] = {}        # conv node id -> GroupNorm input value it produces
         self.gn_part: dict[str, tuple] = {}      # that value -> (partials tensor, splits per frame)
+        self.gn_roles: dict[str, list] = {}      # resampling op -> [(role, value, channel offset)]
+        self.gn_meta: dict[str, int] = {}        # value with handed-over statistics -> splits per frame
         self.exchanger = None
         self._analyse()
         self._layout()
@@ -194,13 +196,49 @@ class Plan:
             self._analyse_gn_feed()
 
     def _analyse_gn_feed(self):
-        """GroupNorms whose input is the stored output of a 3x3 conv (res.conv1 (+ step embedding)
-        -> res.norm2, unet.py:186-193): the conv's GEMM epilogue emits per-(frame, tile) partial
-        sums of exactly the values it stores, so the GroupNorm needs only the finalize."""
+        """GroupNorms whose statistics a producer kernel hands over as partial sums, so the
+        GroupNorm itself only runs the finalize (kernels.py:228-237 statistics):
+          * res.norm2 reads res.conv1's stored output (+ step embedding, unet.py:186-193): the
+            conv's GEMM epilogue sums the values it stores (``gn_feed``: conv id -> value);
+          * down_blocks.i+1.res.norm1 reads the downsample's output, and up_blocks.i.res.norm1 reads
+            concat(skip, upsample(x)) (unet.py:221-244): the downsample kernel sums its output and
+            the skip it reads, the upsample kernel the copies it writes (``gn_roles``: op id ->
+            [(role, value, channel offset)]).
+        Each value gets [frames][splits][C] float2 partials; ``gn_meta``: value -> splits."""
+        self.gn_roles: dict[str, list] = {}
+        self.gn_meta: dict[str, int] = {}
+        f0, f1 = self._frames()
+        nf = f1 - f0
+        sms = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148
+        down_of_input = {grp.head_input: grp.ops[0].id for grp in self.grouped.groups
+                         if len(grp.ops) == 1 and grp.ops[0].kind is OpKind.DOWNSAMPLE2X}
+        up_by_tail = {grp.tail: grp.ops[0].id for grp in self.grouped.groups
+                      if len(grp.ops) == 1 and grp.ops[0].kind is OpKind.UPSAMPLE2X}
+        down_by_tail = {grp.tail: grp.ops[0].id for grp in self.grouped.groups
+                        if len(grp.ops) == 1 and grp.ops[0].kind is OpKind.DOWNSAMPLE2X}
+
+        def resample_splits(v):
+            sh = self.shapes[v]
+            coarse = (sh.h // 2) * (sh.w // 2)
+            return max(1, min((2 * sms) // max(1, nf), -(-coarse // 64)))
         for grp in self.grouped.groups:
             if grp.domain is not Domain.SPATIAL or grp.ops[0].kind is not OpKind.GROUP_NORM:
                 continue
             v = grp.head_input
+            node = self.graph.nodes.get(v)
+            if v in down_by_tail:
+                self.gn_roles.setdefault(down_by_tail[v], []).append(("out", v, 0))
+                self.gn_meta[v] = resample_splits(v)
+                continue
+            if node is not None and node.kind is OpKind.CONCAT and len(node.inputs) == 2:
+                a, b = node.inputs
+                sa, sv = self.shapes[a], self.shapes[v]
+                if a in down_of_input and b in up_by_tail and (sa.h, sa.w) == (sv.h, sv.w) and sa.h % 2 == 0 \
+                        and sa.w % 2 == 0:
+                    self.gn_roles.setdefault(down_of_input[a], []).append(("in", v, 0))
+                    self.gn_roles.setdefault(up_by_tail[b], []).append(("out", v, sa.c))
+                    self.gn_meta[v] = resample_splits(v)
+                continue
             src = self.fused_adds[v][0] if v in self.fused_adds else v
             _, pg = self._producer_group(src)
             if pg is None or pg.domain is not Domain.SPATIAL:
@@ -213,20 +251,24 @@ class Plan:
             if self.shapes[conv.id] != self.shapes[v]:
                 continue
             self.gn_feed[conv.id] = v
-        # partial buffers: one slot per set of producer -> consumer intervals that do not overlap
-        # in the schedule (each norm2 group directly follows its conv1 group: one slot in the U-Net)
+            self.gn_meta[v] = int(N.query("sf_conv_gn_splits", self.shapes[v].h, self.shapes[v].w))
+        # partial buffers: one slot per set of first-producer -> consumer intervals that do not
+        # overlap in the schedule (norm2 follows conv1 directly; a concat's buffer lives from the
+        # down path's downsample to the up block)
         spos = {(k, r): i for i, (k, r) in enumerate(self.grouped.schedule)}
-
-        def gpos(vid):
-            gi, _ = self._producer_group(vid)
-            return spos[("group", gi)]
+        op_pos = {}
+        for gi, grp in enumerate(self.grouped.groups):
+            for o in grp.ops:
+                op_pos[o.id] = spos.get(("group", gi), -1)
         cons_pos = {grp.head_input: spos[("group", gi)] for gi, grp in enumerate(self.grouped.groups)}
-        f0, f1 = self._frames()
+        start = {v: op_pos[c] for c, v in self.gn_feed.items()}
+        for op_id, roles in self.gn_roles.items():
+            for _, v, _ in roles:
+                start[v] = min(start.get(v, op_pos[op_id]), op_pos[op_id])
         self._gn_slot_of, self._gn_slot_elems, free_after = {}, [], []
-        for conv_id, v in sorted(self.gn_feed.items(), key=lambda kv: gpos(kv[0])):
-            a, b = gpos(conv_id), cons_pos[v]
-            s = self.shapes[v]
-            elems = (f1 - f0) * int(N.query("sf_conv_gn_splits", s.h, s.w)) * s.c * 2
+        for v in sorted(start, key=lambda u: start[u]):
+            a, b = start[v], cons_pos[v]
+            elems = nf * self.gn_meta[v] * self.shapes[v].c * 2
             for k, fa in enumerate(free_after):
                 if fa < a:
                     break
@@ -240,14 +282,13 @@ class Plan:
         self._gn_slots: list[torch.Tensor | None] = [None] * len(self._gn_slot_elems)
 
     def gn_partials(self, vid):
-        """(partials buffer over this rank's frames, splits per frame) for a GroupNorm input fed
-        by a conv epilogue; the slot tensor is allocated when the first user compiles."""
+        """(partials buffer over this rank's frames, splits per frame) for a GroupNorm input whose
+        statistics a producer hands over; the slot tensor is allocated when the first user compiles."""
         if vid not in self.gn_part:
             k = self._gn_slot_of[vid]
             if self._gn_slots[k] is None:
                 self._gn_slots[k] = torch.empty((self._gn_slot_elems[k],), dtype=torch.float32, device=self.dev)
-            s = self.shapes[vid]
-            self.gn_part[vid] = (self._gn_slots[k], int(N.query("sf_conv_gn_splits", s.h, s.w)))
+            self.gn_part[vid] = (self._gn_slots[k], self.gn_meta[vid])
         return self.gn_part[vid]
 
     # ------------------------------------------------------------------ layout
@@ -797,8 +838,15 @@ class Plan:
         eps_out = self.fp32_out and tail == self.graph.outputs[0]
         # GroupNorm statistics handed over through conv-epilogue partials (_analyse_gn_feed)
         gn_out = self.gn_partials(self.gn_feed[tail]) if tail in self.gn_feed else None
-        gn_in = self.gn_partials(x_id) if x_id in self.gn_feed.values() else None
-        fr0 = self._frames()[0] if gn_out or gn_in else 0
+        gn_in = self.gn_partials(x_id) if x_id in self.gn_meta else None
+        # resampling ops that hand partials over: role -> (buffer, splits, row length, channel offset)
+        gn_rs = {o.id: {role: (*self.gn_partials(v), self.shapes[v].c, c0) for role, v, c0 in self.gn_roles[o.id]}
+                 for o in ops if o.id in self.gn_roles}
+        fr0 = self._frames()[0] if gn_out or gn_in or gn_rs else 0
+
+        def part_ptr(entry, f):
+            t, splits, ld, _ = entry
+            return t.data_ptr() + (f - fr0) * splits * ld * 8
 
         def run(st0):
             streams = self._fork(st0, ncopy)
@@ -864,8 +912,20 @@ class Plan:
                         D.linear(st, X, Y, nf, ihw, ish.c, osh.c, prm, epi, backend)
                     elif k is OpKind.SPATIAL_ATTENTION:
                         D.spatial_attention(st, X, Y, nf, ihw, ish.c, prm, epi, scratch, backend)
+                    elif k is OpKind.DOWNSAMPLE2X and o.id in gn_rs:
+                        r = gn_rs[o.id]
+                        eo, ei = r.get("out"), r.get("in")
+                        sp = (eo or ei)[1]
+                        assert ei is None or ei[1] == sp
+                        N.call("sf_downsample2x_gn", X.view(), Y.view(), nf, ish.h, ish.w, ish.c, sp,
+                               part_ptr(eo, sl[0]) if eo else None, eo[2] if eo else 0,
+                               part_ptr(ei, sl[0]) if ei else None, ei[2] if ei else 0, st)
                     elif k is OpKind.DOWNSAMPLE2X:
                         N.call("sf_downsample2x", X.view(), Y.view(), nf, ish.h, ish.w, ish.c, st)
+                    elif k is OpKind.UPSAMPLE2X and o.id in gn_rs:
+                        eo = gn_rs[o.id]["out"]
+                        N.call("sf_upsample2x_gn", X.view(), Y.view(), nf, ish.h, ish.w, ish.c, eo[1],
+                               part_ptr(eo, sl[0]), eo[2], eo[3], st)
                     elif k is OpKind.UPSAMPLE2X:
                         N.call("sf_upsample2x", X.view(), Y.view(), nf, ish.h, ish.w, ish.c, st)
                     else:
@@ -1054,7 +1114,7 @@ class _GroupPlan(Plan):
         self.pos = {n: i for i, n in enumerate(self.topo)}
         self.cons = graph.consumers()
         self.values, self.fused_adds, self.epilogue_of, self.units, self.emb_nodes = {}, {}, {}, [], []
-        self.gn_feed, self.gn_part = {}, {}     # one group: no statistics handed across groups
+        self.gn_feed, self.gn_part, self.gn_roles, self.gn_meta = {}, {}, {}, {}   # one group: no hand-over
         self.exchanger = None
         so = self.shapes[group.tail]
         self.inp = torch.empty(in_shape.rows, in_shape.c, dtype=torch.bfloat16, device=self.dev)
@@ -1153,14 +1213,15 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     plan.pos = {n: i for i, n in enumerate(plan.topo)}
     plan.cons = graph.consumers()
     plan.values, plan.fused_adds, plan.epilogue_of, plan.units, plan.emb_nodes = {}, {}, {}, [], []
-    plan.gn_feed, plan.gn_part = {}, {}
+    plan.gn_feed, plan.gn_part, plan.gn_roles, plan.gn_meta = {}, {}, {}, {}
     plan.exchanger = None
     plan._analyse()
     plan._layout()
     led = plan.memory_ledger()
     out = {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers), "ledger": led,
            "ledger_peak_bytes": led.peak_bytes,
-           "gn_partial_bytes": 4 * sum(getattr(plan, "_gn_slot_elems", [])), "gn_from_conv": len(plan.gn_feed)}
+           "gn_partial_bytes": 4 * sum(getattr(plan, "_gn_slot_elems", [])), "gn_from_conv": len(plan.gn_feed),
+           "gn_handed_over": len(plan.gn_meta)}
     if plan.cfg.world > 1:
         from .parallel import exchange_schedule
         ex = exchange_schedule(plan)

@@ -132,10 +132,10 @@ def test_plan_uses_conv_partials_and_matches_stats_path():
     sched = StepSchedule([0, 1, 2], 3)
     d1 = Denoiser(cfg, ExecConfig(gn_from_conv=True))
     a = d1.run(x0, sched)
-    assert len(d1.plan.gn_feed) == 9
+    assert len(d1.plan.gn_feed) == 9 and len(d1.plan.gn_meta) == 15   # + 3 downsamples, 3 concats
     d2 = Denoiser(cfg, ExecConfig(gn_from_conv=False), device_weights=d1.model.dw)
     b = d2.run(x0, sched)
-    assert not d2.plan.gn_feed
+    assert not d2.plan.gn_feed and not d2.plan.gn_meta
     assert np.abs(a - b).max() / np.abs(b).max() < 2e-3
     # ragged frame slices on two streams: the partial buffer is indexed by frame, so every slice
     # finalises its own frames (the conv partials do not depend on the slicing)
@@ -146,3 +146,54 @@ def test_plan_uses_conv_partials_and_matches_stats_path():
     d4 = Denoiser(cfg, ExecConfig(gn_from_conv=True, spatial_k=3, temporal_k=2, slice_streams=1),
                   device_weights=d1.model.dw)
     assert np.array_equal(c, d4.run(x0, sched))
+
+
+@pytest.mark.parametrize("F_,H,W,C,splits", [(3, 72, 128, 320, 11), (5, 36, 64, 640, 9), (4, 18, 32, 1280, 3),
+                                             (2, 16, 16, 8, 2), (25, 18, 32, 2560, 3)])
+def test_downsample_partials(F_, H, W, C, splits):
+    """sf_downsample2x_gn: the same pooled output as sf_downsample2x, bit for bit; partials of the stored
+    output and of the input (the skip it reads, written at channel offset 0 of a wider concat row)."""
+    torch.manual_seed(7)
+    st = torch.cuda.current_stream().cuda_stream
+    x = (torch.randn(F_ * H * W, C, device=dev) * 2 + 0.5).to(torch.bfloat16)
+    y0 = torch.empty(F_ * (H // 2) * (W // 2), C, dtype=torch.bfloat16, device=dev)
+    y1 = torch.empty_like(y0)
+    ld_in = C + 24
+    po = torch.full((F_, splits, C, 2), float("nan"), device=dev)
+    pi = torch.full((F_, splits, ld_in, 2), float("nan"), device=dev)
+    N.call("sf_downsample2x", Rows(x, 0, H * W).view(), Rows(y0, 0, H * W // 4).view(), F_, H, W, C, st)
+    N.call("sf_downsample2x_gn", Rows(x, 0, H * W).view(), Rows(y1, 0, H * W // 4).view(), F_, H, W, C, splits,
+           po.data_ptr(), C, pi.data_ptr(), ld_in, st)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    assert not torch.isnan(po).any() and not torch.isnan(pi[:, :, :C]).any()
+    assert torch.isnan(pi[:, :, C:]).all(), "only the skip's channel range is written"
+    yd = y1.double().view(F_, -1, C)
+    xd = x.double().view(F_, -1, C)
+    assert torch.allclose(po.double().sum(1)[..., 0], yd.sum(1), rtol=1e-5, atol=1e-3)
+    assert torch.allclose(po.double().sum(1)[..., 1], (yd * yd).sum(1), rtol=1e-5, atol=1e-3)
+    assert torch.allclose(pi[:, :, :C].double().sum(1)[..., 0], xd.sum(1), rtol=1e-5, atol=1e-3)
+    assert torch.allclose(pi[:, :, :C].double().sum(1)[..., 1], (xd * xd).sum(1), rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("F_,H,W,C,splits,c0", [(3, 36, 64, 640, 11, 320), (4, 9, 16, 1280, 3, 1280),
+                                                (2, 8, 8, 8, 2, 16)])
+def test_upsample_partials(F_, H, W, C, splits, c0):
+    """sf_upsample2x_gn: the same nearest-neighbour copies as sf_upsample2x; partials = the written
+    copies' sums (4 x the input's), at channel offset c0 of the concat row."""
+    torch.manual_seed(8)
+    st = torch.cuda.current_stream().cuda_stream
+    x = (torch.randn(F_ * H * W, C, device=dev) - 0.3).to(torch.bfloat16)
+    y0 = torch.empty(F_ * 4 * H * W, C, dtype=torch.bfloat16, device=dev)
+    y1 = torch.empty_like(y0)
+    ld = c0 + C
+    pp = torch.full((F_, splits, ld, 2), float("nan"), device=dev)
+    N.call("sf_upsample2x", Rows(x, 0, H * W).view(), Rows(y0, 0, 4 * H * W).view(), F_, H, W, C, st)
+    N.call("sf_upsample2x_gn", Rows(x, 0, H * W).view(), Rows(y1, 0, 4 * H * W).view(), F_, H, W, C, splits,
+           pp.data_ptr(), ld, c0, st)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    assert torch.isnan(pp[:, :, :c0]).all() and not torch.isnan(pp[:, :, c0:]).any()
+    yd = y1.double().view(F_, -1, C)
+    assert torch.allclose(pp[:, :, c0:].double().sum(1)[..., 0], yd.sum(1), rtol=1e-5, atol=1e-3)
+    assert torch.allclose(pp[:, :, c0:].double().sum(1)[..., 1], (yd * yd).sum(1), rtol=1e-5, atol=1e-3)
