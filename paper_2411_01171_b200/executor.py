@@ -217,9 +217,9 @@ class Plan:
         down_by_tail = {grp.tail: grp.ops[0].id for grp in self.grouped.groups
                         if len(grp.ops) == 1 and grp.ops[0].kind is OpKind.DOWNSAMPLE2X}
 
-        def resample_splits(v):
-            sh = self.shapes[v]
-            coarse = (sh.h // 2) * (sh.w // 2)
+        def resample_splits(coarse):
+            # splits over the coarse grid (the downsample's outputs = the upsample's inputs): the same
+            # count for both producers of a concat's partials
             return max(1, min((2 * sms) // max(1, nf), -(-coarse // 64)))
         for grp in self.grouped.groups:
             if grp.domain is not Domain.SPATIAL or grp.ops[0].kind is not OpKind.GROUP_NORM:
@@ -228,7 +228,7 @@ class Plan:
             node = self.graph.nodes.get(v)
             if v in down_by_tail:
                 self.gn_roles.setdefault(down_by_tail[v], []).append(("out", v, 0))
-                self.gn_meta[v] = resample_splits(v)
+                self.gn_meta[v] = resample_splits(self.shapes[v].h * self.shapes[v].w)
                 continue
             if node is not None and node.kind is OpKind.CONCAT and len(node.inputs) == 2:
                 a, b = node.inputs
@@ -237,7 +237,7 @@ class Plan:
                         and sa.w % 2 == 0:
                     self.gn_roles.setdefault(down_of_input[a], []).append(("in", v, 0))
                     self.gn_roles.setdefault(up_by_tail[b], []).append(("out", v, sa.c))
-                    self.gn_meta[v] = resample_splits(v)
+                    self.gn_meta[v] = resample_splits((sv.h // 2) * (sv.w // 2))
                 continue
             src = self.fused_adds[v][0] if v in self.fused_adds else v
             _, pg = self._producer_group(src)
@@ -916,7 +916,8 @@ class Plan:
                         r = gn_rs[o.id]
                         eo, ei = r.get("out"), r.get("in")
                         sp = (eo or ei)[1]
-                        assert ei is None or ei[1] == sp
+                        if ei is not None and ei[1] != sp:
+                            raise InvalidParam(f"{o.id}: output / skip partials need one split count")
                         N.call("sf_downsample2x_gn", X.view(), Y.view(), nf, ish.h, ish.w, ish.c, sp,
                                part_ptr(eo, sl[0]) if eo else None, eo[2] if eo else 0,
                                part_ptr(ei, sl[0]) if ei else None, ei[2] if ei else 0, st)
