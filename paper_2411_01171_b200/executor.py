@@ -252,6 +252,10 @@ class Plan:
                 continue
             self.gn_feed[conv.id] = v
             self.gn_meta[v] = int(N.query("sf_conv_gn_splits", self.shapes[v].h, self.shapes[v].w))
+        for op_id, roles in self.gn_roles.items():
+            if len({self.gn_meta[v] for _, v, _ in roles}) != 1:
+                raise InvalidParam(f"{op_id}: its GroupNorm partials need one split count, got "
+                                   f"{[(r, v, self.gn_meta[v]) for r, v, _ in roles]}")
         # partial buffers: one slot per set of first-producer -> consumer intervals that do not
         # overlap in the schedule (norm2 follows conv1 directly; a concat's buffer lives from the
         # down path's downsample to the up block)
@@ -1207,6 +1211,7 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     plan = Plan.__new__(Plan)
     plan.graph, plan.grouped, plan.dw = graph, grouped, dw
     plan.cfg = ExecConfig(spatial_k=cfg.spatial_k, temporal_k=cfg.temporal_k, scratch_budget=cfg.scratch_budget,
+                          gn_from_conv=cfg.gn_from_conv,
                           device="meta", rank=cfg.rank, world=cfg.world)
     plan.dev = dw.dev
     plan.shapes = infer_shapes(graph)
