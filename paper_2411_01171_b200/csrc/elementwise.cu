@@ -634,40 +634,72 @@ __global__ void __launch_bounds__(256) resample_gn_kernel(sf_view_t x, sf_view_t
 #pragma unroll
     for (int j = 0; j < 8; ++j) os[j] = oq[j] = is[j] = iq[j] = 0.f;
     if (active) {
-      for (int pc = p0 + lane_r; pc < p1; pc += rpi) {
-        const int xc = pc % Wc, yc = pc / Wc;
+      // U coarse pixels per iteration, all loads issued before the math (memory-level parallelism:
+      // a block walks only its split's pixels)
+      constexpr int U = UP ? 4 : 2;
+      for (int pc0 = p0 + lane_r; pc0 < p1; pc0 += U * rpi) {
         if (UP) {
-          const bf16x8 val = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (int64_t)yc * W + xc) + vb * 8);
-          const int64_t o = (int64_t)(2 * yc) * (2 * W) + 2 * xc;
-          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o) + vb * 8) = val;
-          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 1) + vb * 8) = val;
-          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 2 * W) + vb * 8) = val;
-          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 2 * W + 1) + vb * 8) = val;
-          float v[8];
-          unpack8(val, v);
+          bf16x8 val[U];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            os[j] += v[j];
-            oq[j] = fmaf(v[j], v[j], oq[j]);
+          for (int u = 0; u < U; ++u) {
+            const int pc = pc0 + u * rpi;
+            if (pc < p1)
+              val[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (int64_t)(pc / Wc) * W + pc % Wc) +
+                                                        vb * 8);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int pc = pc0 + u * rpi;
+            if (pc >= p1) break;
+            const int xc = pc % Wc, yc = pc / Wc;
+            const int64_t o = (int64_t)(2 * yc) * (2 * W) + 2 * xc;
+            *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o) + vb * 8) = val[u];
+            *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 1) + vb * 8) = val[u];
+            *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 2 * W) + vb * 8) = val[u];
+            *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, o + 2 * W + 1) + vb * 8) = val[u];
+            float v[8];
+            unpack8(val[u], v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              os[j] += v[j];
+              oq[j] = fmaf(v[j], v[j], oq[j]);
+            }
           }
         } else {
-          float a[8], b[8], c[8], d[8], r[8];
-          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc) * W + 2 * xc) + vb * 8), a);
-          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc) * W + 2 * xc + 1) + vb * 8), b);
-          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc + 1) * W + 2 * xc) + vb * 8), c);
-          unpack8(*reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, (2 * yc + 1) * W + 2 * xc + 1) + vb * 8),
-                  d);
+          bf16x8 q[U][4];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) r[j] = (((a[j] + b[j]) + c[j]) + d[j]) * 0.25f;
-          const bf16x8 pk = pack8(r);
-          *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, (int64_t)yc * Wc + xc) + vb * 8) = pk;
-          unpack8(pk, r);   // the statistics of what is stored
+          for (int u = 0; u < U; ++u) {
+            const int pc = pc0 + u * rpi;
+            if (pc < p1) {
+              const int xc = pc % Wc, yc = pc / Wc;
+              const int64_t i0 = (int64_t)(2 * yc) * W + 2 * xc;
+              q[u][0] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, i0) + vb * 8);
+              q[u][1] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, i0 + 1) + vb * 8);
+              q[u][2] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, i0 + W) + vb * 8);
+              q[u][3] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, i0 + W + 1) + vb * 8);
+            }
+          }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            os[j] += r[j];
-            oq[j] = fmaf(r[j], r[j], oq[j]);
-            is[j] += ((a[j] + b[j]) + c[j]) + d[j];
-            iq[j] += ((a[j] * a[j] + b[j] * b[j]) + c[j] * c[j]) + d[j] * d[j];
+          for (int u = 0; u < U; ++u) {
+            const int pc = pc0 + u * rpi;
+            if (pc >= p1) break;
+            float a[8], b[8], c[8], d[8], r[8];
+            unpack8(q[u][0], a);
+            unpack8(q[u][1], b);
+            unpack8(q[u][2], c);
+            unpack8(q[u][3], d);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = (((a[j] + b[j]) + c[j]) + d[j]) * 0.25f;
+            const bf16x8 pk = pack8(r);
+            *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, (int64_t)(pc / Wc) * Wc + pc % Wc) + vb * 8) = pk;
+            unpack8(pk, r);   // the statistics of what is stored
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              os[j] += r[j];
+              oq[j] = fmaf(r[j], r[j], oq[j]);
+              is[j] += ((a[j] + b[j]) + c[j]) + d[j];
+              iq[j] += ((a[j] * a[j] + b[j] * b[j]) + c[j] * c[j]) + d[j] * d[j];
+            }
           }
         }
       }

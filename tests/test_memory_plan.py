@@ -43,6 +43,6 @@ def test_groupnorm_statistics_hand_over(name):
     gg = group_operators(g, cfg.frames, default_temporal_config(cfg.height, cfg.width))
     m = plan_memory(g, gg, ExecConfig())
     assert m["gn_from_conv"] == 9 and m["gn_handed_over"] == 15
-    assert 0 < m["gn_partial_bytes"] < 0.05 * m["arena_bytes"]
+    assert 0 < m["gn_partial_bytes"] < max(0.06 * m["arena_bytes"], 1 << 20)
     off = plan_memory(g, gg, ExecConfig(gn_from_conv=False))
     assert off["gn_handed_over"] == 0 and off["gn_partial_bytes"] == 0
