@@ -219,8 +219,9 @@ class Plan:
 
         def resample_splits(coarse):
             # splits over the coarse grid (the downsample's outputs = the upsample's inputs): the same
-            # count for both producers of a concat's partials; ~4 blocks per SM over the frames
-            return max(1, min((4 * sms) // max(1, nf), coarse, 16))
+            # count for both producers of a concat's partials; frames x splits <= 2 blocks per SM (the
+            # downsample kernel holds 127 registers x 240 threads: two blocks per SM, one wave)
+            return max(1, min((2 * sms) // max(1, nf), coarse, 16))
         for grp in self.grouped.groups:
             if grp.domain is not Domain.SPATIAL or grp.ops[0].kind is not OpKind.GROUP_NORM:
                 continue
