@@ -138,6 +138,12 @@ sf_status sf_conv_gn_partials(sf_view_t y, int32_t frames, int32_t H, int32_t W,
  * fp64 fixed-order combine; n_inner = rows per frame. */
 sf_status sf_group_norm_finalize(const void* partial, int32_t frames, int32_t splits, int32_t n_inner, int32_t C,
                                  int32_t groups, float eps, float* mean, float* rstd, void* stream);
+/* out[r][n] = sum_c act(GN(x))[r][c] * w[n][c] (w bf16 [N][C], N even <= 48, fp32 out rows of ldo):
+ * the GroupNorm apply (+ SiLU) fused into a narrow projection -- the per-tap projection of the
+ * network's out_conv (kernels.py:228-253 then 181-201), so the normalised tensor never reaches HBM. */
+sf_status sf_group_norm_project(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
+                                const float* mean, const float* rstd, const float* gamma, const float* beta,
+                                int32_t act, const void* w, int32_t N, float* out, int64_t ldo, void* stream);
 /* y = act((x - mean) * rstd * gamma + beta), per (frame, group) stats. */
 sf_status sf_group_norm_apply(sf_view_t x, sf_view_t y, int32_t frames, int32_t n_inner, int32_t C,
                               int32_t groups, const float* mean, const float* rstd, const float* gamma,

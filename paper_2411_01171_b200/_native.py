@@ -58,6 +58,7 @@ _PROTOS = {
     "sf_conv_gn_splits": [i32, i32],
     "sf_conv_gn_partials": [View, i32, i32, i32, i32, vp, vp],
     "sf_group_norm_finalize": [vp, i32, i32, i32, i32, i32, f32, vp, vp, vp],
+    "sf_group_norm_project": [View, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp, i32, vp, i64, vp],
     "sf_group_norm_apply": [View, View, i32, i32, i32, i32, vp, vp, vp, vp, i32, vp],
     "sf_layer_norm": [View, View, i32, i32, i32, vp, vp, f32, i32, vp],
     "sf_layer_norm_stats": [View, i32, i32, i32, f32, vp, vp],

@@ -916,6 +916,127 @@ __device__ __forceinline__ unsigned pack_bf2(float a, float b) {
   return *reinterpret_cast<unsigned*>(&h);
 }
 
+// ---------------------------------------------------------------------------
+// GroupNorm-apply + SiLU fused into a narrow projection (the network's out_norm -> out_conv,
+// kernels.py:228-253 then 181-201 regrouped per tap: Y[p][n] = sum_c SiLU(GN(x))[p][c] W[n][c],
+// n = tap * cout + co).  The normalised activations never reach HBM: each warp loads 16 rows of x,
+// applies y = SiLU(x * ss + bb) (ss = rstd * gamma, bb = beta - mean * ss: gn_apply_kernel's exact
+// arithmetic, rounded to bf16 as that kernel stores it) into its shared-memory A tile, and multiplies
+// it with the resident W (bf16 [48][C]) on mma.sync m16n8k16; fp32 out.  Each element is
+// transformed once (the per-tap projection reads every pixel once, unlike a 3x3 implicit GEMM).
+// ---------------------------------------------------------------------------
+constexpr int GP_WARPS = 4, GP_NP = 48;   // output columns padded to 6 n-tiles of 8
+__global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
+    sf_view_t x, int frames, int n_inner, int C, int groups, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta, int act,
+    const bf16* __restrict__ w, int N, float* __restrict__ out, int64_t ldo) {
+  griddep_wait();
+  extern __shared__ __align__(16) uint8_t gp_raw[];
+  const int LD = C + 8;   // +16 B per row: conflict-free ldmatrix
+  bf16* sW = reinterpret_cast<bf16*>(gp_raw);              // [GP_NP][LD]
+  bf16* sA = sW + GP_NP * LD;                              // [GP_WARPS][16][LD]
+  for (int i = threadIdx.x; i < GP_NP * (C / 8); i += blockDim.x) {
+    const int n = i / (C / 8), v = i % (C / 8);
+    *reinterpret_cast<bf16x8*>(sW + n * LD + v * 8) =
+        n < N ? *reinterpret_cast<const bf16x8*>(w + (int64_t)n * C + v * 8) : bf16x8{make_uint4(0, 0, 0, 0)};
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bf16* a = sA + warp * 16 * LD;
+  const int cg = C / groups, nvec = C / 8;
+  const int64_t rows = (int64_t)frames * n_inner;
+  const int64_t ntiles = (rows + 15) / 16;
+  for (int64_t t = (int64_t)blockIdx.x * GP_WARPS + warp; t < ntiles; t += (int64_t)gridDim.x * GP_WARPS) {
+    const int64_t r0 = t * 16;
+    // 16 rows x nvec vectors: load all, then transform into the A tile
+    for (int i0 = 0; i0 < 16 * nvec; i0 += 32 * 8) {
+      bf16x8 in[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * 32 + lane;
+        const int64_t r = r0 + i / nvec;
+        if (i < 16 * nvec && r < rows) {
+          const int f = (int)(r / n_inner);
+          in[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, r - (int64_t)f * n_inner) + (i % nvec) * 8);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * 32 + lane;
+        if (i >= 16 * nvec) break;
+        const int64_t r = r0 + i / nvec;
+        const int v = i % nvec;
+        float fv[8];
+        if (r < rows) {
+          const int f = (int)(r / n_inner);
+          unpack8(in[u], fv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = v * 8 + j, g = c / cg;
+            const float ss = __ldg(rstd + f * groups + g) * __ldg(gamma + c);
+            const float bb = fmaf(-__ldg(mean + f * groups + g), ss, __ldg(beta + c));
+            const float tv = fmaf(fv[j], ss, bb);
+            fv[j] = act ? silu_f(tv) : tv;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) fv[j] = 0.f;
+        }
+        *reinterpret_cast<bf16x8*>(a + (i / nvec) * LD + v * 8) = pack8(fv);
+      }
+    }
+    __syncwarp();
+    float acc[GP_NP / 8][4];
+#pragma unroll
+    for (int j = 0; j < GP_NP / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    for (int kk = 0; kk < C; kk += 16) {
+      unsigned af[4];
+      tq_ldsm_x4(af, a + (lane & 15) * LD + kk + (lane >> 4) * 8);
+#pragma unroll
+      for (int j = 0; j < GP_NP / 8; j += 2) {
+        unsigned b[4];
+        const int nrow = j * 8 + (lane & 7) + ((lane >> 4) << 3);
+        tq_ldsm_x4(b, sW + nrow * LD + kk + ((lane >> 3) & 1) * 8);
+        tq_mma(acc[j], af, b[0], b[1]);
+        tq_mma(acc[j + 1], af, b[2], b[3]);
+      }
+    }
+    const int64_t ra = r0 + (lane >> 2), rb = ra + 8;
+#pragma unroll
+    for (int j = 0; j < GP_NP / 8; ++j) {
+      const int c = j * 8 + (lane & 3) * 2;
+      if (c < N) {   // N even: the pair (c, c + 1) is in range together
+        if (ra < rows) *reinterpret_cast<float2*>(out + ra * ldo + c) = make_float2(acc[j][0], acc[j][1]);
+        if (rb < rows) *reinterpret_cast<float2*>(out + rb * ldo + c) = make_float2(acc[j][2], acc[j][3]);
+      }
+    }
+    __syncwarp();   // the A tile is rewritten by the next tile
+  }
+}
+
+sf_status gn_project_launch(sf_view_t x, int frames, int n_inner, int C, int groups, const float* mean,
+                            const float* rstd, const float* gamma, const float* beta, int act, const void* w, int N,
+                            float* out, int64_t ldo, cudaStream_t st) {
+  const size_t smem = (size_t)(GP_NP + GP_WARPS * 16) * (C + 8) * sizeof(bf16);
+  static size_t set = 48 * 1024;
+  if (smem > set) {
+    cudaFuncSetAttribute(gn_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_project_kernel, GP_WARPS * 32, smem);
+    if (occ < 1) occ = 1;
+  }
+  const int64_t tiles = ((int64_t)frames * n_inner + 15) / 16;
+  int64_t grid = (int64_t)num_sms() * occ;
+  const int64_t most = (tiles + GP_WARPS - 1) / GP_WARPS;
+  if (grid > most) grid = most;
+  launch_k(gn_project_kernel, dim3((unsigned)grid), dim3(GP_WARPS * 32), smem, st, x, frames, n_inner, C, groups, mean,
+           rstd, gamma, beta, act, (const bf16*)w, N, out, ldo);
+  return launch_status("sf_group_norm_project");
+}
+
 // copy a [32 tokens][64 ch] chunk (columns col0..col0+63) into smem, zero rows t >= T / ch >= C
 __device__ __forceinline__ void tq_load(bf16 (*dst)[TQ_LD], const sf_view_t& v, int b, int T, int pix, int col0,
                                         int cvalid, int lane) {
@@ -1647,6 +1768,20 @@ sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int
   SF_CHECK_ARG(total < (1ll << 31), SF_ERR_SHAPE, "upsample input too large for 32-bit indexing");
   launch_k(upsample_kernel, dim3(ew_grid(total, 256)), dim3(256), 0, (cudaStream_t)stream, x, y, frames, H, W, C);
   return launch_status("sf_upsample2x");
+}
+
+sf_status sf_group_norm_project(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
+                                const float* mean, const float* rstd, const float* gamma, const float* beta,
+                                int32_t act, const void* w, int32_t N, float* out, int64_t ldo, void* stream) {
+  SF_CHECK_ARG(frames >= 1 && n_inner >= 1 && C >= 16 && C % 16 == 0 && C <= 1024, SF_ERR_SHAPE,
+               "C must be a multiple of 16 in [16, 1024]");
+  SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
+  SF_CHECK_ARG(N >= 2 && N <= GP_NP && N % 2 == 0 && ldo >= N && ldo % 2 == 0, SF_ERR_SHAPE,
+               "N must be even, <= 48, and fit the output rows");
+  SF_CHECK_ARG(view_vec8_ok(x) && aligned16(w) && ((uintptr_t)out & 7) == 0 && mean && rstd && gamma && beta,
+               SF_ERR_PARAM, "unaligned or null operand");
+  return gn_project_launch(x, frames, n_inner, C, groups, mean, rstd, gamma, beta, act, w, N, out, ldo,
+                           (cudaStream_t)stream);
 }
 
 sf_status sf_downsample2x_gn(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int32_t W, int32_t C,

@@ -807,6 +807,18 @@ class Plan:
                 pf_specs["taps_y"] = (out_shape.h * out_shape.w, 9 * out_shape.c, torch.float32)
             shape = out_shape
             i += 2 if fuse_act else 1
+        # GroupNorm (+ SiLU) -> per-tap out_conv projection: the apply runs inside the projection
+        # (sf_group_norm_project), so the normalised tensor is neither written nor scratch
+        gn_project = {}
+        eps_tail = self.fp32_out and tail == self.graph.outputs[0]
+        for a_, b_ in zip(steps, steps[1:]):
+            (go, gsrc, gdst, gsh, _, gact, _), (co, csrc, _, csh, cosh, cact, clast) = a_, b_
+            if (go.kind is OpKind.GROUP_NORM and co.kind is OpKind.CONV2D and csrc == gdst and clast and eps_tail
+                    and "w_taps" in self.dw.p.get(co.id, {}) and not cact and tail not in self.epilogue_of
+                    and gsh.c % 16 == 0 and gsh.c <= 1024 and 9 * cosh.c <= 48
+                    and os.environ.get("SF_GN_PROJECT") != "0"):
+                gn_project[co.id] = (go, gsrc, gact)
+                pf_specs.pop(gdst, None)
         # exact per-frame slice scratch of this chain -> slice count under the budget
         per_frame = sum(r * c * torch.empty((), dtype=dt).element_size() for r, c, dt in pf_specs.values())
         from .parallel import shard_range
@@ -862,12 +874,15 @@ class Plan:
         def one_slice(sl, scratch, st):
             if True:
                 nf = sl[1] - sl[0]
+                gn_stats_of = {}
 
                 def loc(name, shp):
                     if name == "IN":
                         return vrows(x_id, sl)
                     if name == "OUT":
                         return vrows(tail, sl)
+                    if name not in scratch:
+                        return None    # the GroupNorm output a fused projection never materialises
                     return Rows(scratch[name], 0, shp.h * shp.w)
                 for (o, src, dst, ish, osh, act, last) in steps:
                     prm = self.dw.p.get(o.id)
@@ -883,17 +898,29 @@ class Plan:
                         stats = scratch["gn_stats"]
                         mean = stats[:nf * groups, 0]
                         rstd = stats[fmax * max_groups: fmax * max_groups + nf * groups, 0]
+                        gn_stats_of[o.id] = (mean, rstd)
                         eps = float(o.attrs.get("eps", 1e-5))
                         if src == "IN" and gn_in is not None:
                             N.call("sf_group_norm_finalize", gn_in[0].data_ptr() + (sl[0] - fr0) * gn_in[1] * ish.c * 8,
                                    nf, gn_in[1], ihw, ish.c, groups, eps, mean.data_ptr(), rstd.data_ptr(), st)
                         else:
                             D.group_norm_stats(st, X, nf, ihw, ish.c, groups, eps, scratch["gn_work"], mean, rstd)
-                        D.group_norm_apply(st, X, Y, nf, ihw, ish.c, groups, mean, rstd, prm, act)
+                        if not any(g[0] is o for g in gn_project.values()):
+                            D.group_norm_apply(st, X, Y, nf, ihw, ish.c, groups, mean, rstd, prm, act)
                     elif k is OpKind.LAYER_NORM:
                         D.layer_norm(st, X, Y, nf, ihw, ish.c, prm, float(o.attrs.get("eps", 1e-5)), act)
                     elif k is OpKind.SILU:
                         N.call("sf_silu", X.view(), Y.view(), nf, ihw, ish.c, st)
+                    elif k is OpKind.CONV2D and o.id in gn_project:
+                        go, gsrc, gact = gn_project[o.id]
+                        gp, gx = self.dw.p[go.id], loc(gsrc, ish)
+                        mean, rstd = gn_stats_of[go.id]
+                        ybuf = scratch["taps_y"]
+                        N.call("sf_group_norm_project", gx.view(), nf, ihw, ish.c, int(go.attrs.get("groups", 1)),
+                               mean.data_ptr(), rstd.data_ptr(), gp["gamma"].data_ptr(), gp["beta"].data_ptr(), gact,
+                               prm["w_taps"].data_ptr(), 9 * osh.c, ybuf.data_ptr(), ybuf.stride(0), st)
+                        N.call("sf_conv3x3_tapsum", ybuf.data_ptr(), ybuf.stride(0), nf, osh.h, osh.w, osh.c,
+                               prm["bias"].data_ptr(), self.srows(tail, sl[0]).view(), st)
                     elif k is OpKind.CONV2D:
                         if latent_in and src == "IN":
                             lat = self.latent[sl[0] * ihw:]

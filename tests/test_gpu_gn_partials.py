@@ -197,3 +197,51 @@ def test_upsample_partials(F_, H, W, C, splits, c0):
     yd = y1.double().view(F_, -1, C)
     assert torch.allclose(pp[:, :, c0:].double().sum(1)[..., 0], yd.sum(1), rtol=1e-5, atol=1e-3)
     assert torch.allclose(pp[:, :, c0:].double().sum(1)[..., 1], (yd * yd).sum(1), rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("F_,HW,C,groups,N", [(3, 9216, 320, 32, 36), (2, 1000, 64, 8, 36), (4, 257, 128, 32, 48),
+                                              (1, 16, 16, 4, 2)])
+def test_group_norm_project(F_, HW, C, groups, N):
+    """sf_group_norm_project == the GroupNorm apply (+ SiLU, bf16 as stored) followed by an fp32 projection."""
+    torch.manual_seed(9)
+    st = torch.cuda.current_stream().cuda_stream
+    x = (torch.randn(F_ * HW, C, device=dev) * 1.5 + 0.2).to(torch.bfloat16)
+    gamma = torch.rand(C, device=dev) + 0.5
+    beta = torch.randn(C, device=dev) * 0.1
+    w = rnd(N, C, scale=C ** -0.5)
+    mean = torch.empty(F_ * groups, device=dev)
+    rstd = torch.empty_like(mean)
+    work = torch.empty((N.query("sf_group_norm_workspace", F_, HW, C) + 3) // 4 + 1, device=dev)
+    N.call("sf_group_norm_stats", Rows(x, 0, HW).view(), F_, HW, C, groups, 1e-5, work.data_ptr(), mean.data_ptr(),
+           rstd.data_ptr(), st)
+    y = torch.empty_like(x)
+    N.call("sf_group_norm_apply", Rows(x, 0, HW).view(), Rows(y, 0, HW).view(), F_, HW, C, groups, mean.data_ptr(),
+           rstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), N.ACT_SILU, st)
+    ldo = N + 4
+    out = torch.full((F_ * HW, ldo), float("nan"), device=dev)
+    N.call("sf_group_norm_project", Rows(x, 0, HW).view(), F_, HW, C, groups, mean.data_ptr(), rstd.data_ptr(),
+           gamma.data_ptr(), beta.data_ptr(), N.ACT_SILU, w.data_ptr(), N, out.data_ptr(), ldo, st)
+    torch.cuda.synchronize()
+    ref = y.double() @ w.double().T
+    got = out[:, :N].double()
+    assert torch.isnan(out[:, N:]).all(), "columns past N untouched"
+    assert float((got - ref).abs().max() / ref.abs().max()) < 1e-5
+
+
+def test_out_norm_projection_in_plan(monkeypatch):
+    """The plan runs out_norm -> out_conv as statistics + sf_group_norm_project + tap sum (no normalised
+    tensor); the network output equals the unfused lowering's within fp32 accumulation-order noise."""
+    from paper_2411_01171_b200.executor import ExecConfig
+    from paper_2411_01171_b200.harness import Denoiser, initial_latent
+    from paper_2411_01171_b200.rehash import StepSchedule
+    from paper_2411_01171_b200.unet import UNetConfig
+    cfg = UNetConfig(channels=4, frames=4, height=16, width=16, base_channels=64, norm_groups=8, steps=3)
+    x0 = initial_latent(cfg)
+    sched = StepSchedule([0, 1, 2], 3)
+    d1 = Denoiser(cfg, ExecConfig())
+    a = d1.run(x0, sched)
+    monkeypatch.setenv("SF_GN_PROJECT", "0")
+    d2 = Denoiser(cfg, ExecConfig(), device_weights=d1.model.dw)
+    b = d2.run(x0, sched)
+    assert d1.launches[d1._key(sched, False)] < d2.launches[d2._key(sched, False)]
+    assert np.abs(a - b).max() / np.abs(b).max() < 1e-4
