@@ -935,6 +935,7 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
   const int LD = C + 8;   // +16 B per row: conflict-free ldmatrix
   bf16* sW = reinterpret_cast<bf16*>(gp_raw);              // [GP_NP][LD]
   bf16* sA = sW + GP_NP * LD;                              // [GP_WARPS][16][LD]
+  float2* sT = reinterpret_cast<float2*>(sA + GP_WARPS * 16 * LD);   // [GP_WARPS][2][C] (scale, shift)
   for (int i = threadIdx.x; i < GP_NP * (C / 8); i += blockDim.x) {
     const int n = i / (C / 8), v = i % (C / 8);
     *reinterpret_cast<bf16x8*>(sW + n * LD + v * 8) =
@@ -943,12 +944,31 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bf16* a = sA + warp * 16 * LD;
+  float2* tab = sT + warp * 2 * C;
   const int cg = C / groups, nvec = C / 8;
   const int64_t rows = (int64_t)frames * n_inner;
+  // blocks take contiguous shares of the 16-row tiles (a block touches one or two frames)
   const int64_t ntiles = (rows + 15) / 16;
-  for (int64_t t = (int64_t)blockIdx.x * GP_WARPS + warp; t < ntiles; t += (int64_t)gridDim.x * GP_WARPS) {
+  const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+  int fa = -1, fb = -1;
+  for (int64_t t = t0 + warp; t < t1; t += GP_WARPS) {
     const int64_t r0 = t * 16;
-    // 16 rows x nvec vectors: load all, then transform into the A tile
+    const int f0 = (int)(r0 / n_inner), f1 = (int)(min(r0 + 15, rows - 1) / n_inner);
+    if (f0 != fa || f1 != fb) {
+      // y = x * ss + bb, ss = rstd * gamma, bb = beta - mean * ss (gn_apply_kernel's arithmetic), per
+      // channel of the tile's first / last frame (a 16-row tile spans at most two frames: n_inner >= 16)
+      for (int c = lane; c < C; c += 32) {
+        const int g = c / cg;
+        const float s0 = __ldg(rstd + f0 * groups + g) * __ldg(gamma + c);
+        const float s1 = __ldg(rstd + f1 * groups + g) * __ldg(gamma + c);
+        tab[c] = make_float2(s0, fmaf(-__ldg(mean + f0 * groups + g), s0, __ldg(beta + c)));
+        tab[C + c] = make_float2(s1, fmaf(-__ldg(mean + f1 * groups + g), s1, __ldg(beta + c)));
+      }
+      fa = f0;
+      fb = f1;
+      __syncwarp();
+    }
+    // 16 rows x nvec vectors: a round of up to 8 loads per lane, then the transform into the A tile
     for (int i0 = 0; i0 < 16 * nvec; i0 += 32 * 8) {
       bf16x8 in[8];
 #pragma unroll
@@ -964,25 +984,24 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
       for (int u = 0; u < 8; ++u) {
         const int i = i0 + u * 32 + lane;
         if (i >= 16 * nvec) break;
-        const int64_t r = r0 + i / nvec;
-        const int v = i % nvec;
+        const int rr = i / nvec, v = i % nvec;
+        const int64_t r = r0 + rr;
         float fv[8];
         if (r < rows) {
-          const int f = (int)(r / n_inner);
+          const float4* tv = reinterpret_cast<const float4*>(tab + ((int)(r / n_inner) == f0 ? 0 : C) + v * 8);
           unpack8(in[u], fv);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = v * 8 + j, g = c / cg;
-            const float ss = __ldg(rstd + f * groups + g) * __ldg(gamma + c);
-            const float bb = fmaf(-__ldg(mean + f * groups + g), ss, __ldg(beta + c));
-            const float tv = fmaf(fv[j], ss, bb);
-            fv[j] = act ? silu_f(tv) : tv;
+          for (int q = 0; q < 4; ++q) {
+            const float4 sb = tv[q];   // (ss, bb) of channels 2q, 2q+1
+            const float ta = fmaf(fv[2 * q], sb.x, sb.y), tb = fmaf(fv[2 * q + 1], sb.z, sb.w);
+            fv[2 * q] = act ? silu_f(ta) : ta;
+            fv[2 * q + 1] = act ? silu_f(tb) : tb;
           }
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) fv[j] = 0.f;
         }
-        *reinterpret_cast<bf16x8*>(a + (i / nvec) * LD + v * 8) = pack8(fv);
+        *reinterpret_cast<bf16x8*>(a + rr * LD + v * 8) = pack8(fv);
       }
     }
     __syncwarp();
@@ -1017,7 +1036,7 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
 sf_status gn_project_launch(sf_view_t x, int frames, int n_inner, int C, int groups, const float* mean,
                             const float* rstd, const float* gamma, const float* beta, int act, const void* w, int N,
                             float* out, int64_t ldo, cudaStream_t st) {
-  const size_t smem = (size_t)(GP_NP + GP_WARPS * 16) * (C + 8) * sizeof(bf16);
+  const size_t smem = (size_t)(GP_NP + GP_WARPS * 16) * (C + 8) * sizeof(bf16) + (size_t)GP_WARPS * 2 * C * sizeof(float2);
   static size_t set = 48 * 1024;
   if (smem > set) {
     cudaFuncSetAttribute(gn_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1773,8 +1792,8 @@ sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int
 sf_status sf_group_norm_project(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
                                 const float* mean, const float* rstd, const float* gamma, const float* beta,
                                 int32_t act, const void* w, int32_t N, float* out, int64_t ldo, void* stream) {
-  SF_CHECK_ARG(frames >= 1 && n_inner >= 1 && C >= 16 && C % 16 == 0 && C <= 1024, SF_ERR_SHAPE,
-               "C must be a multiple of 16 in [16, 1024]");
+  SF_CHECK_ARG(frames >= 1 && n_inner >= 16 && C >= 16 && C % 16 == 0 && C <= 1024, SF_ERR_SHAPE,
+               "C must be a multiple of 16 in [16, 1024], frames of >= 16 rows");
   SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
   SF_CHECK_ARG(N >= 2 && N <= GP_NP && N % 2 == 0 && ldo >= N && ldo % 2 == 0, SF_ERR_SHAPE,
                "N must be even, <= 48, and fit the output rows");

@@ -199,16 +199,16 @@ def test_upsample_partials(F_, H, W, C, splits, c0):
     assert torch.allclose(pp[:, :, c0:].double().sum(1)[..., 1], (yd * yd).sum(1), rtol=1e-5, atol=1e-3)
 
 
-@pytest.mark.parametrize("F_,HW,C,groups,N", [(3, 9216, 320, 32, 36), (2, 1000, 64, 8, 36), (4, 257, 128, 32, 48),
-                                              (1, 16, 16, 4, 2)])
-def test_group_norm_project(F_, HW, C, groups, N):
+@pytest.mark.parametrize("F_,HW,C,groups,Nn", [(3, 9216, 320, 32, 36), (2, 1000, 64, 8, 36), (4, 257, 128, 32, 48),
+                                               (1, 16, 16, 4, 2), (5, 24, 32, 8, 36)])
+def test_group_norm_project(F_, HW, C, groups, Nn):
     """sf_group_norm_project == the GroupNorm apply (+ SiLU, bf16 as stored) followed by an fp32 projection."""
     torch.manual_seed(9)
     st = torch.cuda.current_stream().cuda_stream
     x = (torch.randn(F_ * HW, C, device=dev) * 1.5 + 0.2).to(torch.bfloat16)
     gamma = torch.rand(C, device=dev) + 0.5
     beta = torch.randn(C, device=dev) * 0.1
-    w = rnd(N, C, scale=C ** -0.5)
+    w = rnd(Nn, C, scale=C ** -0.5)
     mean = torch.empty(F_ * groups, device=dev)
     rstd = torch.empty_like(mean)
     work = torch.empty((N.query("sf_group_norm_workspace", F_, HW, C) + 3) // 4 + 1, device=dev)
@@ -217,14 +217,14 @@ def test_group_norm_project(F_, HW, C, groups, N):
     y = torch.empty_like(x)
     N.call("sf_group_norm_apply", Rows(x, 0, HW).view(), Rows(y, 0, HW).view(), F_, HW, C, groups, mean.data_ptr(),
            rstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), N.ACT_SILU, st)
-    ldo = N + 4
+    ldo = Nn + 4
     out = torch.full((F_ * HW, ldo), float("nan"), device=dev)
     N.call("sf_group_norm_project", Rows(x, 0, HW).view(), F_, HW, C, groups, mean.data_ptr(), rstd.data_ptr(),
-           gamma.data_ptr(), beta.data_ptr(), N.ACT_SILU, w.data_ptr(), N, out.data_ptr(), ldo, st)
+           gamma.data_ptr(), beta.data_ptr(), N.ACT_SILU, w.data_ptr(), Nn, out.data_ptr(), ldo, st)
     torch.cuda.synchronize()
     ref = y.double() @ w.double().T
-    got = out[:, :N].double()
-    assert torch.isnan(out[:, N:]).all(), "columns past N untouched"
+    got = out[:, :Nn].double()
+    assert torch.isnan(out[:, Nn:]).all(), "columns past N untouched"
     assert float((got - ref).abs().max() / ref.abs().max()) < 1e-5
 
 
