@@ -968,41 +968,58 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
       fb = f1;
       __syncwarp();
     }
-    // 16 rows x nvec vectors: a round of up to 8 loads per lane, then the transform into the A tile
+    // 16 rows x nvec vectors: a round of up to 8 loads per lane, then the transform into the A tile.
+    // Row -> frame without divisions: the tile's rows from `split` on belong to frame f0 + 1
+    const int split = (int)min((int64_t)16, (int64_t)(f0 + 1) * n_inner - r0);
+    const int64_t base0 = r0 - (int64_t)f0 * n_inner;              // local row of row 0 in frame f0
+    const int nvalid = (int)min((int64_t)16, rows - r0);
+    int rr0 = lane / nvec, v0 = lane % nvec;                        // (row, vector) of element i0 + lane
     for (int i0 = 0; i0 < 16 * nvec; i0 += 32 * 8) {
       bf16x8 in[8];
+      int rr = rr0, v = v0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * 32 + lane;
-        const int64_t r = r0 + i / nvec;
-        if (i < 16 * nvec && r < rows) {
-          const int f = (int)(r / n_inner);
-          in[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f, r - (int64_t)f * n_inner) + (i % nvec) * 8);
+        if (rr < nvalid) {
+          const bool second = rr >= split;
+          const int64_t local = second ? rr - split : base0 + rr;
+          in[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f0 + (second ? 1 : 0), local) + v * 8);
+        }
+        v += 32;
+        while (v >= nvec) {
+          v -= nvec;
+          ++rr;
         }
       }
+      rr = rr0;
+      v = v0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * 32 + lane;
-        if (i >= 16 * nvec) break;
-        const int rr = i / nvec, v = i % nvec;
-        const int64_t r = r0 + rr;
-        float fv[8];
-        if (r < rows) {
-          const float4* tv = reinterpret_cast<const float4*>(tab + ((int)(r / n_inner) == f0 ? 0 : C) + v * 8);
-          unpack8(in[u], fv);
+        if (rr < 16) {
+          float fv[8];
+          if (rr < nvalid) {
+            const float4* tv = reinterpret_cast<const float4*>(tab + (rr >= split ? C : 0) + v * 8);
+            unpack8(in[u], fv);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 sb = tv[q];   // (ss, bb) of channels 2q, 2q+1
-            const float ta = fmaf(fv[2 * q], sb.x, sb.y), tb = fmaf(fv[2 * q + 1], sb.z, sb.w);
-            fv[2 * q] = act ? silu_f(ta) : ta;
-            fv[2 * q + 1] = act ? silu_f(tb) : tb;
+            for (int q = 0; q < 4; ++q) {
+              const float4 sb = tv[q];   // (ss, bb) of channels 2q, 2q+1
+              const float ta = fmaf(fv[2 * q], sb.x, sb.y), tb = fmaf(fv[2 * q + 1], sb.z, sb.w);
+              fv[2 * q] = act ? silu_f(ta) : ta;
+              fv[2 * q + 1] = act ? silu_f(tb) : tb;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) fv[j] = 0.f;
           }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) fv[j] = 0.f;
+          *reinterpret_cast<bf16x8*>(a + rr * LD + v * 8) = pack8(fv);
         }
-        *reinterpret_cast<bf16x8*>(a + rr * LD + v * 8) = pack8(fv);
+        v += 32;
+        while (v >= nvec) {
+          v -= nvec;
+          ++rr;
+        }
       }
+      rr0 = rr;
+      v0 = v;
     }
     __syncwarp();
     float acc[GP_NP / 8][4];
