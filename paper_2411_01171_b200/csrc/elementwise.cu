@@ -925,7 +925,8 @@ __device__ __forceinline__ unsigned pack_bf2(float a, float b) {
 // it with the resident W (bf16 [48][C]) on mma.sync m16n8k16; fp32 out.  Each element is
 // transformed once (the per-tap projection reads every pixel once, unlike a 3x3 implicit GEMM).
 // ---------------------------------------------------------------------------
-constexpr int GP_WARPS = 4, GP_NP = 48;   // output columns padded to 6 n-tiles of 8
+constexpr int GP_WARPS = 16, GP_NP = 48;   // output columns padded to 6 n-tiles of 8
+constexpr int GP_LDA = 64 + 8;              // one 64-channel K chunk per A buffer, +16 B per row
 __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
     sf_view_t x, int frames, int n_inner, int C, int groups, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta, int act,
@@ -933,9 +934,9 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
   griddep_wait();
   extern __shared__ __align__(16) uint8_t gp_raw[];
   const int LD = C + 8;   // +16 B per row: conflict-free ldmatrix
-  bf16* sW = reinterpret_cast<bf16*>(gp_raw);              // [GP_NP][LD]
-  bf16* sA = sW + GP_NP * LD;                              // [GP_WARPS][16][LD]
-  float2* sT = reinterpret_cast<float2*>(sA + GP_WARPS * 16 * LD);   // [GP_WARPS][2][C] (scale, shift)
+  bf16* sW = reinterpret_cast<bf16*>(gp_raw);                        // [GP_NP][LD]
+  bf16* sA = sW + GP_NP * LD;                                        // [GP_WARPS][2][16][GP_LDA]
+  float2* sT = reinterpret_cast<float2*>(sA + GP_WARPS * 2 * 16 * GP_LDA);   // [GP_WARPS][2][C] (scale, shift)
   for (int i = threadIdx.x; i < GP_NP * (C / 8); i += blockDim.x) {
     const int n = i / (C / 8), v = i % (C / 8);
     *reinterpret_cast<bf16x8*>(sW + n * LD + v * 8) =
@@ -943,13 +944,15 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  bf16* a = sA + warp * 16 * LD;
+  bf16* abuf = sA + warp * 2 * 16 * GP_LDA;
   float2* tab = sT + warp * 2 * C;
-  const int cg = C / groups, nvec = C / 8;
+  const int cg = C / groups, nk = C / 64;
   const int64_t rows = (int64_t)frames * n_inner;
   // blocks take contiguous shares of the 16-row tiles (a block touches one or two frames)
   const int64_t ntiles = (rows + 15) / 16;
   const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+  // a K chunk = 16 rows x 8 vectors: lane -> rows lane / 8 + {0, 4, 8, 12}, vector lane % 8
+  const int lr = lane >> 3, lv = lane & 7;
   int fa = -1, fb = -1;
   for (int64_t t = t0 + warp; t < t1; t += GP_WARPS) {
     const int64_t r0 = t * 16;
@@ -968,74 +971,68 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
       fb = f1;
       __syncwarp();
     }
-    // 16 rows x nvec vectors: a round of up to 8 loads per lane, then the transform into the A tile.
-    // Row -> frame without divisions: the tile's rows from `split` on belong to frame f0 + 1
+    // row -> (frame, local row) without divisions: rows from `split` on belong to frame f0 + 1
     const int split = (int)min((int64_t)16, (int64_t)(f0 + 1) * n_inner - r0);
-    const int64_t base0 = r0 - (int64_t)f0 * n_inner;              // local row of row 0 in frame f0
+    const int64_t base0 = r0 - (int64_t)f0 * n_inner;
     const int nvalid = (int)min((int64_t)16, rows - r0);
-    int rr0 = lane / nvec, v0 = lane % nvec;                        // (row, vector) of element i0 + lane
-    for (int i0 = 0; i0 < 16 * nvec; i0 += 32 * 8) {
-      bf16x8 in[8];
-      int rr = rr0, v = v0;
+    const bf16* src[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (rr < nvalid) {
-          const bool second = rr >= split;
-          const int64_t local = second ? rr - split : base0 + rr;
-          in[u] = *reinterpret_cast<const bf16x8*>(row_ptr<const bf16>(x, f0 + (second ? 1 : 0), local) + v * 8);
-        }
-        v += 32;
-        while (v >= nvec) {
-          v -= nvec;
-          ++rr;
-        }
-      }
-      rr = rr0;
-      v = v0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (rr < 16) {
-          float fv[8];
-          if (rr < nvalid) {
-            const float4* tv = reinterpret_cast<const float4*>(tab + (rr >= split ? C : 0) + v * 8);
-            unpack8(in[u], fv);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 sb = tv[q];   // (ss, bb) of channels 2q, 2q+1
-              const float ta = fmaf(fv[2 * q], sb.x, sb.y), tb = fmaf(fv[2 * q + 1], sb.z, sb.w);
-              fv[2 * q] = act ? silu_f(ta) : ta;
-              fv[2 * q + 1] = act ? silu_f(tb) : tb;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) fv[j] = 0.f;
-          }
-          *reinterpret_cast<bf16x8*>(a + rr * LD + v * 8) = pack8(fv);
-        }
-        v += 32;
-        while (v >= nvec) {
-          v -= nvec;
-          ++rr;
-        }
-      }
-      rr0 = rr;
-      v0 = v;
+    for (int u = 0; u < 4; ++u) {
+      const int rr = lr + 4 * u;
+      const bool second = rr >= split;
+      src[u] = rr < nvalid ? row_ptr<const bf16>(x, f0 + (second ? 1 : 0), second ? rr - split : base0 + rr) + lv * 8
+                           : nullptr;
     }
-    __syncwarp();
+    bf16x8 cur[4], nxt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (src[u]) cur[u] = *reinterpret_cast<const bf16x8*>(src[u]);
     float acc[GP_NP / 8][4];
 #pragma unroll
     for (int j = 0; j < GP_NP / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-    for (int kk = 0; kk < C; kk += 16) {
-      unsigned af[4];
-      tq_ldsm_x4(af, a + (lane & 15) * LD + kk + (lane >> 4) * 8);
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) {   // the next chunk's loads fly while this one is transformed and multiplied
 #pragma unroll
-      for (int j = 0; j < GP_NP / 8; j += 2) {
-        unsigned b[4];
-        const int nrow = j * 8 + (lane & 7) + ((lane >> 4) << 3);
-        tq_ldsm_x4(b, sW + nrow * LD + kk + ((lane >> 3) & 1) * 8);
-        tq_mma(acc[j], af, b[0], b[1]);
-        tq_mma(acc[j + 1], af, b[2], b[3]);
+        for (int u = 0; u < 4; ++u)
+          if (src[u]) nxt[u] = *reinterpret_cast<const bf16x8*>(src[u] + (kc + 1) * 64);
       }
+      bf16* a = abuf + (kc & 1) * 16 * GP_LDA;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = lr + 4 * u;
+        float fv[8];
+        if (src[u]) {
+          const float4* tv = reinterpret_cast<const float4*>(tab + (rr >= split ? C : 0) + kc * 64 + lv * 8);
+          unpack8(cur[u], fv);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 sb = tv[q];   // (ss, bb) of channels 2q, 2q+1
+            const float ta = fmaf(fv[2 * q], sb.x, sb.y), tb = fmaf(fv[2 * q + 1], sb.z, sb.w);
+            fv[2 * q] = act ? silu_f(ta) : ta;
+            fv[2 * q + 1] = act ? silu_f(tb) : tb;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) fv[j] = 0.f;
+        }
+        *reinterpret_cast<bf16x8*>(a + rr * GP_LDA + lv * 8) = pack8(fv);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int kk = 0; kk < 64; kk += 16) {
+        unsigned af[4];
+        tq_ldsm_x4(af, a + (lane & 15) * GP_LDA + kk + (lane >> 4) * 8);
+#pragma unroll
+        for (int j = 0; j < GP_NP / 8; j += 2) {
+          unsigned b[4];
+          const int nrow = j * 8 + (lane & 7) + ((lane >> 4) << 3);
+          tq_ldsm_x4(b, sW + nrow * LD + kc * 64 + kk + ((lane >> 3) & 1) * 8);
+          tq_mma(acc[j], af, b[0], b[1]);
+          tq_mma(acc[j + 1], af, b[2], b[3]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
     }
     const int64_t ra = r0 + (lane >> 2), rb = ra + 8;
 #pragma unroll
@@ -1046,14 +1043,15 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
         if (rb < rows) *reinterpret_cast<float2*>(out + rb * ldo + c) = make_float2(acc[j][2], acc[j][3]);
       }
     }
-    __syncwarp();   // the A tile is rewritten by the next tile
+    __syncwarp();   // the A buffers are rewritten by the next tile
   }
 }
 
 sf_status gn_project_launch(sf_view_t x, int frames, int n_inner, int C, int groups, const float* mean,
                             const float* rstd, const float* gamma, const float* beta, int act, const void* w, int N,
                             float* out, int64_t ldo, cudaStream_t st) {
-  const size_t smem = (size_t)(GP_NP + GP_WARPS * 16) * (C + 8) * sizeof(bf16) + (size_t)GP_WARPS * 2 * C * sizeof(float2);
+  const size_t smem = ((size_t)GP_NP * (C + 8) + (size_t)GP_WARPS * 2 * 16 * GP_LDA) * sizeof(bf16) +
+                      (size_t)GP_WARPS * 2 * C * sizeof(float2);
   static size_t set = 48 * 1024;
   if (smem > set) {
     cudaFuncSetAttribute(gn_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1809,8 +1807,8 @@ sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int
 sf_status sf_group_norm_project(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
                                 const float* mean, const float* rstd, const float* gamma, const float* beta,
                                 int32_t act, const void* w, int32_t N, float* out, int64_t ldo, void* stream) {
-  SF_CHECK_ARG(frames >= 1 && n_inner >= 16 && C >= 16 && C % 16 == 0 && C <= 1024, SF_ERR_SHAPE,
-               "C must be a multiple of 16 in [16, 1024], frames of >= 16 rows");
+  SF_CHECK_ARG(frames >= 1 && n_inner >= 16 && C >= 64 && C % 64 == 0 && C <= 384, SF_ERR_SHAPE,
+               "C must be a multiple of 64 in [64, 384] (shared memory), frames of >= 16 rows");
   SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
   SF_CHECK_ARG(N >= 2 && N <= GP_NP && N % 2 == 0 && ldo >= N && ldo % 2 == 0, SF_ERR_SHAPE,
                "N must be even, <= 48, and fit the output rows");
