@@ -997,16 +997,32 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
           if (src[u]) nxt[u] = *reinterpret_cast<const bf16x8*>(src[u] + (kc + 1) * 64);
       }
       bf16* a = abuf + (kc & 1) * 16 * GP_LDA;
+      // this lane's 8 channels' (ss, bb) once per chunk (its 4 rows share them unless the tile
+      // straddles two frames)
+      float4 sbA[4];
+      {
+        const float4* tv = reinterpret_cast<const float4*>(tab + kc * 64 + lv * 8);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sbA[q] = tv[q];
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int rr = lr + 4 * u;
         float fv[8];
         if (src[u]) {
-          const float4* tv = reinterpret_cast<const float4*>(tab + (rr >= split ? C : 0) + kc * 64 + lv * 8);
+          float4 sb4[4];
+          if (rr >= split) {
+            const float4* tv = reinterpret_cast<const float4*>(tab + C + kc * 64 + lv * 8);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sb4[q] = tv[q];
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sb4[q] = sbA[q];
+          }
           unpack8(cur[u], fv);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 sb = tv[q];   // (ss, bb) of channels 2q, 2q+1
+            const float4 sb = sb4[q];   // (ss, bb) of channels 2q, 2q+1
             const float ta = fmaf(fv[2 * q], sb.x, sb.y), tb = fmaf(fv[2 * q + 1], sb.z, sb.w);
             fv[2 * q] = act ? silu_f(ta) : ta;
             fv[2 * q + 1] = act ? silu_f(tb) : tb;
