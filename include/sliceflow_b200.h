@@ -217,6 +217,12 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
  * sf_gemm with the tap-major weight matrix); this sums the 9 shifted taps with
  * zero padding: out[f][p][co] = bias[co] + sum_tap Y[f][p + off(tap)][tap*cout + co]
  * (kernels.py:181-201 regrouped; fixed tap order).  out: fp32 rows view. */
+/* in_conv with the GroupNorm partials of its output (the statistics of down_blocks.0.res.norm1,
+ * unet.py:213-216): part[(frame * splits + split) * cout + c] = (sum, sum sq) of the stored bf16 values
+ * over the split's contiguous run of 16-pixel tiles.  Tensor-core path only (cout % 64 == 0). */
+sf_status sf_conv3x3_smallcin_gn(const float* x, int32_t frames, int32_t H, int32_t W, int32_t cin, const float* w,
+                                 const float* bias, int32_t cout, sf_view_t y, int32_t splits, void* part,
+                                 void* stream);
 sf_status sf_conv3x3_tapsum(const float* y, int32_t ldy, int32_t frames, int32_t H, int32_t W, int32_t cout,
                             const float* bias, sf_view_t out, void* stream);
 /* y[n] = W[n][:] . e + b[n] for a batch of step embeddings (res-block emb_proj) */

@@ -76,6 +76,7 @@ _PROTOS = {
     "sf_temporal_attention_fused_supported": [i32, i32],
     "sf_temporal_attention_fused": [View, vp, View, View, i32, i32, i32, i32, vp],
     "sf_conv3x3_smallcin": [vp, i32, i32, i32, i32, vp, vp, i32, View, vp],
+    "sf_conv3x3_smallcin_gn": [vp, i32, i32, i32, i32, vp, vp, i32, View, i32, vp, vp],
     "sf_conv3x3_tapsum": [vp, i32, i32, i32, i32, i32, vp, View, vp],
     "sf_gemv_f32": [vp, vp, vp, vp, i32, i32, vp],
     "sf_bcthw_to_rows_f32": [vp, vp, i32, i32, i32, vp],

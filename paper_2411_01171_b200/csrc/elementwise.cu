@@ -1370,127 +1370,164 @@ __global__ void __launch_bounds__(SC_THREADS) conv_smallcin_kernel(const float* 
 // latent into shared memory (taps outside the image are zero), keeps the whole
 // weight matrix [cout][K] resident, and writes bf16 output through a staging
 // tile so every row leaves as full 128-byte segments.
-constexpr int SCM_THREADS = 256, SCM_TILE = 128, SCM_NCH = 64;
+constexpr int SCM_THREADS = 256, SCM_WARPS = SCM_THREADS / 32, SCM_NCH = 64;
 template <int KP>
 struct ScmLayout {
   static constexpr int LDA = KP + 8;                 // +16 B per row: conflict-free ldmatrix
   static constexpr int LDO = SCM_NCH + 8;
-  static constexpr int A_ELEMS = SCM_TILE * LDA;
-  static constexpr int O_ELEMS = SCM_TILE * LDO;
+  static constexpr int A_ELEMS = SCM_WARPS * 16 * LDA;   // per warp: its 16-pixel im2col tile
+  static constexpr int O_ELEMS = SCM_WARPS * 16 * LDO;   // per warp: a 16 x 64 output staging tile
 };
+// The network's in_conv (kernels.py:181-201 with 4 input channels): im2col rows of K = 9 * cin
+// (padded to KP) gathered from the fp32 latent, multiplied on mma.sync by the resident weights.
+// Every warp works on its own tasks -- task = (frame, split): a contiguous run of 16-pixel tiles of
+// one frame -- with warp-private im2col / staging tiles, so no block barrier follows the weight load.
+// With part != nullptr the warp also sums the bf16 values it stores per channel over its task and
+// writes part[(frame * splits + split) * cout + c] (float2 sum, sum sq): the statistics of the
+// GroupNorm that reads this output (unet.py:213-216, in_conv -> down_blocks.0.res.norm1).
 template <int KP>
 __global__ void __launch_bounds__(SCM_THREADS) conv_smallcin_mma_kernel(const float* __restrict__ x, int frames, int H,
                                                                        int W, int cin, const float* __restrict__ wt,
                                                                        const float* __restrict__ bias, int cout,
-                                                                       sf_view_t y) {
+                                                                       sf_view_t y, int splits, float2* part) {
   griddep_wait();
   using L = ScmLayout<KP>;
   extern __shared__ __align__(16) uint8_t scm_raw[];
-  bf16* sA = reinterpret_cast<bf16*>(scm_raw);
-  bf16* sO = sA + L::A_ELEMS;
-  bf16* sB = sO + L::O_ELEMS;  // [cout][LDA]
+  bf16* sA0 = reinterpret_cast<bf16*>(scm_raw);
+  bf16* sO0 = sA0 + L::A_ELEMS;
+  bf16* sB = sO0 + L::O_ELEMS;  // [cout][LDA]
   float* sBias = reinterpret_cast<float*>(sB + (size_t)cout * L::LDA);
   const int K = 9 * cin;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bf16* sA = sA0 + warp * 16 * L::LDA;
+  bf16* sO = sO0 + warp * 16 * L::LDO;
+  float2* sP = reinterpret_cast<float2*>(sBias + cout) + (size_t)warp * cout;   // [cout] task sums (part != 0)
   // weights [9][cin][cout] fp32 -> [cout][k = tap*cin + ci] bf16, zero past K
   for (int i = threadIdx.x; i < cout * KP; i += SCM_THREADS) {
     const int co = i / KP, k = i % KP;
     sB[co * L::LDA + k] = __float2bfloat16(k < K ? wt[(size_t)k * cout + co] : 0.f);
   }
   for (int i = threadIdx.x; i < cout; i += SCM_THREADS) sBias[i] = bias[i];
-  // K padding columns of the im2col tile stay zero for every tile
-  for (int i = threadIdx.x; i < SCM_TILE * (KP - K); i += SCM_THREADS)
-    sA[(i / (KP - K)) * L::LDA + K + i % (KP - K)] = __float2bfloat16(0.f);
+  // K padding columns of the im2col tiles stay zero for every tile
+  for (int i = lane; i < 16 * (KP - K); i += 32) sA[(i / (KP - K)) * L::LDA + K + i % (KP - K)] = __float2bfloat16(0.f);
+  __syncthreads();
   const int HW = H * W;
-  const int64_t npix = (int64_t)frames * HW;
-  const int64_t ntiles = (npix + SCM_TILE - 1) / SCM_TILE;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t p0 = t * SCM_TILE;
-    __syncthreads();  // previous tile's sA / sO reads are done (and weights are in place)
-    // one (pixel, tap) per thread iteration: cin consecutive floats
-    for (int i = threadIdx.x; i < SCM_TILE * 9; i += SCM_THREADS) {
-      const int r = i / 9, tap = i - r * 9;
-      const int64_t pp = p0 + r;
-      bf16* dst = sA + r * L::LDA + tap * cin;
-      const float* src = nullptr;
-      if (pp < npix) {
-        const int f = (int)(pp / HW), pix = (int)(pp - (int64_t)f * HW);
-        const int py = pix / W, px = pix - py * W;
-        const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
-        if (yy >= 0 && yy < H && xx >= 0 && xx < W) src = x + ((int64_t)f * HW + (int64_t)yy * W + xx) * cin;
+  const int tpf = (HW + 15) / 16;                  // 16-pixel tiles per frame (none straddles frames)
+  const int tps = (tpf + splits - 1) / splits;     // tiles per split
+  const int64_t ntasks = (int64_t)frames * splits;
+  const int nch = cout / SCM_NCH;
+  for (int64_t task = (int64_t)blockIdx.x * SCM_WARPS + warp; task < ntasks; task += (int64_t)gridDim.x * SCM_WARPS) {
+    const int f = (int)(task / splits), sp = (int)(task % splits);
+    const int ta = sp * tps, tb = min(tpf, ta + tps);
+    if (part != nullptr)   // lane-owned columns 2 lane, 2 lane + 1 of every 64-channel chunk
+      for (int c = 2 * lane; c < cout; c += 64) sP[c] = sP[c + 1] = make_float2(0.f, 0.f);
+    for (int t = ta; t < tb; ++t) {
+      const int q0 = t * 16;
+      // im2col: one (pixel, tap) per lane iteration, cin consecutive floats
+      for (int i = lane; i < 16 * 9; i += 32) {
+        const int r = i / 9, tap = i - r * 9;
+        const int pix = q0 + r;
+        bf16* dst = sA + r * L::LDA + tap * cin;
+        const float* src = nullptr;
+        if (pix < HW) {
+          const int py = pix / W, px = pix - py * W;
+          const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+          if (yy >= 0 && yy < H && xx >= 0 && xx < W) src = x + ((int64_t)f * HW + (int64_t)yy * W + xx) * cin;
+        }
+        if (cin == 4) {
+          float4 v = src ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<unsigned*>(dst) = pack_bf2(v.x, v.y);
+          *reinterpret_cast<unsigned*>(dst + 2) = pack_bf2(v.z, v.w);
+        } else {
+          for (int ci = 0; ci < cin; ++ci) dst[ci] = __float2bfloat16(src ? __ldg(src + ci) : 0.f);
+        }
       }
-      if (cin == 4) {
-        float4 v = src ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        *reinterpret_cast<unsigned*>(dst) = pack_bf2(v.x, v.y);
-        *reinterpret_cast<unsigned*>(dst + 2) = pack_bf2(v.z, v.w);
-      } else {
-        for (int ci = 0; ci < cin; ++ci) dst[ci] = __float2bfloat16(src ? __ldg(src + ci) : 0.f);
+      __syncwarp();
+      unsigned af[KP / 16][4];
+#pragma unroll
+      for (int kk = 0; kk < KP / 16; ++kk) tq_ldsm_x4(af[kk], sA + (lane & 15) * L::LDA + kk * 16 + (lane >> 4) * 8);
+      const int nvalid = min(16, HW - q0);
+      for (int ch = 0; ch < nch; ++ch) {
+        const int n0 = ch * SCM_NCH;
+        float acc[SCM_NCH / 8][4];
+#pragma unroll
+        for (int j = 0; j < SCM_NCH / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < KP / 16; ++kk) {
+#pragma unroll
+          for (int j = 0; j < SCM_NCH / 8; j += 2) {
+            unsigned b[4];
+            const int nrow = n0 + j * 8 + (lane & 7) + ((lane >> 4) << 3);
+            tq_ldsm_x4(b, sB + nrow * L::LDA + kk * 16 + ((lane >> 3) & 1) * 8);
+            tq_mma(acc[j], af[kk], b[0], b[1]);
+            tq_mma(acc[j + 1], af[kk], b[2], b[3]);
+          }
+        }
+        // bias, bf16, the warp's 16 x 64 staging tile
+        const int r0 = lane >> 2;
+#pragma unroll
+        for (int j = 0; j < SCM_NCH / 8; ++j) {
+          const int c = j * 8 + (lane & 3) * 2;
+          const float b0 = sBias[n0 + c], b1 = sBias[n0 + c + 1];
+          *reinterpret_cast<unsigned*>(sO + r0 * L::LDO + c) = pack_bf2(acc[j][0] + b0, acc[j][1] + b1);
+          *reinterpret_cast<unsigned*>(sO + (r0 + 8) * L::LDO + c) = pack_bf2(acc[j][2] + b0, acc[j][3] + b1);
+        }
+        __syncwarp();
+        // 16 rows x 128 B: 8 lanes per row, 16 B each, 4 rows per pass
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = k * 4 + (lane >> 3), v = lane & 7;
+          if (r < nvalid)
+            *reinterpret_cast<bf16x8*>(row_ptr<bf16>(y, f, q0 + r) + n0 + v * 8) =
+                *reinterpret_cast<const bf16x8*>(sO + r * L::LDO + v * 8);
+        }
+        if (part != nullptr) {
+          // the stored values' sums: lane owns columns 2 lane, 2 lane + 1 of the chunk, rows in order
+          float2 a = sP[n0 + 2 * lane], b = sP[n0 + 2 * lane + 1];
+          for (int r = 0; r < nvalid; ++r) {
+            const float2 v2 = __bfloat1622float2(*reinterpret_cast<const bf162*>(sO + r * L::LDO + 2 * lane));
+            a.x += v2.x;
+            a.y = fmaf(v2.x, v2.x, a.y);
+            b.x += v2.y;
+            b.y = fmaf(v2.y, v2.y, b.y);
+          }
+          sP[n0 + 2 * lane] = a;
+          sP[n0 + 2 * lane + 1] = b;
+        }
+        __syncwarp();
       }
     }
-    __syncthreads();
-    // A fragments of this warp's 16 rows, all K
-    unsigned af[KP / 16][4];
-#pragma unroll
-    for (int kk = 0; kk < KP / 16; ++kk)
-      tq_ldsm_x4(af[kk], sA + (warp * 16 + (lane & 15)) * L::LDA + kk * 16 + (lane >> 4) * 8);
-    for (int n0 = 0; n0 < cout; n0 += SCM_NCH) {
-      float acc[SCM_NCH / 8][4];
-#pragma unroll
-      for (int j = 0; j < SCM_NCH / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < KP / 16; ++kk) {
-#pragma unroll
-        for (int j = 0; j < SCM_NCH / 8; j += 2) {
-          // two n-tiles: lanes 0-15 -> n-tile j (k lo/hi), lanes 16-31 -> n-tile j+1
-          unsigned b[4];
-          const int nrow = n0 + j * 8 + (lane & 7) + ((lane >> 4) << 3);
-          tq_ldsm_x4(b, sB + nrow * L::LDA + kk * 16 + ((lane >> 3) & 1) * 8);
-          tq_mma(acc[j], af[kk], b[0], b[1]);
-          tq_mma(acc[j + 1], af[kk], b[2], b[3]);
-        }
+    if (part != nullptr) {
+      float2* dst = part + ((int64_t)f * splits + sp) * cout;
+      for (int c = 2 * lane; c < cout; c += 64) {
+        dst[c] = sP[c];
+        dst[c + 1] = sP[c + 1];
       }
-      // bias, bf16, staging tile [128][64]
-      const int r0 = warp * 16 + (lane >> 2);
-#pragma unroll
-      for (int j = 0; j < SCM_NCH / 8; ++j) {
-        const int c = j * 8 + (lane & 3) * 2;
-        const float b0 = sBias[n0 + c], b1 = sBias[n0 + c + 1];
-        *reinterpret_cast<unsigned*>(sO + r0 * L::LDO + c) = pack_bf2(acc[j][0] + b0, acc[j][1] + b1);
-        *reinterpret_cast<unsigned*>(sO + (r0 + 8) * L::LDO + c) = pack_bf2(acc[j][2] + b0, acc[j][3] + b1);
-      }
-      __syncthreads();
-      // 128 rows x 128 B: 8 threads per row, 16 B each
-      for (int i = threadIdx.x; i < SCM_TILE * (SCM_NCH / 8); i += SCM_THREADS) {
-        const int r = i >> 3, v = i & 7;
-        const int64_t pp = p0 + r;
-        if (pp < npix) {
-          const int f = (int)(pp / HW);
-          bf16* dst = row_ptr<bf16>(y, f, pp - (int64_t)f * HW) + n0 + v * 8;
-          *reinterpret_cast<bf16x8*>(dst) = *reinterpret_cast<const bf16x8*>(sO + r * L::LDO + v * 8);
-        }
-      }
-      __syncthreads();
     }
   }
 }
 
 template <int KP>
 static sf_status conv_smallcin_mma_launch(const float* x, int frames, int H, int W, int cin, const float* w,
-                                          const float* bias, int cout, sf_view_t y, cudaStream_t st) {
+                                          const float* bias, int cout, sf_view_t y, int splits, void* part,
+                                          cudaStream_t st) {
   using L = ScmLayout<KP>;
-  const size_t smem = (size_t)(L::A_ELEMS + L::O_ELEMS + cout * L::LDA) * sizeof(bf16) + cout * sizeof(float);
+  const size_t smem = (size_t)(L::A_ELEMS + L::O_ELEMS + cout * L::LDA) * sizeof(bf16) + cout * sizeof(float) +
+                      (size_t)SCM_WARPS * cout * sizeof(float2);
   static size_t cfg = 0;
   if (smem > 48 * 1024 && smem > cfg) {
     cudaFuncSetAttribute(conv_smallcin_mma_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cfg = smem;
   }
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_smallcin_mma_kernel<KP>, SCM_THREADS, smem);
-  const int64_t ntiles = ((int64_t)frames * H * W + SCM_TILE - 1) / SCM_TILE;
-  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));
-  launch_k(conv_smallcin_mma_kernel<KP>, dim3((unsigned)grid), dim3(SCM_THREADS), smem, st, x, frames, H, W, cin, w, bias, cout, y);
+  // without partials the split count only shapes the work: ~2 tasks per warp slot
+  const int tpf = (H * W + 15) / 16;
+  if (!part) splits = std::max(1, std::min(tpf, (2 * num_sms() * std::max(per_sm, 1) * SCM_WARPS + frames - 1) / frames));
+  const int64_t ntasks = (int64_t)frames * splits;
+  const int64_t grid = std::min<int64_t>((ntasks + SCM_WARPS - 1) / SCM_WARPS, (int64_t)num_sms() * std::max(per_sm, 1));
+  launch_k(conv_smallcin_mma_kernel<KP>, dim3((unsigned)grid), dim3(SCM_THREADS), smem, st, x, frames, H, W, cin, w,
+           bias, cout, y, splits, (float2*)part);
   return launch_status("sf_conv3x3_smallcin(mma)");
 }
 
@@ -1918,9 +1955,9 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
   // tensor-core path: K = 9*cin padded to 16, whole cout resident in smem
   if (cout % SCM_NCH == 0 && cout <= 640 && 9 * cin <= 96) {
     const int kp = (9 * cin + 15) / 16 * 16;
-    if (kp <= 16) return conv_smallcin_mma_launch<16>(x, frames, H, W, cin, w, bias, cout, y, st);
-    if (kp <= 48) return conv_smallcin_mma_launch<48>(x, frames, H, W, cin, w, bias, cout, y, st);
-    return conv_smallcin_mma_launch<96>(x, frames, H, W, cin, w, bias, cout, y, st);
+    if (kp <= 16) return conv_smallcin_mma_launch<16>(x, frames, H, W, cin, w, bias, cout, y, 0, nullptr, st);
+    if (kp <= 48) return conv_smallcin_mma_launch<48>(x, frames, H, W, cin, w, bias, cout, y, 0, nullptr, st);
+    return conv_smallcin_mma_launch<96>(x, frames, H, W, cin, w, bias, cout, y, 0, nullptr, st);
   }
   if (cout % 32 == 0) {
     static size_t cfg32 = 0;
@@ -1942,6 +1979,22 @@ sf_status sf_conv3x3_smallcin(const float* x, int32_t frames, int32_t H, int32_t
                                                                                   cout, y);
   }
   return launch_status("sf_conv3x3_smallcin");
+}
+
+sf_status sf_conv3x3_smallcin_gn(const float* x, int32_t frames, int32_t H, int32_t W, int32_t cin, const float* w,
+                                 const float* bias, int32_t cout, sf_view_t y, int32_t splits, void* part,
+                                 void* stream) {
+  SF_CHECK_ARG(frames >= 1 && H >= 1 && W >= 1 && cin >= 1, SF_ERR_SHAPE, "bad extents");
+  SF_CHECK_ARG(cout % SCM_NCH == 0 && cout <= 640 && 9 * cin <= 96, SF_ERR_UNSUPPORTED,
+               "GroupNorm partials need the tensor-core in_conv (cout % 64 == 0, <= 640; 9 cin <= 96)");
+  SF_CHECK_ARG(splits >= 1 && splits <= (H * W + 15) / 16, SF_ERR_PARAM, "1 <= splits <= 16-pixel tiles per frame");
+  SF_CHECK_ARG(x && w && bias && part && view_vec8_ok(y) && ((uintptr_t)part & 7) == 0, SF_ERR_PARAM,
+               "null or unaligned operand");
+  const int kp = (9 * cin + 15) / 16 * 16;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kp <= 16) return conv_smallcin_mma_launch<16>(x, frames, H, W, cin, w, bias, cout, y, splits, part, st);
+  if (kp <= 48) return conv_smallcin_mma_launch<48>(x, frames, H, W, cin, w, bias, cout, y, splits, part, st);
+  return conv_smallcin_mma_launch<96>(x, frames, H, W, cin, w, bias, cout, y, splits, part, st);
 }
 
 sf_status sf_conv3x3_tapsum(const float* y, int32_t ldy, int32_t frames, int32_t H, int32_t W, int32_t cout,

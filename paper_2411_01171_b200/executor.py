@@ -245,9 +245,17 @@ class Plan:
             if pg is None or pg.domain is not Domain.SPATIAL:
                 continue
             conv = pg.ops[-1]
-            if conv.kind is not OpKind.CONV2D or "w" not in self.dw.p.get(conv.id, {}):
+            if conv.kind is not OpKind.CONV2D or conv.id in self.gn_feed:
                 continue
-            if pg.head_input == "x" or conv.id in self.gn_feed:
+            if pg.head_input == "x" and len(pg.ops) == 1 and "wt32" in self.dw.p.get(conv.id, {}):
+                # in_conv on the tensor-core small-channel kernel (sf_conv3x3_smallcin_gn):
+                # task-ordered partials, about one task per warp slot (2 blocks x 8 warps per SM)
+                sv, cin = self.shapes[v], self.shapes["x"].c
+                if sv.c % 64 == 0 and sv.c <= 640 and 9 * cin <= 96 and v == conv.id:
+                    self.gn_roles.setdefault(conv.id, []).append(("smallcin", v, 0))
+                    self.gn_meta[v] = max(1, min(-(-(sv.h * sv.w) // 16), (16 * sms) // max(1, nf), 64))
+                continue
+            if "w" not in self.dw.p.get(conv.id, {}) or pg.head_input == "x":
                 continue
             if self.shapes[conv.id] != self.shapes[v]:
                 continue
@@ -924,8 +932,14 @@ class Plan:
                     elif k is OpKind.CONV2D:
                         if latent_in and src == "IN":
                             lat = self.latent[sl[0] * ihw:]
-                            N.call("sf_conv3x3_smallcin", lat.data_ptr(), nf, ish.h, ish.w, ish.c,
-                                   prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), st)
+                            if o.id in gn_rs:
+                                e = gn_rs[o.id]["smallcin"]
+                                N.call("sf_conv3x3_smallcin_gn", lat.data_ptr(), nf, ish.h, ish.w, ish.c,
+                                       prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), e[1],
+                                       part_ptr(e, sl[0]), st)
+                            else:
+                                N.call("sf_conv3x3_smallcin", lat.data_ptr(), nf, ish.h, ish.w, ish.c,
+                                       prm["wt32"].data_ptr(), prm["bias"].data_ptr(), osh.c, Y.view(), st)
                         elif last and eps_out:
                             # out_conv: fp32 network output (per-tap projection + shifted sum for tiny cout)
                             out = self.srows(tail, sl[0])
@@ -1232,6 +1246,8 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     for n in graph.nodes.values():
         if n.kind is OpKind.CONV2D and graph.nodes[n.id].inputs[0] != "x":
             dw.p[n.id] = {"w": None}
+        elif n.kind is OpKind.CONV2D:
+            dw.p[n.id] = {"wt32": None}    # in_conv: the small-channel kernel
         elif n.kind is OpKind.LINEAR:
             dw.p[n.id] = {"w32": torch.empty(1, 1, device="meta"), "bias": torch.empty(1, device="meta")}
         elif n.param_ref:

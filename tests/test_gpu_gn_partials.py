@@ -132,7 +132,7 @@ def test_plan_uses_conv_partials_and_matches_stats_path():
     sched = StepSchedule([0, 1, 2], 3)
     d1 = Denoiser(cfg, ExecConfig(gn_from_conv=True))
     a = d1.run(x0, sched)
-    assert len(d1.plan.gn_feed) == 9 and len(d1.plan.gn_meta) == 15   # + 3 downsamples, 3 concats
+    assert len(d1.plan.gn_feed) == 9 and len(d1.plan.gn_meta) == 16   # + 3 downsamples, 3 concats, in_conv
     d2 = Denoiser(cfg, ExecConfig(gn_from_conv=False), device_weights=d1.model.dw)
     b = d2.run(x0, sched)
     assert not d2.plan.gn_feed and not d2.plan.gn_meta
@@ -245,3 +245,28 @@ def test_out_norm_projection_in_plan(monkeypatch):
     b = d2.run(x0, sched)
     assert d1.launches[d1._key(sched, False)] < d2.launches[d2._key(sched, False)]
     assert np.abs(a - b).max() / np.abs(b).max() < 1e-4
+
+
+@pytest.mark.parametrize("F_,H,W,cout,splits", [(3, 72, 128, 320, 94), (2, 16, 16, 64, 3), (5, 9, 12, 128, 7)])
+def test_in_conv_partials(F_, H, W, cout, splits):
+    """sf_conv3x3_smallcin_gn: the same in_conv output as sf_conv3x3_smallcin, bit for bit, plus per-(frame,
+    split, channel) sums of the stored values (frames whose pixel count is not a multiple of 16 included)."""
+    torch.manual_seed(10)
+    st = torch.cuda.current_stream().cuda_stream
+    cin = 4
+    x = torch.randn(F_ * H * W, cin, device=dev)
+    w = torch.randn(9, cin, cout, device=dev) * 0.3
+    b = torch.randn(cout, device=dev)
+    y0 = torch.empty(F_ * H * W, cout, dtype=torch.bfloat16, device=dev)
+    y1 = torch.empty_like(y0)
+    part = torch.full((F_, splits, cout, 2), float("nan"), device=dev)
+    N.call("sf_conv3x3_smallcin", x.data_ptr(), F_, H, W, cin, w.data_ptr(), b.data_ptr(), cout,
+           Rows(y0, 0, H * W).view(), st)
+    N.call("sf_conv3x3_smallcin_gn", x.data_ptr(), F_, H, W, cin, w.data_ptr(), b.data_ptr(), cout,
+           Rows(y1, 0, H * W).view(), splits, part.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    assert not torch.isnan(part).any()
+    yd = y1.double().view(F_, H * W, cout)
+    assert torch.allclose(part.double().sum(1)[..., 0], yd.sum(1), rtol=1e-5, atol=1e-3)
+    assert torch.allclose(part.double().sum(1)[..., 1], (yd * yd).sum(1), rtol=1e-5, atol=1e-3)
