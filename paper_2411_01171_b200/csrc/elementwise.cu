@@ -1483,14 +1483,29 @@ __global__ void __launch_bounds__(SCM_THREADS) conv_smallcin_mma_kernel(const fl
         }
         if (part != nullptr) {
           // the stored values' sums: lane owns columns 2 lane, 2 lane + 1 of the chunk, rows in order
-          float2 a = sP[n0 + 2 * lane], b = sP[n0 + 2 * lane + 1];
-          for (int r = 0; r < nvalid; ++r) {
-            const float2 v2 = __bfloat1622float2(*reinterpret_cast<const bf162*>(sO + r * L::LDO + 2 * lane));
-            a.x += v2.x;
-            a.y = fmaf(v2.x, v2.x, a.y);
-            b.x += v2.y;
-            b.y = fmaf(v2.y, v2.y, b.y);
+          // four independent row chains (rows r = 4i + u), combined (0+1)+(2+3) per tile
+          float4 acc4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int r4 = 0; r4 < 16; r4 += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (r4 + u < nvalid) {
+                const float2 v2 =
+                    __bfloat1622float2(*reinterpret_cast<const bf162*>(sO + (r4 + u) * L::LDO + 2 * lane));
+                acc4[u].x += v2.x;
+                acc4[u].y = fmaf(v2.x, v2.x, acc4[u].y);
+                acc4[u].z += v2.y;
+                acc4[u].w = fmaf(v2.y, v2.y, acc4[u].w);
+              }
+            }
           }
+          float2 a = sP[n0 + 2 * lane], b = sP[n0 + 2 * lane + 1];
+          a.x += (acc4[0].x + acc4[1].x) + (acc4[2].x + acc4[3].x);
+          a.y += (acc4[0].y + acc4[1].y) + (acc4[2].y + acc4[3].y);
+          b.x += (acc4[0].z + acc4[1].z) + (acc4[2].z + acc4[3].z);
+          b.y += (acc4[0].w + acc4[1].w) + (acc4[2].w + acc4[3].w);
           sP[n0 + 2 * lane] = a;
           sP[n0 + 2 * lane + 1] = b;
         }
