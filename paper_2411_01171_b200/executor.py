@@ -209,7 +209,8 @@ class Plan:
         self.gn_meta: dict[str, int] = {}
         f0, f1 = self._frames()
         nf = f1 - f0
-        sms = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148
+        sms = (torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+               if torch.cuda.is_available() else 148)
         down_of_input = {grp.head_input: grp.ops[0].id for grp in self.grouped.groups
                          if len(grp.ops) == 1 and grp.ops[0].kind is OpKind.DOWNSAMPLE2X}
         up_by_tail = {grp.tail: grp.ops[0].id for grp in self.grouped.groups
