@@ -299,7 +299,14 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
         rec, d2, key = measure(ecfg)
         out["equal_peak_plan"] = dict(
             plan=f"budget slicing at the per-frame plan's scratch ({budget / 2**20:.1f} MiB), 1 slice stream",
-            **rec, slices=slice_summary(d2.plan), gpu_launches_per_run=d2.launches[key])
+            **rec, slices=slice_summary(d2.plan), gpu_launches_per_run=d2.launches[key], variants=[])
+        del d2
+        # the same total scratch split over two slice streams (half the budget per copy)
+        ecfg = ExecConfig(gemm_backend=args.backend, scratch_budget=budget // 2, slice_streams=2)
+        rec, d2, key = measure(ecfg)
+        out["equal_peak_plan"]["variants"].append(dict(
+            plan=f"budget slicing at half the per-frame plan's scratch per copy, 2 slice streams",
+            **{k: rec[k] for k in ("value", "ms_per_step", "peak_hbm_bytes", "scratch_bytes")}))
         del d2
     return out
 
