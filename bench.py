@@ -305,7 +305,7 @@ def north_star_plan(args, cfg, den, sched, x0) -> dict:
         ecfg = ExecConfig(gemm_backend=args.backend, scratch_budget=budget // 2, slice_streams=2)
         rec, d2, key = measure(ecfg)
         out["equal_peak_plan"]["variants"].append(dict(
-            plan=f"budget slicing at half the per-frame plan's scratch per copy, 2 slice streams",
+            plan="budget slicing at half the per-frame plan's scratch per copy, 2 slice streams",
             **{k: rec[k] for k in ("value", "ms_per_step", "peak_hbm_bytes", "scratch_bytes")}))
         del d2
     return out
