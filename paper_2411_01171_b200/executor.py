@@ -280,8 +280,10 @@ class Plan:
             for _, v, _ in roles:
                 start[v] = min(start.get(v, op_pos[op_id]), op_pos[op_id])
         self._gn_slot_of, self._gn_slot_elems, free_after = {}, [], []
+        self.gn_intervals: dict[str, tuple[int, int]] = {}   # value -> (first producer, consumer) positions
         for v in sorted(start, key=lambda u: start[u]):
             a, b = start[v], cons_pos[v]
+            self.gn_intervals[v] = (a, b)
             elems = nf * self.gn_meta[v] * self.shapes[v].c * 2
             for k, fa in enumerate(free_after):
                 if fa < a:
@@ -1272,7 +1274,9 @@ def plan_memory(graph: Graph, grouped: GroupedGraph, cfg: ExecConfig | None = No
     out = {"arena_bytes": plan.arena_bytes, "buffers": len(plan.buffers), "ledger": led,
            "ledger_peak_bytes": led.peak_bytes,
            "gn_partial_bytes": 4 * sum(getattr(plan, "_gn_slot_elems", [])), "gn_from_conv": len(plan.gn_feed),
-           "gn_handed_over": len(plan.gn_meta)}
+           "gn_handed_over": len(plan.gn_meta),
+           "gn_slots": {v: (getattr(plan, "_gn_slot_of", {}).get(v), *plan.gn_intervals[v])
+                        for v in getattr(plan, "gn_intervals", {})}}
     if plan.cfg.world > 1:
         from .parallel import exchange_schedule
         ex = exchange_schedule(plan)

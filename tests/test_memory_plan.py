@@ -47,3 +47,28 @@ def test_groupnorm_statistics_hand_over(name):
     assert 0 < m["gn_partial_bytes"] < max(0.06 * m["arena_bytes"], 1 << 20)
     off = plan_memory(g, gg, ExecConfig(gn_from_conv=False))
     assert off["gn_handed_over"] == 0 and off["gn_partial_bytes"] == 0
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_groupnorm_partial_slots_do_not_overlap(name):
+    """Partial buffers are shared only between hand-overs whose [first producer, consumer] schedule
+    intervals are disjoint (a concat's lives from the down path's downsample to the up block)."""
+    import bench
+    from paper_2411_01171_b200.executor import ExecConfig, plan_memory
+    from paper_2411_01171_b200.grouping import group_operators
+    from paper_2411_01171_b200.slicer import default_temporal_config
+    from paper_2411_01171_b200.unet import UNetConfig, build_toy_unet
+    cfg = UNetConfig(**bench.CONFIGS[name])
+    g, _ = build_toy_unet(cfg)
+    gg = group_operators(g, cfg.frames, default_temporal_config(cfg.height, cfg.width))
+    slots = plan_memory(g, gg, ExecConfig())["gn_slots"]
+    assert len(slots) >= 15
+    by_slot = {}
+    for v, (k, a, b) in slots.items():
+        assert a < b, v
+        by_slot.setdefault(k, []).append((a, b, v))
+    for k, iv in by_slot.items():
+        iv.sort()
+        for (a0, b0, v0), (a1, b1, v1) in zip(iv, iv[1:]):
+            assert b0 < a1, f"slot {k}: {v0} [{a0}, {b0}] overlaps {v1} [{a1}, {b1}]"
+    assert len(by_slot) >= 2     # the concats' long-lived partials need slots of their own
