@@ -474,7 +474,10 @@ def run_ours(args, world, rank, local):
                                  f"{K - len(sched.key_steps)} tail evaluations), one CUDA graph",
                    "schedule": {"key_steps": sched.key_steps, "gamma": gamma, "decision_margin": sched.margin},
                    "l2": "activations exceed L2 (no flush needed)" if args.config != "c1" else "toy fits L2",
-                   "parallelism": f"frame/pixel sharded x{world} (NCCL all-to-all)" if world > 1 else "single"},
+                   "parallelism": (f"frame/pixel sharded x{world} ("
+                                   + ("gloo all-to-all, every rank on one GPU: a plumbing test"
+                                      if os.environ.get("SF_BENCH_ONE_GPU") == "1" else "NCCL all-to-all") + ")")
+                                  if world > 1 else "single"},
         "peak_hbm_bytes": int(peak_hbm), "arena_bytes": den.plan.arena_bytes,
         "scratch_bytes": den.plan.scratch_bytes,
         "frames_per_s": round(value / K * cfg.frames, 3),
