@@ -202,9 +202,10 @@ class Plan:
             conv's GEMM epilogue sums the values it stores (``gn_feed``: conv id -> value);
           * down_blocks.i+1.res.norm1 reads the downsample's output, and up_blocks.i.res.norm1 reads
             concat(skip, upsample(x)) (unet.py:221-244): the downsample kernel sums its output and
-            the skip it reads, the upsample kernel the copies it writes (``gn_roles``: op id ->
+            the skip it reads, the upsample kernel the copies it writes; down_blocks.0.res.norm1 reads
+            the in_conv output, which the tensor-core in_conv kernel sums (``gn_roles``: op id ->
             [(role, value, channel offset)]).
-        Each value gets [frames][splits][C] float2 partials; ``gn_meta``: value -> splits."""
+        Each value gets [frames][splits][C] float2 partials; ``gn_meta``: value -> splits.
         self.gn_roles: dict[str, list] = {}
         self.gn_meta: dict[str, int] = {}
         f0, f1 = self._frames()
@@ -274,7 +275,10 @@ class Plan:
         for gi, grp in enumerate(self.grouped.groups):
             for o in grp.ops:
                 op_pos[o.id] = spos.get(("group", gi), -1)
-        cons_pos = {grp.head_input: spos[("group", gi)] for gi, grp in enumerate(self.grouped.groups)}
+        cons_pos: dict[str, int] = {}   # the GroupNorm group that finalizes each value (latest, to be safe)
+        for gi, grp in enumerate(self.grouped.groups):
+            if grp.ops[0].kind is OpKind.GROUP_NORM:
+                cons_pos[grp.head_input] = max(cons_pos.get(grp.head_input, -1), spos[("group", gi)])
         start = {v: op_pos[c] for c, v in self.gn_feed.items()}
         for op_id, roles in self.gn_roles.items():
             for _, v, _ in roles:
