@@ -205,7 +205,7 @@ class Plan:
             the skip it reads, the upsample kernel the copies it writes; down_blocks.0.res.norm1 reads
             the in_conv output, which the tensor-core in_conv kernel sums (``gn_roles``: op id ->
             [(role, value, channel offset)]).
-        Each value gets [frames][splits][C] float2 partials; ``gn_meta``: value -> splits.
+        Each value gets [frames][splits][C] float2 partials; ``gn_meta``: value -> splits."""
         self.gn_roles: dict[str, list] = {}
         self.gn_meta: dict[str, int] = {}
         f0, f1 = self._frames()
