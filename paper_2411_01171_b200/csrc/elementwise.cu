@@ -1527,8 +1527,9 @@ static sf_status conv_smallcin_mma_launch(const float* x, int frames, int H, int
                                           const float* bias, int cout, sf_view_t y, int splits, void* part,
                                           cudaStream_t st) {
   using L = ScmLayout<KP>;
+  // the per-warp sums (sP) only when partials are requested: without them three blocks fit per SM
   const size_t smem = (size_t)(L::A_ELEMS + L::O_ELEMS + cout * L::LDA) * sizeof(bf16) + cout * sizeof(float) +
-                      (size_t)SCM_WARPS * cout * sizeof(float2);
+                      (part ? (size_t)SCM_WARPS * cout * sizeof(float2) : 0);
   static size_t cfg = 0;
   if (smem > 48 * 1024 && smem > cfg) {
     cudaFuncSetAttribute(conv_smallcin_mma_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
