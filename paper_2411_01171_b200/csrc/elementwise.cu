@@ -925,9 +925,8 @@ __device__ __forceinline__ unsigned pack_bf2(float a, float b) {
 // it with the resident W (bf16 [48][C]) on mma.sync m16n8k16; fp32 out.  Each element is
 // transformed once (the per-tap projection reads every pixel once, unlike a 3x3 implicit GEMM).
 // ---------------------------------------------------------------------------
-constexpr int GP_WARPS = 8, GP_NP = 48;    // output columns padded to 6 n-tiles of 8
-constexpr int GP_R = 32;                     // rows per warp tile: two m16 MMA tiles share each B fragment
-constexpr int GP_LDA = 64 + 8;               // one 64-channel K chunk per A buffer, +16 B per row
+constexpr int GP_WARPS = 16, GP_NP = 48;   // output columns padded to 6 n-tiles of 8
+constexpr int GP_LDA = 64 + 8;              // one 64-channel K chunk per A buffer, +16 B per row
 __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
     sf_view_t x, int frames, int n_inner, int C, int groups, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta, int act,
@@ -936,8 +935,8 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
   extern __shared__ __align__(16) uint8_t gp_raw[];
   const int LD = C + 8;   // +16 B per row: conflict-free ldmatrix
   bf16* sW = reinterpret_cast<bf16*>(gp_raw);                        // [GP_NP][LD]
-  bf16* sA = sW + GP_NP * LD;                                        // [GP_WARPS][2][GP_R][GP_LDA]
-  float2* sT = reinterpret_cast<float2*>(sA + GP_WARPS * 2 * GP_R * GP_LDA);   // [GP_WARPS][2][C] (scale, shift)
+  bf16* sA = sW + GP_NP * LD;                                        // [GP_WARPS][2][16][GP_LDA]
+  float2* sT = reinterpret_cast<float2*>(sA + GP_WARPS * 2 * 16 * GP_LDA);   // [GP_WARPS][2][C] (scale, shift)
   for (int i = threadIdx.x; i < GP_NP * (C / 8); i += blockDim.x) {
     const int n = i / (C / 8), v = i % (C / 8);
     *reinterpret_cast<bf16x8*>(sW + n * LD + v * 8) =
@@ -945,23 +944,22 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  bf16* abuf = sA + warp * 2 * GP_R * GP_LDA;
+  bf16* abuf = sA + warp * 2 * 16 * GP_LDA;
   float2* tab = sT + warp * 2 * C;
   const int cg = C / groups, nk = C / 64;
   const int64_t rows = (int64_t)frames * n_inner;
-  // blocks take contiguous shares of the GP_R-row tiles (a block touches one or two frames)
-  const int64_t ntiles = (rows + GP_R - 1) / GP_R;
+  // blocks take contiguous shares of the 16-row tiles (a block touches one or two frames)
+  const int64_t ntiles = (rows + 15) / 16;
   const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
-  // a K chunk = GP_R rows x 8 vectors: lane -> rows lane / 8 + 4 u, vector lane % 8
-  constexpr int U = GP_R / 4;
+  // a K chunk = 16 rows x 8 vectors: lane -> rows lane / 8 + {0, 4, 8, 12}, vector lane % 8
   const int lr = lane >> 3, lv = lane & 7;
   int fa = -1, fb = -1;
   for (int64_t t = t0 + warp; t < t1; t += GP_WARPS) {
-    const int64_t r0 = t * GP_R;
-    const int f0 = (int)(r0 / n_inner), f1 = (int)(min(r0 + GP_R - 1, rows - 1) / n_inner);
+    const int64_t r0 = t * 16;
+    const int f0 = (int)(r0 / n_inner), f1 = (int)(min(r0 + 15, rows - 1) / n_inner);
     if (f0 != fa || f1 != fb) {
       // y = x * ss + bb, ss = rstd * gamma, bb = beta - mean * ss (gn_apply_kernel's arithmetic), per
-      // channel of the tile's first / last frame (a tile spans at most two frames: n_inner >= GP_R)
+      // channel of the tile's first / last frame (a 16-row tile spans at most two frames: n_inner >= 16)
       for (int c = lane; c < C; c += 32) {
         const int g = c / cg;
         const float s0 = __ldg(rstd + f0 * groups + g) * __ldg(gamma + c);
@@ -974,34 +972,32 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
       __syncwarp();
     }
     // row -> (frame, local row) without divisions: rows from `split` on belong to frame f0 + 1
-    const int split = (int)min((int64_t)GP_R, (int64_t)(f0 + 1) * n_inner - r0);
+    const int split = (int)min((int64_t)16, (int64_t)(f0 + 1) * n_inner - r0);
     const int64_t base0 = r0 - (int64_t)f0 * n_inner;
-    const int nvalid = (int)min((int64_t)GP_R, rows - r0);
-    const bf16* src[U];
+    const int nvalid = (int)min((int64_t)16, rows - r0);
+    const bf16* src[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int rr = lr + 4 * u;
       const bool second = rr >= split;
       src[u] = rr < nvalid ? row_ptr<const bf16>(x, f0 + (second ? 1 : 0), second ? rr - split : base0 + rr) + lv * 8
                            : nullptr;
     }
-    bf16x8 cur[U], nxt[U];
+    bf16x8 cur[4], nxt[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < 4; ++u)
       if (src[u]) cur[u] = *reinterpret_cast<const bf16x8*>(src[u]);
-    float acc[2][GP_NP / 8][4];
+    float acc[GP_NP / 8][4];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int j = 0; j < GP_NP / 8; ++j) acc[m][j][0] = acc[m][j][1] = acc[m][j][2] = acc[m][j][3] = 0.f;
+    for (int j = 0; j < GP_NP / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     for (int kc = 0; kc < nk; ++kc) {
       if (kc + 1 < nk) {   // the next chunk's loads fly while this one is transformed and multiplied
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < 4; ++u)
           if (src[u]) nxt[u] = *reinterpret_cast<const bf16x8*>(src[u] + (kc + 1) * 64);
       }
-      bf16* a = abuf + (kc & 1) * GP_R * GP_LDA;
-      // this lane's 8 channels' (ss, bb) once per chunk (its rows share them unless the tile
+      bf16* a = abuf + (kc & 1) * 16 * GP_LDA;
+      // this lane's 8 channels' (ss, bb) once per chunk (its 4 rows share them unless the tile
       // straddles two frames)
       float4 sbA[4];
       {
@@ -1010,7 +1006,7 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
         for (int q = 0; q < 4; ++q) sbA[q] = tv[q];
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int rr = lr + 4 * u;
         float fv[8];
         if (src[u]) {
@@ -1040,34 +1036,27 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
       __syncwarp();
 #pragma unroll
       for (int kk = 0; kk < 64; kk += 16) {
-        unsigned af[2][4];
-#pragma unroll
-        for (int m = 0; m < 2; ++m) tq_ldsm_x4(af[m], a + (m * 16 + (lane & 15)) * GP_LDA + kk + (lane >> 4) * 8);
+        unsigned af[4];
+        tq_ldsm_x4(af, a + (lane & 15) * GP_LDA + kk + (lane >> 4) * 8);
 #pragma unroll
         for (int j = 0; j < GP_NP / 8; j += 2) {
           unsigned b[4];
           const int nrow = j * 8 + (lane & 7) + ((lane >> 4) << 3);
           tq_ldsm_x4(b, sW + nrow * LD + kc * 64 + kk + ((lane >> 3) & 1) * 8);
-#pragma unroll
-          for (int m = 0; m < 2; ++m) {
-            tq_mma(acc[m][j], af[m], b[0], b[1]);
-            tq_mma(acc[m][j + 1], af[m], b[2], b[3]);
-          }
+          tq_mma(acc[j], af, b[0], b[1]);
+          tq_mma(acc[j + 1], af, b[2], b[3]);
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
     }
+    const int64_t ra = r0 + (lane >> 2), rb = ra + 8;
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int64_t ra = r0 + m * 16 + (lane >> 2), rb = ra + 8;
-#pragma unroll
-      for (int j = 0; j < GP_NP / 8; ++j) {
-        const int c = j * 8 + (lane & 3) * 2;
-        if (c < N) {   // N even: the pair (c, c + 1) is in range together
-          if (ra < rows) *reinterpret_cast<float2*>(out + ra * ldo + c) = make_float2(acc[m][j][0], acc[m][j][1]);
-          if (rb < rows) *reinterpret_cast<float2*>(out + rb * ldo + c) = make_float2(acc[m][j][2], acc[m][j][3]);
-        }
+    for (int j = 0; j < GP_NP / 8; ++j) {
+      const int c = j * 8 + (lane & 3) * 2;
+      if (c < N) {   // N even: the pair (c, c + 1) is in range together
+        if (ra < rows) *reinterpret_cast<float2*>(out + ra * ldo + c) = make_float2(acc[j][0], acc[j][1]);
+        if (rb < rows) *reinterpret_cast<float2*>(out + rb * ldo + c) = make_float2(acc[j][2], acc[j][3]);
       }
     }
     __syncwarp();   // the A buffers are rewritten by the next tile
@@ -1077,7 +1066,7 @@ __global__ void __launch_bounds__(GP_WARPS * 32) gn_project_kernel(
 sf_status gn_project_launch(sf_view_t x, int frames, int n_inner, int C, int groups, const float* mean,
                             const float* rstd, const float* gamma, const float* beta, int act, const void* w, int N,
                             float* out, int64_t ldo, cudaStream_t st) {
-  const size_t smem = ((size_t)GP_NP * (C + 8) + (size_t)GP_WARPS * 2 * GP_R * GP_LDA) * sizeof(bf16) +
+  const size_t smem = ((size_t)GP_NP * (C + 8) + (size_t)GP_WARPS * 2 * 16 * GP_LDA) * sizeof(bf16) +
                       (size_t)GP_WARPS * 2 * C * sizeof(float2);
   static size_t set = 48 * 1024;
   if (smem > set) {
@@ -1089,7 +1078,7 @@ sf_status gn_project_launch(sf_view_t x, int frames, int n_inner, int C, int gro
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_project_kernel, GP_WARPS * 32, smem);
     if (occ < 1) occ = 1;
   }
-  const int64_t tiles = ((int64_t)frames * n_inner + GP_R - 1) / GP_R;
+  const int64_t tiles = ((int64_t)frames * n_inner + 15) / 16;
   int64_t grid = (int64_t)num_sms() * occ;
   const int64_t most = (tiles + GP_WARPS - 1) / GP_WARPS;
   if (grid > most) grid = most;
@@ -1887,8 +1876,8 @@ sf_status sf_upsample2x(sf_view_t x, sf_view_t y, int32_t frames, int32_t H, int
 sf_status sf_group_norm_project(sf_view_t x, int32_t frames, int32_t n_inner, int32_t C, int32_t groups,
                                 const float* mean, const float* rstd, const float* gamma, const float* beta,
                                 int32_t act, const void* w, int32_t N, float* out, int64_t ldo, void* stream) {
-  SF_CHECK_ARG(frames >= 1 && n_inner >= GP_R && C >= 64 && C % 64 == 0 && C <= 384, SF_ERR_SHAPE,
-               "C must be a multiple of 64 in [64, 384] (shared memory), frames of >= 32 rows");
+  SF_CHECK_ARG(frames >= 1 && n_inner >= 16 && C >= 64 && C % 64 == 0 && C <= 384, SF_ERR_SHAPE,
+               "C must be a multiple of 64 in [64, 384] (shared memory), frames of >= 16 rows");
   SF_CHECK_ARG(groups >= 1 && C % groups == 0, SF_ERR_PARAM, "groups must divide channels");
   SF_CHECK_ARG(N >= 2 && N <= GP_NP && N % 2 == 0 && ldo >= N && ldo % 2 == 0, SF_ERR_SHAPE,
                "N must be even, <= 48, and fit the output rows");

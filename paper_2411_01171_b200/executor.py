@@ -830,7 +830,7 @@ class Plan:
             (go, gsrc, gdst, gsh, _, gact, _), (co, csrc, _, csh, cosh, cact, clast) = a_, b_
             if (go.kind is OpKind.GROUP_NORM and co.kind is OpKind.CONV2D and csrc == gdst and clast and eps_tail
                     and "w_taps" in self.dw.p.get(co.id, {}) and not cact and tail not in self.epilogue_of
-                    and gsh.c % 64 == 0 and gsh.c <= 384 and 9 * cosh.c <= 48 and gsh.h * gsh.w >= 32
+                    and gsh.c % 64 == 0 and gsh.c <= 384 and 9 * cosh.c <= 48 and gsh.h * gsh.w >= 16
                     and os.environ.get("SF_GN_PROJECT") != "0"):
                 gn_project[co.id] = (go, gsrc, gact)
                 pf_specs.pop(gdst, None)
